@@ -1,0 +1,160 @@
+/* gcmc_b200 — B200-native grand-canonical Monte Carlo per-move energy path.
+ *
+ * Plain C ABI (no CUDA or torch types). One opaque handle = one Markov chain
+ * on one device; host buffers are copied, the device owns the state. Every
+ * call returns gcmc_status; gcmc_last_error() gives a thread-local message
+ * whose text matches the exception the reference would have thrown.
+ *
+ * Each entry point replaces a reference interface (paths relative to
+ * /root/reference/proj/include/gcmc/):
+ *
+ *   gcmc_create / gcmc_destroy      make_strategy + strategy ctor            engine.hpp:189-202,
+ *                                                                            microcell_grid.hpp:140-156,
+ *                                                                            cell_grid.hpp:48-68
+ *   gcmc_upload_positions           ParticleStore(std::vector<Vec3>)         particles.hpp:19
+ *   gcmc_download_positions         ParticleStore::positions()               particles.hpp:26
+ *   gcmc_build                      NeighborStrategy::build()                strategy.hpp:34
+ *   gcmc_delta_displace/insert/     NeighborStrategy::delta_*                strategy.hpp:36-38
+ *     delete, gcmc_delta_batch
+ *   gcmc_commit_displace/insert/    NeighborStrategy::commit_*               strategy.hpp:40-42
+ *     delete
+ *   gcmc_rebuild_check              NeighborStrategy::rebuild_check()        strategy.hpp:46
+ *   gcmc_peak_occupancy             NeighborStrategy::peak_cell_occupancy()  strategy.hpp:49
+ *   gcmc_download_grid              occupancy_view() / slots_view()          microcell_grid.hpp:167-168,
+ *                                                                            cell_grid.hpp:78-79
+ *   gcmc_total_energy               total_energy()                           engine.hpp:74-94
+ *   gcmc_set/get_rng_state          RngStream engine state                   rng.hpp:47-77
+ *   gcmc_set/get_state              SystemState / RunStatistics / step_      engine.hpp:112-140, 244-252
+ *   gcmc_run_moves                  Simulation::step() x n  (run_to loop)    engine.hpp:293-325
+ *   gcmc_random_initial_configuration  random_initial_configuration()        init_config.hpp:19-64
+ */
+#ifndef GCMC_B200_H
+#define GCMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gcmc_status {
+  GCMC_OK = 0,
+  GCMC_INVALID_PID = 1,   /* std::out_of_range ("...: invalid particle id")          */
+  GCMC_CELL_OVERFLOW = 2, /* std::runtime_error ("...: cell C exceeds capacity K...") */
+  GCMC_NOT_FOUND = 3,     /* std::runtime_error ("...not found in cell C")           */
+  GCMC_OVERLAP = 4,       /* std::runtime_error ("total_energy: particles i and j overlap") */
+  GCMC_CUDA = 5,          /* CUDA runtime failure                                     */
+  GCMC_ARG = 6,           /* std::invalid_argument / config error                     */
+  GCMC_STATE = 7          /* call not valid in the current state                      */
+} gcmc_status;
+
+/* Strategy enum values match gcmc::Strategy (config.hpp:16). */
+enum { GCMC_ALL_PAIRS = 0, GCMC_CELL_LIST = 1, GCMC_MICROCELL = 2 };
+
+/* RunConfig subset the per-move path needs (config.hpp:42-64). */
+typedef struct gcmc_params {
+  double box_length;
+  double epsilon, sigma, r_cut;
+  double temperature, chemical_potential, lambda;
+  double displace_percent, max_displacement;
+  uint64_t equilibration_steps, sampling_interval;
+  int32_t strategy;
+  int32_t cell_capacity;      /* 0 = default_cell_capacity() (cell_grid.hpp:36-38) */
+  int32_t microcell_capacity; /* 0 = 5 (microcell_grid.hpp:149) */
+  int32_t tail_corrections;
+  uint64_t max_particles;     /* store capacity; 0 = automatic */
+  int32_t cluster_ctas;       /* engine CTAs per chain (0 = automatic) */
+  int32_t warps_per_cta;      /* engine evaluator warps per CTA (0 = automatic) */
+} gcmc_params;
+
+/* SystemState + RunStatistics + step counter (engine.hpp:112-140, 436). */
+typedef struct gcmc_state {
+  uint64_t step;
+  uint64_t n;
+  double energy, virial;
+  uint64_t attempted[3], accepted[3]; /* index = MoveKind: displace, insert, remove */
+  uint64_t samples;
+  double sum_u, sum_p, sum_n, sum_n2;
+  int32_t peak_occupancy;
+  int32_t pad;
+} gcmc_state;
+
+/* One MoveOutcome (engine.hpp:104-110) plus N after the move. */
+typedef struct gcmc_trace_rec {
+  int32_t kind; /* 0 displace, 1 insert, 2 remove */
+  int32_t accepted;
+  double delta_u, delta_w, acceptance_prob;
+  uint64_t n_after;
+} gcmc_trace_rec;
+
+typedef struct gcmc_run_result {
+  gcmc_state state;   /* after the run */
+  uint64_t moves;     /* moves executed by this call */
+  uint64_t rounds;    /* speculative evaluation rounds the device used */
+  double device_ms;   /* device time of the move loop (CUDA events) */
+  double gen_ms;      /* device time of proposal generation */
+} gcmc_run_result;
+
+typedef struct gcmc_dev gcmc_dev;
+
+const char* gcmc_last_error(void);
+const char* gcmc_version(void);
+
+gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out);
+gcmc_status gcmc_destroy(gcmc_dev* h);
+
+/* Positions are AoS xyz doubles (Vec3, vec3.hpp:7-27). Upload replaces the
+ * store and rebuilds the grid (the strategy ctor builds immediately). */
+gcmc_status gcmc_upload_positions(gcmc_dev* h, const double* xyz, uint64_t n);
+gcmc_status gcmc_download_positions(gcmc_dev* h, double* xyz, uint64_t capacity, uint64_t* n);
+gcmc_status gcmc_build(gcmc_dev* h);
+
+/* Grid geometry: cells per axis, slots per cell, total cells. */
+gcmc_status gcmc_grid_info(gcmc_dev* h, int32_t* dims, int32_t* capacity, uint64_t* ncells);
+gcmc_status gcmc_download_grid(gcmc_dev* h, int32_t* occ, int32_t* slots);
+gcmc_status gcmc_rebuild_check(gcmc_dev* h, char* msg, size_t msg_cap, int32_t* clean);
+gcmc_status gcmc_peak_occupancy(gcmc_dev* h, int32_t* peak);
+
+gcmc_status gcmc_delta_displace(gcmc_dev* h, uint64_t pid, const double pos[3], double* du,
+                                double* dw);
+gcmc_status gcmc_delta_insert(gcmc_dev* h, const double pos[3], double* du, double* dw);
+gcmc_status gcmc_delta_delete(gcmc_dev* h, uint64_t pid, double* du, double* dw);
+/* n proposals against the same state: kinds[i] 0/1/2, pids[i], xyz[3i..3i+2]. */
+gcmc_status gcmc_delta_batch(gcmc_dev* h, uint64_t n, const int32_t* kinds, const uint64_t* pids,
+                             const double* xyz, double* du, double* dw);
+
+gcmc_status gcmc_commit_displace(gcmc_dev* h, uint64_t pid, const double pos[3]);
+gcmc_status gcmc_commit_insert(gcmc_dev* h, const double pos[3], uint64_t* pid);
+gcmc_status gcmc_commit_delete(gcmc_dev* h, uint64_t pid);
+
+gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w);
+
+/* std::mt19937_64 state in libstdc++ order: 312 words + position (_M_p),
+ * plus RngStream's draw counter. */
+gcmc_status gcmc_seed_rng(gcmc_dev* h, uint64_t seed);
+gcmc_status gcmc_set_rng_state(gcmc_dev* h, const uint64_t words[312], uint64_t index,
+                               uint64_t draws);
+gcmc_status gcmc_get_rng_state(gcmc_dev* h, uint64_t words[312], uint64_t* index,
+                               uint64_t* draws);
+
+gcmc_status gcmc_set_state(gcmc_dev* h, const gcmc_state* s); /* resume (n is ignored) */
+gcmc_status gcmc_get_state(gcmc_dev* h, gcmc_state* s);
+
+/* Runs n Simulation::step()s on the device: proposals from the device MT
+ * stream, exact speculative evaluation, on-device acceptance, commit and
+ * statistics. `trace` (host, nullable) receives one record per move. */
+gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace,
+                           gcmc_run_result* out);
+
+/* Host-side initial configuration (init_config.hpp:19-64) consuming the
+ * identical MT stream; returns the RNG state left for the MC stream. */
+gcmc_status gcmc_random_initial_configuration(uint64_t n, double box_length, double min_sep,
+                                              uint64_t seed, double* out_xyz,
+                                              uint64_t words[312], uint64_t* index,
+                                              uint64_t* draws);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCMC_B200_H */

@@ -1,0 +1,650 @@
+// C ABI of libgcmc_b200.so (declared in include/gcmc_b200.h). Host-side
+// plumbing only: argument checks with the reference's error wording, device
+// allocation, staging copies, and dispatch to the kernels in grid.cu,
+// delta.cu, energy.cu, gen.cu and engine.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace gcmcb;
+
+namespace gcmcb {
+
+thread_local std::string g_last_error;
+
+gcmc_status set_error(gcmc_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+gcmc_status cuda_error(cudaError_t e, const char* where) {
+  std::string m = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+  return set_error(GCMC_CUDA, m);
+}
+
+}  // namespace gcmcb
+
+namespace {
+
+#define CK(expr, where)                          \
+  do {                                           \
+    cudaError_t e_ = (expr);                     \
+    if (e_ != cudaSuccess) return cuda_error(e_, where); \
+  } while (0)
+
+Chain* H(gcmc_dev* h) { return reinterpret_cast<Chain*>(h); }
+
+gcmc_status invalid_pid(const Chain& c) {
+  return set_error(GCMC_INVALID_PID, strategy_name(c.grid.kind) + ": invalid particle id");
+}
+
+std::string g17(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.17g", v);
+  return buf;
+}
+
+// RunConfig::validate subset (config.hpp:69-87).
+gcmc_status validate(const gcmc_params& p) {
+  auto fail = [](const std::string& why) { return set_error(GCMC_ARG, "config: " + why); };
+  if (!(p.temperature > 0.0)) return fail("temperature must be > 0");
+  if (!(p.lambda > 0.0)) return fail("lambda must be > 0");
+  if (!(p.sigma > 0.0)) return fail("sigma must be > 0");
+  if (p.epsilon < 0.0) return fail("epsilon must be >= 0");
+  if (!(p.r_cut > 0.0)) return fail("r_cut must be > 0");
+  if (!(p.box_length > 0.0) || !std::isfinite(p.box_length)) return fail("box length must be > 0");
+  if (p.r_cut > p.box_length / 2.0)
+    return fail("r_cut must be <= box_length/2 for the minimum image convention (r_cut=" +
+                g17(p.r_cut) + ", L=" + g17(p.box_length) + ")");
+  if (p.displace_percent < 0.0 || p.displace_percent > 1.0)
+    return fail("displace_percent must lie in [0, 1]");
+  if (p.sampling_interval == 0) return fail("sampling_interval must be >= 1");
+  if (p.cell_capacity < 0) return fail("cell_capacity must be >= 1 (or 0 for automatic)");
+  if (p.microcell_capacity < 0) return fail("microcell_capacity must be >= 1");
+  if (p.max_displacement < 0.0) return fail("max_displacement must be >= 0");
+  if (p.strategy < GCMC_ALL_PAIRS || p.strategy > GCMC_MICROCELL) return fail("unknown strategy");
+  return GCMC_OK;
+}
+
+void sync_state_to_device(Chain& c) {
+  cudaMemcpyAsync(c.st, c.st_host, sizeof(ChainState), cudaMemcpyHostToDevice, c.stream);
+}
+
+gcmc_status pull_state(Chain& c) {
+  CK(cudaMemcpyAsync(c.st_host, c.st, sizeof(ChainState), cudaMemcpyDeviceToHost, c.stream),
+     "state");
+  CK(cudaStreamSynchronize(c.stream), "state");
+  return GCMC_OK;
+}
+
+gcmc_status ensure_batch(Chain& c, uint64_t n) {
+  if (n <= c.batch_cap) return GCMC_OK;
+  if (c.dscratch) cudaFree(c.dscratch);
+  if (c.iscratch) cudaFree(c.iscratch);
+  uint64_t cap = n < 1024 ? 1024 : n;
+  // doubles: du, dw, xyz(3) ; ints: kinds ; u64 pids -> stored in the double block
+  CK(cudaMalloc(&c.dscratch, cap * 7 * sizeof(double)), "alloc");
+  CK(cudaMalloc(&c.iscratch, cap * sizeof(int32_t) + 64), "alloc");
+  c.batch_cap = cap;
+  return GCMC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gcmc_last_error(void) { return g_last_error.c_str(); }
+const char* gcmc_version(void) { return "gcmc_b200 0.1 (sm_100a)"; }
+
+gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
+  if (!params || !out) return set_error(GCMC_ARG, "null argument");
+  *out = nullptr;
+  gcmc_status s = validate(*params);
+  if (s) return s;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev), "device count");
+  if (device < 0 || device >= ndev) return set_error(GCMC_ARG, "invalid device ordinal");
+  CK(cudaSetDevice(device), "set device");
+  auto* c = new Chain();
+  c->device = device;
+  c->params = *params;
+  const gcmc_params& P = c->params;
+  // Box / LJ constants (potential.hpp:17-27, box.hpp:47)
+  c->box.l = P.box_length;
+  c->box.inv_l = 1.0 / P.box_length;
+  c->box.eps = P.epsilon;
+  c->box.sigma = P.sigma;
+  c->box.sigma2 = P.sigma * P.sigma;
+  c->box.rc = P.r_cut;
+  c->box.rc2 = P.r_cut * P.r_cut;
+  c->box.four_eps = 4.0 * P.epsilon;
+  c->box.tf_eps = 24.0 * P.epsilon;
+  c->box.pad = 1e-9 * P.sigma;
+  c->box.inv_sigma = 1.0 / P.sigma;
+  // Grid geometry
+  Grid& g = c->grid;
+  g.kind = P.strategy;
+  if (g.kind == GCMC_MICROCELL) {  // microcell_grid.hpp:29-35, 149
+    const double cells = P.box_length / P.sigma;
+    const double whole = std::floor(cells);
+    const double frac = cells - whole;
+    if (frac < 1e-9) {
+      g.dims = (int)std::llround(whole);
+      g.last_w = 1.0;
+    } else {
+      g.dims = (int)whole + 1;
+      g.last_w = frac;
+    }
+    g.inv_cell = 1.0 / P.sigma;
+    g.cap = P.microcell_capacity > 0 ? P.microcell_capacity : 5;
+  } else if (g.kind == GCMC_CELL_LIST) {  // cell_grid.hpp:27-38
+    int t = (int)(P.box_length / P.r_cut);
+    while ((double)(t + 1) * P.r_cut <= P.box_length) ++t;
+    while (t > 1 && (double)t * P.r_cut > P.box_length) --t;
+    if (t < 3) t = 3;
+    g.dims = t;
+    g.inv_cell = 1.0 / (P.box_length / t);
+    g.cap = P.cell_capacity > 0 ? P.cell_capacity : (P.r_cut <= 4.0 * P.sigma ? 48 : 96);
+    g.last_w = 1.0;
+  }
+  if (g.cap > kMaxCap) {
+    delete c;
+    return set_error(GCMC_ARG, "cell capacity above the device limit of 128");
+  }
+  g.ncells = g.kind == GCMC_ALL_PAIRS ? 0 : (uint64_t)g.dims * g.dims * g.dims;
+  if ((uint64_t)g.cap * g.ncells >= (1ull << 31)) {
+    delete c;
+    return set_error(GCMC_ARG, "grid too large (cap * cells must be < 2^31)");
+  }
+  const double vol = P.box_length * P.box_length * P.box_length;
+  uint64_t capn = P.max_particles;
+  if (capn == 0) {
+    capn = (uint64_t)(vol * 1.5) + 1024;
+    if (g.kind != GCMC_ALL_PAIRS) capn = std::min<uint64_t>(capn, (uint64_t)g.cap * g.ncells + 1);
+  }
+  c->capn = capn;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device), "props");
+  c->sm_count = prop.multiProcessorCount;
+  c->engine_ctas = P.cluster_ctas > 0 ? P.cluster_ctas : 16;
+  // moves per CTA (the C ABI field keeps its name): 1, 2 or 4; K = ctas * moves <= 64
+  c->engine_warps = P.warps_per_cta > 0 ? P.warps_per_cta : 1;
+  if (c->engine_warps != 1 && c->engine_warps != 2) c->engine_warps = 4;
+  while (c->engine_ctas * c->engine_warps > 64) --c->engine_ctas;
+  if (c->engine_ctas > 16) c->engine_ctas = 16;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+  CK(cudaStreamCreateWithFlags(&c->gen_stream, cudaStreamNonBlocking), "stream");
+  for (auto& ev : c->ev) CK(cudaEventCreate(&ev), "event");
+  CK(cudaMalloc(&c->pos, capn * sizeof(double4)), "alloc pos");
+  CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
+  if (g.ncells) {
+    CK(cudaMalloc(&g.occ, g.ncells * sizeof(int32_t)), "alloc occ");
+    CK(cudaMalloc(&g.slots, g.ncells * g.cap * sizeof(int32_t)), "alloc slots");
+    CK(cudaMalloc(&g.cellpos, g.ncells * g.cap * sizeof(double4)), "alloc cellpos");
+    CK(cudaMemset(g.occ, 0, g.ncells * sizeof(int32_t)), "memset");
+    CK(cudaMemset(g.slots, 0xff, g.ncells * g.cap * sizeof(int32_t)), "memset");  // -1
+    CK(cudaMemset(g.cellpos, 0, g.ncells * g.cap * sizeof(double4)), "memset");
+  }
+  CK(cudaMalloc(&c->st, sizeof(ChainState)), "alloc state");
+  CK(cudaMallocHost(&c->st_host, sizeof(ChainState)), "alloc state");
+  std::memset(c->st_host, 0, sizeof(ChainState));
+  CK(cudaMalloc(&c->mt, 314 * sizeof(uint64_t)), "alloc rng");
+  if ((s = ensure_batch(*c, 1024))) return s;
+  sync_state_to_device(*c);
+  *out = reinterpret_cast<gcmc_dev*>(c);
+  return gcmc_seed_rng(*out, 1);  // RunConfig::seed default (config.hpp:56)
+}
+
+gcmc_status gcmc_destroy(gcmc_dev* h) {
+  if (!h) return GCMC_OK;
+  Chain* c = H(h);
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->pos);
+  cudaFree(c->grid.occ);
+  cudaFree(c->grid.slots);
+  cudaFree(c->grid.cellpos);
+  cudaFree(c->st);
+  cudaFreeHost(c->st_host);
+  cudaFree(c->mt);
+  cudaFree(c->props);
+  cudaFree(c->trace);
+  cudaFree(c->dscratch);
+  cudaFree(c->iscratch);
+  cudaFree(c->egrid);
+  for (auto& ev : c->ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->gen_stream);
+  delete c;
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_upload_positions(gcmc_dev* h, const double* xyz, uint64_t n) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (n > c.capn) return set_error(GCMC_ARG, "more particles than the store capacity");
+  if (n && !xyz) return set_error(GCMC_ARG, "null positions");
+  std::vector<double4> tmp(n);
+  for (uint64_t i = 0; i < n; ++i) tmp[i] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 0.0);
+  if (n) CK(cudaMemcpyAsync(c.pos, tmp.data(), n * sizeof(double4), cudaMemcpyHostToDevice, c.stream), "upload");
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  c.st_host->n = n;
+  c.st_host->peak = 0;
+  c.st_host->error = 0;
+  sync_state_to_device(c);
+  return grid_build(c);
+}
+
+gcmc_status gcmc_download_positions(gcmc_dev* h, double* xyz, uint64_t capacity, uint64_t* n) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  const uint64_t cnt = c.st_host->n;
+  if (n) *n = cnt;
+  if (!xyz) return GCMC_OK;
+  if (capacity < cnt) return set_error(GCMC_ARG, "position buffer too small");
+  std::vector<double4> tmp(cnt);
+  if (cnt) CK(cudaMemcpy(tmp.data(), c.pos, cnt * sizeof(double4), cudaMemcpyDeviceToHost), "download");
+  for (uint64_t i = 0; i < cnt; ++i) {
+    xyz[3 * i] = tmp[i].x;
+    xyz[3 * i + 1] = tmp[i].y;
+    xyz[3 * i + 2] = tmp[i].z;
+  }
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_build(gcmc_dev* h) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  return grid_build(c);
+}
+
+gcmc_status gcmc_grid_info(gcmc_dev* h, int32_t* dims, int32_t* capacity, uint64_t* ncells) {
+  Chain& c = *H(h);
+  if (dims) *dims = c.grid.dims;
+  if (capacity) *capacity = c.grid.cap;
+  if (ncells) *ncells = c.grid.ncells;
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_download_grid(gcmc_dev* h, int32_t* occ, int32_t* slots) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (!c.grid.ncells) return GCMC_OK;
+  CK(cudaStreamSynchronize(c.stream), "download grid");
+  if (occ) CK(cudaMemcpy(occ, c.grid.occ, c.grid.ncells * 4, cudaMemcpyDeviceToHost), "download grid");
+  if (slots)
+    CK(cudaMemcpy(slots, c.grid.slots, c.grid.ncells * c.grid.cap * 4, cudaMemcpyDeviceToHost),
+       "download grid");
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_rebuild_check(gcmc_dev* h, char* msg, size_t msg_cap, int32_t* clean) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  std::string issue;
+  s = grid_check(c, &issue);
+  if (s) return s;
+  if (clean) *clean = issue.empty() ? 1 : 0;
+  if (msg && msg_cap) {
+    std::strncpy(msg, issue.c_str(), msg_cap - 1);
+    msg[msg_cap - 1] = 0;
+  }
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_peak_occupancy(gcmc_dev* h, int32_t* peak) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  *peak = c.st_host->peak;
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_delta_batch(gcmc_dev* h, uint64_t n, const int32_t* kinds, const uint64_t* pids,
+                             const double* xyz, double* du, double* dw) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (n == 0) return GCMC_OK;
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (kinds[i] < 0 || kinds[i] > 2) return set_error(GCMC_ARG, "bad move kind");
+    if (kinds[i] != 1 && pids[i] >= c.st_host->n) return invalid_pid(c);
+  }
+  if ((s = ensure_batch(c, n))) return s;
+  double* d_du = c.dscratch;
+  double* d_dw = d_du + c.batch_cap;
+  double* d_xyz = d_dw + c.batch_cap;
+  uint64_t* d_pid = reinterpret_cast<uint64_t*>(d_xyz + 3 * c.batch_cap);
+  int32_t* d_kind = c.iscratch;
+  std::vector<double> xyz_buf(3 * n, 0.0);
+  std::vector<uint64_t> pid_buf(n, 0);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (xyz) for (int k = 0; k < 3; ++k) xyz_buf[3 * i + k] = xyz[3 * i + k];
+    if (pids) pid_buf[i] = pids[i];
+  }
+  CK(cudaMemcpyAsync(d_kind, kinds, n * 4, cudaMemcpyHostToDevice, c.stream), "delta");
+  CK(cudaMemcpyAsync(d_pid, pid_buf.data(), n * 8, cudaMemcpyHostToDevice, c.stream), "delta");
+  CK(cudaMemcpyAsync(d_xyz, xyz_buf.data(), n * 24, cudaMemcpyHostToDevice, c.stream), "delta");
+  if ((s = delta_batch(c, n, d_kind, d_pid, d_xyz, d_du, d_dw))) return s;
+  CK(cudaMemcpyAsync(du, d_du, n * 8, cudaMemcpyDeviceToHost, c.stream), "delta");
+  CK(cudaMemcpyAsync(dw, d_dw, n * 8, cudaMemcpyDeviceToHost, c.stream), "delta");
+  CK(cudaStreamSynchronize(c.stream), "delta");
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_delta_displace(gcmc_dev* h, uint64_t pid, const double pos[3], double* du,
+                                double* dw) {
+  const int32_t k = 0;
+  return gcmc_delta_batch(h, 1, &k, &pid, pos, du, dw);
+}
+
+gcmc_status gcmc_delta_insert(gcmc_dev* h, const double pos[3], double* du, double* dw) {
+  const int32_t k = 1;
+  const uint64_t pid = 0;
+  return gcmc_delta_batch(h, 1, &k, &pid, pos, du, dw);
+}
+
+gcmc_status gcmc_delta_delete(gcmc_dev* h, uint64_t pid, double* du, double* dw) {
+  const int32_t k = 2;
+  const double z[3] = {0, 0, 0};
+  return gcmc_delta_batch(h, 1, &k, &pid, z, du, dw);
+}
+
+gcmc_status gcmc_commit_displace(gcmc_dev* h, uint64_t pid, const double pos[3]) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  if (pid >= c.st_host->n) return invalid_pid(c);
+  return commit_one(c, 0, pid, pos, nullptr);
+}
+
+gcmc_status gcmc_commit_insert(gcmc_dev* h, const double pos[3], uint64_t* pid) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  if (c.st_host->n + 1 > c.capn) return set_error(GCMC_ARG, "store capacity exhausted");
+  return commit_one(c, 1, 0, pos, pid);
+}
+
+gcmc_status gcmc_commit_delete(gcmc_dev* h, uint64_t pid) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  if (pid >= c.st_host->n) return invalid_pid(c);
+  return commit_one(c, 2, pid, nullptr, nullptr);
+}
+
+gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  return total_energy(c, u, w);
+}
+
+gcmc_status gcmc_seed_rng(gcmc_dev* h, uint64_t seed) {
+  std::mt19937_64 eng(seed);  // RngStream(seed) (rng.hpp:23)
+  std::ostringstream os;
+  os << eng;
+  std::istringstream is(os.str());
+  uint64_t words[313];
+  for (auto& w : words) is >> w;
+  return gcmc_set_rng_state(h, words, words[312], 0);
+}
+
+gcmc_status gcmc_set_rng_state(gcmc_dev* h, const uint64_t words[312], uint64_t index,
+                               uint64_t draws) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (index > 312) return set_error(GCMC_ARG, "rng state: bad position");
+  uint64_t buf[314];
+  std::memcpy(buf, words, 312 * 8);
+  buf[312] = index;
+  buf[313] = draws;
+  CK(cudaMemcpyAsync(c.mt, buf, sizeof buf, cudaMemcpyHostToDevice, c.stream), "rng");
+  CK(cudaStreamSynchronize(c.stream), "rng");
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_get_rng_state(gcmc_dev* h, uint64_t words[312], uint64_t* index,
+                               uint64_t* draws) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  uint64_t buf[314];
+  CK(cudaMemcpyAsync(buf, c.mt, sizeof buf, cudaMemcpyDeviceToHost, c.stream), "rng");
+  CK(cudaStreamSynchronize(c.stream), "rng");
+  if (words) std::memcpy(words, buf, 312 * 8);
+  if (index) *index = buf[312];
+  if (draws) *draws = buf[313];
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_set_state(gcmc_dev* h, const gcmc_state* s_in) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  ChainState& st = *c.st_host;
+  st.step = s_in->step;
+  st.energy = s_in->energy;
+  st.virial = s_in->virial;
+  for (int k = 0; k < 3; ++k) {
+    st.attempted[k] = s_in->attempted[k];
+    st.accepted[k] = s_in->accepted[k];
+  }
+  st.samples = s_in->samples;
+  st.sum_u = s_in->sum_u;
+  st.sum_p = s_in->sum_p;
+  st.sum_n = s_in->sum_n;
+  st.sum_n2 = s_in->sum_n2;
+  sync_state_to_device(c);
+  CK(cudaStreamSynchronize(c.stream), "state");
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_get_state(gcmc_dev* h, gcmc_state* out) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  const ChainState& st = *c.st_host;
+  out->step = st.step;
+  out->n = st.n;
+  out->energy = st.energy;
+  out->virial = st.virial;
+  for (int k = 0; k < 3; ++k) {
+    out->attempted[k] = st.attempted[k];
+    out->accepted[k] = st.accepted[k];
+  }
+  out->samples = st.samples;
+  out->sum_u = st.sum_u;
+  out->sum_p = st.sum_p;
+  out->sum_n = st.sum_n;
+  out->sum_n2 = st.sum_n2;
+  out->peak_occupancy = st.peak;
+  out->pad = 0;
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_run_result* out) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (!c.built) return set_error(GCMC_STATE, "grid not built (upload positions first)");
+  const uint64_t kChunk = 1ull << 21;
+  const uint64_t chunk_cap = n < kChunk ? (n ? n : 1) : kChunk;
+  if (chunk_cap > c.props_cap) {
+    cudaFree(c.props);
+    c.props = nullptr;
+    CK(cudaMalloc(&c.props, chunk_cap * sizeof(Proposal)), "alloc proposals");
+    c.props_cap = chunk_cap;
+  }
+  if (trace && chunk_cap > c.trace_cap) {
+    cudaFree(c.trace);
+    c.trace = nullptr;
+    CK(cudaMalloc(&c.trace, chunk_cap * sizeof(gcmc_trace_rec)), "alloc trace");
+    c.trace_cap = chunk_cap;
+  }
+  float gen_ms = 0.f, eng_ms = 0.f;
+  uint64_t done = 0, rounds = 0;
+  gcmc_status s = GCMC_OK;
+  while (done < n) {
+    const uint64_t m = std::min(chunk_cap, n - done);
+    CK(cudaEventRecord(c.ev[0], c.stream), "event");
+    if ((s = gen_proposals(c, m, c.stream))) return s;
+    if (std::getenv("GCMC_ENGINE_PROFILE") && !c.prof) {
+      CK(cudaMalloc(&c.prof, 16 * 16 * sizeof(unsigned long long)), "prof");
+    }
+    CK(cudaEventRecord(c.ev[1], c.stream), "event");
+    if ((s = engine_run(c, m, trace ? c.trace : nullptr, c.stream))) return s;
+    CK(cudaEventRecord(c.ev[2], c.stream), "event");
+    if (trace)
+      CK(cudaMemcpyAsync(trace + done, c.trace, m * sizeof(gcmc_trace_rec), cudaMemcpyDeviceToHost,
+                         c.stream),
+         "trace");
+    if ((s = pull_state(c))) return s;
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+    cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
+    gen_ms += a;
+    eng_ms += b;
+    rounds += c.st_host->rounds;
+    if (c.prof) {
+      unsigned long long hp[16 * 16];
+      cudaMemcpy(hp, c.prof, sizeof hp, cudaMemcpyDeviceToHost);
+      const char* names[] = {"eval", "arrive1", "wait1", "decide", "commit+keep", "arrive2", "wait2"};
+      for (int r = 0; r < c.engine_ctas; r += (c.engine_ctas > 1 ? c.engine_ctas - 1 : 1)) {
+        std::fprintf(stderr, "[engine prof] cta %d rounds %llu:", r, hp[r * 16 + 8]);
+        for (int k = 0; k < 7; ++k)
+          std::fprintf(stderr, " %s=%.0fns", names[k], (double)hp[r * 16 + k] / (double)(hp[r * 16 + 8] ? hp[r * 16 + 8] : 1));
+        const char* en[] = {"ev.lead", "ev.sync", "ev.sums", "ev.reduce"};
+        for (int k = 0; k < 4; ++k)
+          std::fprintf(stderr, " %s=%.0fns", en[k], (double)hp[r * 16 + 9 + k] / (double)(hp[r * 16 + 8] ? hp[r * 16 + 8] : 1));
+        std::fprintf(stderr, "\n");
+      }
+    }
+    if (c.st_host->error) break;
+    done += m;
+  }
+  const ChainState& st = *c.st_host;
+  if (st.error) {
+    const int err = st.error;
+    c.st_host->error = 0;
+    sync_state_to_device(c);
+    if (err == GCMC_CELL_OVERFLOW) return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, st.err_a, st.err_b));
+    std::ostringstream os;
+    os << strategy_name(c.grid.kind) << ": particle " << st.err_a << " not found in cell " << st.err_b;
+    return set_error((gcmc_status)err, os.str());
+  }
+  if (out) {
+    gcmc_get_state(h, &out->state);
+    out->moves = done;
+    out->rounds = rounds;
+    out->device_ms = eng_ms;
+    out->gen_ms = gen_ms;
+  }
+  return GCMC_OK;
+}
+
+gcmc_status gcmc_random_initial_configuration(uint64_t n, double l, double min_sep, uint64_t seed,
+                                              double* out_xyz, uint64_t words[312],
+                                              uint64_t* index, uint64_t* draws) {
+  // init_config.hpp:19-64, same draw sequence (3 per candidate incl. rejects).
+  if (!(l > 0.0) || !(min_sep > 0.0)) return set_error(GCMC_ARG, "bad box or separation");
+  std::mt19937_64 eng(seed);
+  uint64_t ndraws = 0;
+  auto uniform = [&]() {
+    ++ndraws;
+    return static_cast<double>(eng() >> 11) * 0x1.0p-53;
+  };
+  auto wrap = [l](double v) {
+    double r = std::fmod(v, l);
+    if (r < 0.0) r += l;
+    if (r >= l) r = 0.0;
+    return r;
+  };
+  int dims = static_cast<int>(l / min_sep);
+  if (dims < 1) dims = 1;
+  const double inv_width = dims / l;
+  const uint64_t ncells = (uint64_t)dims * dims * dims;
+  std::vector<int64_t> head(ncells, -1), next(n ? n : 1, -1);
+  auto coord = [&](double v) {
+    const int c = static_cast<int>(v * inv_width);
+    return c < dims ? c : dims - 1;
+  };
+  const double min_sep2 = min_sep * min_sep;
+  const double inv_l = 1.0 / l;
+  uint64_t count = 0, rejects = 0;
+  while (count < n) {
+    const double x = wrap(uniform() * l), y = wrap(uniform() * l), z = wrap(uniform() * l);
+    const int cx = coord(x), cy = coord(y), cz = coord(z);
+    const int span = std::min(3, dims);
+    bool clash = false;
+    for (int a = 0; a < span && !clash; ++a)
+      for (int b = 0; b < span && !clash; ++b)
+        for (int q = 0; q < span && !clash; ++q) {
+          int ix = (cx - 1) % dims, iy = (cy - 1) % dims, iz = (cz - 1) % dims;
+          if (ix < 0) ix += dims;
+          if (iy < 0) iy += dims;
+          if (iz < 0) iz += dims;
+          ix = (ix + q) % dims;
+          iy = (iy + b) % dims;
+          iz = (iz + a) % dims;
+          for (int64_t j = head[ix + (uint64_t)dims * (iy + (uint64_t)dims * iz)]; j >= 0; j = next[j]) {
+            double dx = x - out_xyz[3 * j], dy = y - out_xyz[3 * j + 1], dz = z - out_xyz[3 * j + 2];
+            // box.hpp:45-55 (host build has no -march, hence no FMA contraction)
+            dx -= l * std::nearbyint(dx * inv_l);
+            dy -= l * std::nearbyint(dy * inv_l);
+            dz -= l * std::nearbyint(dz * inv_l);
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 < min_sep2) {
+              clash = true;
+              break;
+            }
+          }
+        }
+    if (clash) {
+      if (++rejects >= 1000000)
+        return set_error(GCMC_ARG, "initial configuration: 1000000 consecutive rejections; "
+                                   "density too high for the minimum separation");
+      continue;
+    }
+    rejects = 0;
+    out_xyz[3 * count] = x;
+    out_xyz[3 * count + 1] = y;
+    out_xyz[3 * count + 2] = z;
+    const uint64_t cell = cx + (uint64_t)dims * (cy + (uint64_t)dims * cz);
+    next[count] = head[cell];
+    head[cell] = (int64_t)count;
+    ++count;
+  }
+  std::ostringstream os;
+  os << eng;
+  std::istringstream is(os.str());
+  uint64_t w[313];
+  for (auto& v : w) is >> v;
+  if (words) std::memcpy(words, w, 312 * 8);
+  if (index) *index = w[312];
+  if (draws) *draws = ndraws;
+  return GCMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Host-side internals shared by the translation units of libgcmc_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "common.cuh"
+
+namespace gcmcb {
+
+// Per-chain device handle (what gcmc_dev* points at).
+struct Chain {
+  int device = 0;
+  gcmc_params params{};
+  Box box{};
+  Grid grid{};
+  double4* pos = nullptr;        // [capn]
+  uint64_t capn = 0;
+  ChainState* st = nullptr;      // device
+  ChainState* st_host = nullptr; // pinned mirror
+  // device MT19937-64 state: 312 words + position + draw counter
+  uint64_t* mt = nullptr;        // [312 + 2]
+  // proposal ring (engine input)
+  Proposal* props = nullptr;
+  uint64_t props_cap = 0;
+  gcmc_trace_rec* trace = nullptr;
+  uint64_t trace_cap = 0;
+  // scratch for single-move API / batches
+  double* dscratch = nullptr;    // [2 * batch_cap]
+  int32_t* iscratch = nullptr;
+  uint64_t batch_cap = 0;
+  // energy grid scratch (counting sort)
+  void* egrid = nullptr;
+  size_t egrid_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t gen_stream = nullptr;
+  cudaEvent_t ev[4] = {};
+  int sm_count = 0;
+  int engine_ctas = 0;
+  int engine_warps = 0;
+  bool built = false;
+  unsigned long long* prof = nullptr;  // engine phase timers (GCMC_ENGINE_PROFILE=1)
+};
+
+// Thread-local error plumbing (api.cu).
+gcmc_status set_error(gcmc_status s, const std::string& msg);
+gcmc_status cuda_error(cudaError_t e, const char* where);
+
+// grid.cu
+gcmc_status grid_build(Chain& c);                              // occ/slots/cellpos from pos
+gcmc_status grid_check(Chain& c, std::string* issue);          // rebuild_check
+gcmc_status commit_one(Chain& c, int kind, uint64_t pid, const double* p, uint64_t* new_pid);
+
+// delta.cu
+gcmc_status delta_batch(Chain& c, uint64_t n, const int32_t* kinds_d, const uint64_t* pids_d,
+                        const double* xyz_d, double* du_d, double* dw_d);
+
+// energy.cu
+gcmc_status total_energy(Chain& c, double* u, double* w);
+
+// gen.cu: parse the next `n` moves of the MT stream into c.props[0..n).
+gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s);
+
+// engine.cu: run n moves from c.props; optional device trace.
+gcmc_status engine_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
+
+// Error text in the reference's wording.
+std::string overflow_message(const Chain& c, int64_t cell, int64_t occ);
+std::string strategy_name(int kind);
+
+}  // namespace gcmcb

@@ -1,0 +1,109 @@
+// Latency microbenchmarks for the engine's critical path (single thread).
+#include <cstdio>
+#include <cstring>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+using namespace gcmcb;
+
+__global__ void k_lat(const int* chase, int steps, const double4* recs, Box b, unsigned long long* out, double* sink) {
+  if (threadIdx.x) return;
+  // L2 (.cg) pointer chase
+  int p = 0;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < steps; ++i) p = __ldcg(chase + p);
+  unsigned long long t1 = clock64();
+  out[0] = (t1 - t0) / steps;
+  // default-cached chase (L1)
+  p = 0;
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) p = chase[p];
+  t1 = clock64();
+  out[1] = (t1 - t0) / steps;
+  // dependent DADD chain
+  double x = sink[0];
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) x = __dadd_rn(x, 1.0);
+  t1 = clock64();
+  out[2] = (t1 - t0) / steps;
+  // rint chain
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) x = rint(__dadd_rn(x, 0.3));
+  t1 = clock64();
+  out[3] = (t1 - t0) / steps;
+  // div chain
+  double y = 1.7;
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) y = __ddiv_rn(1.3, __dadd_rn(y, 1.0));
+  t1 = clock64();
+  out[4] = (t1 - t0) / steps;
+  // full pair term (min image + LJ) chained through r2 perturbation
+  double acc = 0.0;
+  double px = 1.0, py = 2.0, pz = 3.0;
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) {
+    const double4 r = make_double4(1.5 + acc * 1e-30, 2.2, 3.1, 0.0);
+    const double r2 = min_image_dist2(px, py, pz, r.x, r.y, r.z, b);
+    double u, w;
+    lj_pair_clamped(r2, b, u, w);
+    acc = __dadd_rn(acc, u);
+  }
+  t1 = clock64();
+  out[5] = (t1 - t0) / steps;
+  // exp chain
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) y = exp(-__dmul_rn(y, 1e-3));
+  t1 = clock64();
+  out[6] = (t1 - t0) / steps;
+  // 8 independent .cg loads then use (MLP): time per batch
+  t0 = clock64();
+  int q = 0;
+  for (int i = 0; i < steps / 8; ++i) {
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(chase + ((q + k * 977) & 65535));
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+    q = s & 65535;
+  }
+  t1 = clock64();
+  out[7] = (t1 - t0) / (steps / 8);
+  // double4 ld_cg chase via pid field
+  long long pid = 0;
+  t0 = clock64();
+  for (int i = 0; i < steps; ++i) {
+    const double4 r = ld_cg(recs + pid);
+    pid = bits_pid(r.w);
+  }
+  t1 = clock64();
+  out[8] = (t1 - t0) / steps;
+  sink[0] = x + y + acc + p + q + pid;
+}
+
+int main() {
+  const int N = 1 << 16;
+  int* h = new int[N];
+  // random cyclic permutation
+  unsigned s = 12345;
+  int* perm = new int[N];
+  for (int i = 0; i < N; ++i) perm[i] = i;
+  for (int i = N - 1; i > 0; --i) { s = s * 1103515245u + 12345u; int j = s % (i + 1); int t = perm[i]; perm[i] = perm[j]; perm[j] = t; }
+  for (int i = 0; i < N; ++i) h[perm[i]] = perm[(i + 1) % N];
+  double4* hr = new double4[N];
+  for (int i = 0; i < N; ++i) hr[perm[i]] = make_double4(0, 0, 0, [&]{ long long v = perm[(i + 1) % N]; double dd; memcpy(&dd, &v, 8); return dd; }());
+  int* d; double4* dr; unsigned long long* o; double* sink;
+  cudaMalloc(&d, N * 4); cudaMalloc(&dr, N * 32); cudaMalloc(&o, 16 * 8); cudaMalloc(&sink, 8);
+  cudaMemcpy(d, h, N * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dr, hr, N * 32, cudaMemcpyHostToDevice);
+  cudaMemset(sink, 0, 8);
+  Box b{};
+  b.l = 36.57; b.inv_l = 1.0 / b.l; b.eps = 1; b.sigma = 1; b.sigma2 = 1; b.rc = 2.5; b.rc2 = 6.25; b.four_eps = 4; b.tf_eps = 24;
+  for (int rep = 0; rep < 2; ++rep) k_lat<<<1, 32>>>(d, 4096, dr, b, o, sink);
+  unsigned long long ho[16];
+  cudaMemcpy(ho, o, 16 * 8, cudaMemcpyDeviceToHost);
+  const char* names[] = {"ld.cg chase", "ld chase", "dadd", "rint+dadd", "ddiv+dadd", "pair_term", "exp", "8x ld.cg batch", "double4 ld.cg chase"};
+  for (int i = 0; i < 9; ++i) printf("%-22s %6llu cycles\n", names[i], ho[i]);
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
