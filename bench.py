@@ -1,0 +1,319 @@
+"""Benchmark: MC trial moves/s of the GCMC per-move energy path on B200.
+
+Workload (BASELINE.json configs[3], "LJ fluid GCMC ~1M particles on 1 B200"):
+N0 = 1,048,576 LJ particles, rho0 = 0.67 (L = 116.10 sigma), T = 2, mu = +1,
+r_cut = 2.5 sigma, microcell strategy, 30/35/35 displace/insert/delete mix,
+seed 1 (+ rank), random sequential start (init_config.hpp:19-64, 0.85 sigma).
+One "step" = one gcmc_run_moves() batch of --moves-per-step Simulation::step()s
+on the device (proposal generation + persistent engine). Synthetic data: the
+reference's own random initial configuration.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank runs an independent
+chain (seed 1 + rank) — "replicas only", no collective on the hot path; the
+only NCCL call is the max-over-ranks of the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MC trial moves/sec"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# microcell, reference layout, rho ~ 0.67: per window ~220
+# occupancy words (4 B) + ~147 candidates x (4 B slot id + 24 B xyz) ~ 5.0 KB;
+# 1.3 windows per move (0.3 x 2 + 0.7 x 1) -> 6.5 KB per move.
+ALG_BYTES_PER_MOVE = 6.5e3
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n0", type=int, default=1 << 20)
+    ap.add_argument("--density", type=float, default=0.67)
+    ap.add_argument("--mu", type=float, default=1.0)
+    ap.add_argument("--temperature", type=float, default=2.0)
+    ap.add_argument("--strategy", default="microcell")
+    ap.add_argument("--moves-per-step", type=int, default=1 << 18)
+    ap.add_argument("--cpu-moves", type=int, default=100000,
+                    help="bounded CPU reference sample (moves)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+        mask = 0
+        for _, _, r in self.samples:
+            mask |= r
+        reasons = [v for k, v in names.items() if mask & k and k != 0x1]
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def config_dict(a, world):
+    return {"workload": f"LJ fluid GCMC ~1M particles on 1 B200 (BASELINE configs[3])"
+                        if a.n0 == 1 << 20 else f"LJ fluid GCMC N0={a.n0}",
+            "n0": a.n0, "density": a.density, "temperature": a.temperature, "mu": a.mu,
+            "r_cut": 2.5, "strategy": a.strategy, "move_mix": "30/35/35",
+            "moves_per_step": a.moves_per_step, "chains": world,
+            "start": "random sequential insertion, 0.85 sigma (init_config.hpp:19-64)",
+            "l2": "state (~70 MB at 1M) stays L2/HBM resident; inputs > L2 flush not needed: "
+                  "each step reads a fresh 12 MB proposal stream and random cells",
+            "parallelism": f"replicas x{world} (independent chains, seed 1+rank)"}
+
+
+def cpu_baseline(xyz, rng_hex, u0, w0, a, box):
+    """The reference's own Simulation::step loop (oracle/_ref) on this host,
+    resumed from the same start state (engine.hpp:244-252), 1 core."""
+    import oracle as O
+
+    if os.path.exists(O.REF_SO):
+        kind = "reference"
+        cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+                           strategy=a.strategy)
+        sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=rng_hex, step=0, energy=u0, virial=w0)
+        secs, _ = sim.run(a.cpu_moves)
+    else:
+        kind = "port"
+        p = O.port_params(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+                          strategy=a.strategy)
+        sim = O.PortSim(p, xyz, O.rng_from_hex(rng_hex), energy=u0, virial=w0)
+        t0 = time.perf_counter()
+        sim.run(a.cpu_moves)
+        secs = time.perf_counter() - t0
+    return {"value": a.cpu_moves / secs, "unit": "moves/s", "cores": 1, "kind": kind,
+            "sample": f"{a.cpu_moves} Simulation::step() moves of the same 1M workload from the "
+                      f"same start state (resume ctor), {secs:.2f} s, host {os.cpu_count()} cores, "
+                      "1 used"}
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the reference CPU implementation on this host."""
+    if rank != 0:
+        return
+    import oracle as O
+
+    box = (a.n0 / a.density) ** (1.0 / 3.0)
+    xyz, hexs = O.ref_initial_configuration(a.n0, box, 1)  # the reference's own init
+    cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+                       strategy=a.strategy)
+    # U/W only matter for reported observables, not for the trajectory; the
+    # resume ctor avoids the O(N^2) total energy (hours at 1M on one core).
+    sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=hexs, step=0, energy=0.0, virial=0.0)
+    per_step = max(1000, a.cpu_moves // 5)
+    for _ in range(a.warmup):
+        sim.run(per_step)
+    secs = 0.0
+    for _ in range(a.steps):
+        s, _ = sim.run(per_step)
+        secs += s
+    moves = per_step * a.steps
+    v = moves / secs
+    line = {"metric": METRIC, "value": v, "unit": "moves/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(a, 1), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "moves/s", "cores": 1,
+                             "kind": "reference" if os.path.exists(O.REF_SO) else "port",
+                             "sample": f"{per_step} moves per step, reference Simulation::step loop "
+                                       "(oracle/_ref, g++ -O3, proj/CMakeLists Release flags)"},
+            "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse_args()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    import torch
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    from paper_1408_3764_b200 import engine as E
+    from paper_1408_3764_b200.config import RunConfig
+
+    box = (a.n0 / a.density) ** (1.0 / 3.0)
+    xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, 1 + rank)
+    cfg = RunConfig(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+                    strategy=a.strategy, seed=1 + rank)
+    sim = E.Simulation(cfg, xyz, rng, device=local)
+    st0 = sim.dev.get_state()
+    u0, w0 = st0.energy, st0.virial
+
+    # CPU baseline from the identical start state (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(xyz, rng.serialize_hex(), u0, w0, a, box)
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    for _ in range(a.warmup):
+        sim.run(a.moves_per_step)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+
+    # ---- device-resident timing (value): CUDA events inside the library
+    barrier()
+    dev_ms = eng_ms = 0.0
+    rounds = 0
+    acc0 = sum(sim.dev.get_state().accepted)
+    with ClockSampler(local) as clk:
+        for _ in range(a.steps):
+            sim.run(a.moves_per_step)
+            r = sim.last_run
+            dev_ms += r.device_ms + r.gen_ms
+            eng_ms += r.device_ms
+            rounds += r.rounds
+    barrier()
+    acc1 = sum(sim.dev.get_state().accepted)
+    # ---- end-to-end through the C ABI (run + checkpoint read-back of state,
+    #      RNG and positions to host memory), wall clock
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        sim.run(a.moves_per_step)
+        sim.dev.get_state()
+        sim.dev.get_rng()
+        sim.dev.positions()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+
+    moves_rank = a.moves_per_step * a.steps
+    t_dev = dev_ms / 1e3
+    if pg:
+        t = torch.tensor([t_dev, e2e_s], dtype=torch.float64, device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        t_dev, e2e_s = float(t[0]), float(t[1])
+    value = moves_rank * world / t_dev
+    e2e = moves_rank * world / e2e_s
+    peak, peak_kind = hbm_peak()
+    eng_launch_s = eng_ms / 1e3 / a.steps  # one engine launch per step (<= 2^21 moves)
+    achieved = ALG_BYTES_PER_MOVE * a.moves_per_step / eng_launch_s / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "engine_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                tj = json.load(f)
+            traffic = tj.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    n_final = sim.dev.get_state().n
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t_dev / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(a, world),
+            "e2e": {"value": e2e, "unit": "moves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 256 + 314 * 8 + 24 * n_final},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_kind,
+                         "kernel": "k_engine (persistent cluster Metropolis loop)",
+                         "alg_bytes_per_move": ALG_BYTES_PER_MOVE,
+                         "note": "serial Markov chain: latency-bound, not HBM-bound; see "
+                                 "ns_per_round and DESIGN.md"},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": 2 * a.steps,
+            "ns_per_move": 1e9 * t_dev / moves_rank,
+            "ns_per_round": 1e9 * (eng_ms / 1e3) / max(rounds, 1),
+            "moves_per_round": moves_rank / max(rounds, 1),
+            "acceptance": (acc1 - acc0) / moves_rank,
+            "n_final": n_final,
+        }
+        if cpu and cpu.get("value"):
+            line["speedup_vs_cpu_e2e"] = e2e / cpu["value"]
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
