@@ -29,8 +29,8 @@ class GcmcParams(C.Structure):
                 ("displace_percent", _d), ("max_displacement", _d),
                 ("equilibration_steps", _u64), ("sampling_interval", _u64),
                 ("strategy", _i32), ("cell_capacity", _i32), ("microcell_capacity", _i32),
-                ("tail_corrections", _i32), ("max_particles", _u64), ("cluster_ctas", _i32),
-                ("warps_per_cta", _i32)]
+                ("tail_corrections", _i32), ("max_particles", _u64), ("engine_ctas", _i32),
+                ("engine_group", _i32), ("engine_variants", _i32), ("engine_bias", _i32)]
 
 
 class GcmcState(C.Structure):

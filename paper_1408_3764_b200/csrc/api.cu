@@ -173,24 +173,66 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device), "props");
   c->sm_count = prop.multiProcessorCount;
-  c->engine_ctas = P.cluster_ctas > 0 ? P.cluster_ctas : 16;
-  // moves per CTA (the C ABI field keeps its name): 1, 2 or 4; K = ctas * moves <= 64
-  c->engine_warps = P.warps_per_cta > 0 ? P.warps_per_cta : 1;
-  if (c->engine_warps != 1 && c->engine_warps != 2) c->engine_warps = 4;
-  while (c->engine_ctas * c->engine_warps > 64) --c->engine_ctas;
-  if (c->engine_ctas > 16) c->engine_ctas = 16;
+  // Engine shape (engine.cu): one persistent CTA per SM, 1 sequencer + evaluators.
+  c->engine_group = P.engine_group == 128 || P.engine_group == 512 ? P.engine_group : 256;
+  c->engine_ctas = P.engine_ctas > 1 && P.engine_ctas <= c->sm_count ? P.engine_ctas : c->sm_count;
+  {
+    const int mg = 512 / c->engine_group;
+    const int max_ctas = 1 + engine_max_slots() / mg;
+    if (c->engine_ctas > max_ctas) c->engine_ctas = max_ctas;
+  }
+  c->engine_variants = P.engine_variants > 0 ? (P.engine_variants > 31 ? 31 : P.engine_variants) : 7;
+  c->engine_bias = P.engine_bias > 0 ? 1 : -1;
+  // Evaluation mirror: bricks of side L/dims >= r_cut (1e-9 relative margin).
+  {
+    Mirror& m = c->mirror;
+    int d = (int)std::floor(P.box_length / (P.r_cut * (1.0 + 1e-9)));
+    if (d < 1) d = 1;
+    if (d > 1024) d = 1024;
+    m.dims = d;
+    m.nb = (uint32_t)d * d * d;
+    m.side = P.box_length / d;
+    m.inv = (double)d / P.box_length;
+    // records per brick: generous over the densest LJ states (rho <= ~1.2)
+    const double vb = m.side * m.side * m.side / (P.sigma * P.sigma * P.sigma);
+    int cap = (int)std::ceil(vb * 2.0) + 16;
+    if (cap < 32) cap = 32;
+    if (cap > 128) cap = 128;
+    m.cap = cap;
+    // conflict reach: the window (1 brick) and any reference cell
+    double ref_side = 0.0;
+    if (g.kind == GCMC_MICROCELL) ref_side = P.sigma;
+    if (g.kind == GCMC_CELL_LIST) ref_side = P.box_length / g.dims;
+    int reach = (int)std::ceil(ref_side / m.side);
+    m.reach = reach < 1 ? 1 : reach;
+  }
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
   CK(cudaStreamCreateWithFlags(&c->gen_stream, cudaStreamNonBlocking), "stream");
   for (auto& ev : c->ev) CK(cudaEventCreate(&ev), "event");
   CK(cudaMalloc(&c->pos, capn * sizeof(double4)), "alloc pos");
   CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
+  CK(cudaMalloc(&c->rslot, capn * sizeof(int32_t)), "alloc rslot");
+  CK(cudaMalloc(&c->bslot, capn * sizeof(int32_t)), "alloc bslot");
   if (g.ncells) {
     CK(cudaMalloc(&g.occ, g.ncells * sizeof(int32_t)), "alloc occ");
     CK(cudaMalloc(&g.slots, g.ncells * g.cap * sizeof(int32_t)), "alloc slots");
-    CK(cudaMalloc(&g.cellpos, g.ncells * g.cap * sizeof(double4)), "alloc cellpos");
     CK(cudaMemset(g.occ, 0, g.ncells * sizeof(int32_t)), "memset");
     CK(cudaMemset(g.slots, 0xff, g.ncells * g.cap * sizeof(int32_t)), "memset");  // -1
-    CK(cudaMemset(g.cellpos, 0, g.ncells * g.cap * sizeof(double4)), "memset");
+  }
+  {
+    Mirror& m = c->mirror;
+    const size_t nrec = (size_t)m.nb * m.cap;
+    CK(cudaMalloc(&m.rx, nrec * sizeof(double)), "alloc mirror");
+    CK(cudaMalloc(&m.ry, nrec * sizeof(double)), "alloc mirror");
+    CK(cudaMalloc(&m.rz, nrec * sizeof(double)), "alloc mirror");
+    CK(cudaMalloc(&m.rid, nrec * sizeof(int32_t)), "alloc mirror");
+    CK(cudaMalloc(&m.occ, (size_t)m.nb * sizeof(int32_t)), "alloc mirror");
+    CK(cudaMemset(m.occ, 0, (size_t)m.nb * sizeof(int32_t)), "memset");
+    size_t bd, br, be;
+    engine_buffer_bytes(engine_max_slots(), &bd, &br, &be);
+    CK(cudaMalloc(&c->eng_dec, bd), "alloc engine");
+    CK(cudaMalloc(&c->eng_res, br), "alloc engine");
+    CK(cudaMalloc(&c->eng_ext, be), "alloc engine");
   }
   CK(cudaMalloc(&c->st, sizeof(ChainState)), "alloc state");
   CK(cudaMallocHost(&c->st_host, sizeof(ChainState)), "alloc state");
@@ -210,7 +252,16 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   cudaFree(c->pos);
   cudaFree(c->grid.occ);
   cudaFree(c->grid.slots);
-  cudaFree(c->grid.cellpos);
+  cudaFree(c->rslot);
+  cudaFree(c->bslot);
+  cudaFree(c->mirror.rx);
+  cudaFree(c->mirror.ry);
+  cudaFree(c->mirror.rz);
+  cudaFree(c->mirror.rid);
+  cudaFree(c->mirror.occ);
+  cudaFree(c->eng_dec);
+  cudaFree(c->eng_res);
+  cudaFree(c->eng_ext);
   cudaFree(c->st);
   cudaFreeHost(c->st_host);
   cudaFree(c->mt);
@@ -511,8 +562,9 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     CK(cudaEventRecord(c.ev[0], c.stream), "event");
     if ((s = gen_proposals(c, m, c.stream))) return s;
     if (std::getenv("GCMC_ENGINE_PROFILE") && !c.prof) {
-      CK(cudaMalloc(&c.prof, 16 * 16 * sizeof(unsigned long long)), "prof");
+      CK(cudaMalloc(&c.prof, 48 * sizeof(unsigned long long)), "prof");
     }
+    if (c.prof) CK(cudaMemsetAsync(c.prof, 0, 48 * sizeof(unsigned long long), c.stream), "prof");
     CK(cudaEventRecord(c.ev[1], c.stream), "event");
     if ((s = engine_run(c, m, trace ? c.trace : nullptr, c.stream))) return s;
     CK(cudaEventRecord(c.ev[2], c.stream), "event");
@@ -528,18 +580,19 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     eng_ms += b;
     rounds += c.st_host->rounds;
     if (c.prof) {
-      unsigned long long hp[16 * 16];
+      unsigned long long hp[48];
       cudaMemcpy(hp, c.prof, sizeof hp, cudaMemcpyDeviceToHost);
-      const char* names[] = {"eval", "arrive1", "wait1", "decide", "commit+keep", "arrive2", "wait2"};
-      for (int r = 0; r < c.engine_ctas; r += (c.engine_ctas > 1 ? c.engine_ctas - 1 : 1)) {
-        std::fprintf(stderr, "[engine prof] cta %d rounds %llu:", r, hp[r * 16 + 8]);
-        for (int k = 0; k < 7; ++k)
-          std::fprintf(stderr, " %s=%.0fns", names[k], (double)hp[r * 16 + k] / (double)(hp[r * 16 + 8] ? hp[r * 16 + 8] : 1));
-        const char* en[] = {"ev.lead", "ev.sync", "ev.sums", "ev.reduce"};
-        for (int k = 0; k < 4; ++k)
-          std::fprintf(stderr, " %s=%.0fns", en[k], (double)hp[r * 16 + 9 + k] / (double)(hp[r * 16 + 8] ? hp[r * 16 + 8] : 1));
-        std::fprintf(stderr, "\n");
-      }
+      const double R = (double)(hp[15] ? hp[15] : 1);
+      const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "close_publish", "walk_masks", "walk_iter"};
+      std::fprintf(stderr, "[engine prof] rounds %llu sequencer:", hp[15]);
+      for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.0f", sn[k], hp[k] / R);
+      const char* en[] = {"idle", "poll_D", "assign", "setup", "sums", "publish", "tail"};
+      std::fprintf(stderr, "\n[engine prof] evaluator(cta1,g0):");
+      for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %s=%.0f", en[k], hp[16 + k] / R);
+      std::fprintf(stderr, "\n[engine prof] helpers: work=%.0f idle=%.0f (cycles/round)\n", hp[32] / R,
+                   hp[33] / R);
+      std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",
+                   hp[40], hp[41], hp[42], hp[43], hp[44], hp[45]);
     }
     if (c.st_host->error) break;
     done += m;
@@ -549,6 +602,11 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     const int err = st.error;
     c.st_host->error = 0;
     sync_state_to_device(c);
+    if (err == GCMC_CELL_OVERFLOW && st.err_c == 1) {
+      std::ostringstream os;
+      os << "mirror: brick " << st.err_a << " exceeds capacity " << c.mirror.cap;
+      return set_error(GCMC_CELL_OVERFLOW, os.str());
+    }
     if (err == GCMC_CELL_OVERFLOW) return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, st.err_a, st.err_b));
     std::ostringstream os;
     os << strategy_name(c.grid.kind) << ": particle " << st.err_a << " not found in cell " << st.err_b;

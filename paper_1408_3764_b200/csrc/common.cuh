@@ -36,7 +36,29 @@ struct Grid {
   double last_w;            // microcell boundary cell width (sigma units)
   int32_t* occ;             // [ncells]          occupancy_view()
   int32_t* slots;           // [cap*ncells]      slots_view(): micro k*nc+c, cell c*cap+k
-  double4* cellpos;         // [cap*ncells]      same index as slots: (x, y, z, pid bits)
+};
+
+// Evaluation mirror ("bricks"): cells of side L/dims >= r_cut, so the 3x3x3
+// brick neighbourhood of a point holds every particle within r_cut (the
+// reference's traditional cell-list geometry, cell_grid.hpp:27-33, with a
+// 1e-9 relative margin). Records are SoA double planes indexed brick*cap+k,
+// densely packed per brick (swap-last removal), so the resident footprint is
+// ~N*28 bytes regardless of the strategy whose reference layout (Grid) is
+// maintained for parity. Any window covering the cutoff sphere yields the
+// same pair set, so the ΔE it produces is the reference's up to summation
+// order.
+struct Mirror {
+  int dims;                 // bricks per axis
+  int cap;                  // records per brick
+  uint32_t nb;              // dims^3
+  int reach;                // conflict reach in bricks (engine.cu)
+  double inv;               // dims / L
+  double side;              // L / dims
+  double* rx;               // [nb*cap] record planes
+  double* ry;
+  double* rz;
+  int32_t* rid;             // [nb*cap] particle id of each record
+  int32_t* occ;             // [nb]
 };
 
 // Per-chain scalars on the device (one 256-byte block, L2 resident).
@@ -249,6 +271,33 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Compensated accumulator (kahan.hpp:8-20) and a TwoSum warp tree; used by
+// the full-system energy (energy.cu).
+struct Kahan {
+  double s, c;
+  __device__ __forceinline__ void add(double v) {
+    const double y = __dsub_rn(v, c);
+    const double t = __dadd_rn(s, y);
+    c = __dsub_rn(__dsub_rn(t, s), y);
+    s = t;
+  }
+};
+
+__device__ __forceinline__ double warp_sum_comp(Kahan k) {
+  double s = k.s, e = -k.c;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const double e2 = __shfl_xor_sync(0xffffffffu, e, o);
+    const double t = __dadd_rn(s, s2);
+    const double bp = __dsub_rn(t, s);
+    const double err = __dadd_rn(__dsub_rn(s, __dsub_rn(t, bp)), __dsub_rn(s2, bp));
+    s = t;
+    e = __dadd_rn(__dadd_rn(e, e2), err);
+  }
+  return __dadd_rn(s, e);
 }
 
 }  // namespace gcmcb

@@ -15,7 +15,7 @@
 #include <sstream>
 
 #include "internal.h"
-#include "window.cuh"
+#include "common.cuh"
 
 namespace gcmcb {
 

@@ -1,66 +1,672 @@
 // Persistent on-device Metropolis loop: Simulation::step() x n
-// (engine.hpp:293-308, 350-426) with exact speculative evaluation.
+// (engine.hpp:293-308, 350-426), executed as exact multi-move speculation
+// across the whole GPU.
 //
-// Why this is exact: every move's random draws are fixed before its ΔE is
-// known (engine.hpp:207-213, 352-354), so the proposals are precomputed
-// (gen.cu). One thread-block cluster per chain evaluates K = C*M consecutive
-// proposals at once — M groups of 512/M threads per CTA, one proposal per
-// group (cta_window.cuh) — all against the SAME state S. Moves before the
-// first accepted one were each evaluated against exactly the state the
-// serial chain would have seen (nothing changed in between), so their
-// rejections are the serial chain's rejections. The first accepted move is
-// committed by the CTA that evaluated it; later evaluations are discarded
-// and redone next round against the new state. The chain is therefore
-// move-for-move the reference chain (the paper's "run multiple moves
-// concurrently ... keep the first one that is accepted"),
-// while the serial latency is paid once per ACCEPTED move instead of once
-// per move.
+// Why speculation is exact. Every move's random draws are fixed before its ΔE
+// is known (engine.hpp:207-213, 352-354), so proposals are precomputed
+// (gen.cu). Only two things couple a move to its predecessors: the state its
+// ΔE reads, and N, which picks the particle (pid = index_from(pick, N)) and
+// enters the exchange acceptance ratios. A round evaluates a window of
+// upcoming moves against the current state S in parallel — pid-based moves
+// once per candidate N ("variant") — then a single sequencer walks the window
+// in order, tracking N, and keeps the longest prefix in which every move's
+// evaluation provably equals what the serial chain computes:
+//   * the variant for the move's true N was evaluated,
+//   * no earlier accepted move of this round, and no move committed in the
+//     previous round (whose stores may still be in flight), changed anything
+//     the evaluation read: no changed position within reach of its windows,
+//     no changed particle slot it loaded (mirror.cuh, conflict()).
+// Every decision in that prefix is the reference's decision; the first move
+// that fails the test starts the next round. Accepted moves of one round are
+// pairwise independent, so their commits (commit.cuh) run concurrently.
 //
-// Round protocol (one kernel launch for the whole batch; no host trips):
-//   evaluate  group G (= rank*M + g) owns the one move m == G (mod K) in the
-//             window [base, base+K): its proposal was prefetched rounds ago,
-//             so only pos[pid] and the window cells are loaded; the group's
-//             last warp prefetches the commit plan (commit.cuh) meanwhile.
-//             accept + kind bits -> the CTA's flag word
-//   barrier.cluster (release/acquire)
-//   decide    every warp reads the C flag words over DSMEM, rotates the
-//             K-bit masks to move order -> first accept j, kind counts
-//   commit    group j's leader replays the prefetched plan (stores only);
-//             CTA 0 warp 1 applies SystemState / RunStatistics bookkeeping
-//             with the reference's sequential double adds; trace records;
-//             consumed groups advance m += K and prefetch m + 2K
-//   barrier.cluster
-#include <cooperative_groups.h>
+// Roles (one persistent CTA per SM, cooperative launch):
+//   CTA 0        sequencer: polls the slot results of round r, walks, verifies,
+//                publishes decision D_{r+1}; helper warps commit round r's
+//                accepted moves, do the RunStatistics bookkeeping (same
+//                sequential double adds as Simulation::sample) and the trace
+//                while round r+1 is being evaluated.
+//   CTAs 1..G-1  evaluators: MG groups of T threads, one slot (move, variant)
+//                per group per round (slot.cuh), against a shared-memory
+//                replica of the mirror occupancy.
+// Communication is through L2 with self-validating tagged 64-bit words
+// (round tag in the top 16 bits, payload below), so neither side needs a
+// fence on the critical path; the one release/acquire pair orders the
+// commits before the next-but-one round reads them.
+#include <cstdlib>
 
 #include "commit.cuh"
-#include "cta_window.cuh"
 #include "internal.h"
-
-namespace cg = cooperative_groups;
+#include "slot.cuh"
 
 namespace gcmcb {
 
 namespace {
 
+constexpr int kThreads = 512;
+constexpr int kMaxMoves = 64;    // moves per round
+constexpr int kMaxAcc = 32;      // accepted moves per round
+constexpr int kRing = 256;       // proposal ring (moves)
+constexpr int kPre = 2 * kMaxMoves + 2;  // slot prefix entries
+constexpr int kDecHdr = 4;
+constexpr int kDecEnt = 5;
+constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 164
+constexpr int kResWords = 8;     // 6 used
+constexpr int kPollWarps = 12;   // sequencer warps that poll / walk / verify
+constexpr int kMaxSlots = kPollWarps * 32;
+constexpr int kInsSpan = 32;     // insertion accept mask covers d in [-16, 15]
+
+constexpr uint64_t kPay = 0xffffffffffffull;
+
+enum SlotFlag : uint32_t {
+  kFKindMask = 3u,   // 0 displace, 1 insert, 2 delete
+  kFConflict = 4u,   // overlaps a commit of the previous round
+  kFOverflow = 8u,   // accepted commit would overflow a cell / brick
+  kFEmpty = 16u,     // N == 0: counted rejection (engine.hpp:355, 399)
+};
+
+struct SlotExt {  // untagged per-slot payload, published with its own tag
+  double du, dw, pe;  // ΔU, ΔW, p (insert: exp factor E)
+  MoveData md;
+  int32_t cb, ocb, bb, obb;  // cell / brick entered and occupancy (overflow report)
+  uint64_t tag;
+  uint64_t pad;
+};
+static_assert(sizeof(SlotExt) % 16 == 0, "SlotExt layout");
+
 struct EngineArgs {
   Grid g;
+  Mirror m;
   Box b;
-  double4* pos;
+  Store s;
   ChainState* st;
   const Proposal* props;
   gcmc_trace_rec* trace;
   uint64_t nmoves;
   double beta, mu, lambda3, vol, temp, max_disp;
   uint64_t equil, interval;
-  int tail, pad;
-  double tail_cu, tail_cp, tail_s3, tail_bu, tail_bp;  // see engine_run()
-  unsigned long long* prof;  // optional phase timers [C][16] (GCMC_ENGINE_PROFILE)
+  int tail, nslots;  // nslots = (gridDim.x - 1) * MG
+  double tail_cu, tail_cp, tail_s3, tail_bu, tail_bp;
+  uint64_t* dec;     // [kDecWords]
+  uint64_t* res;     // [2][nslots][kResWords]
+  SlotExt* ext;      // [2][nslots]
+  int smem_occ;      // mirror occupancy replicated in shared memory
+  int bias0;         // initial variant bias (+1 / -1)
+  int nvar;          // variants per displace / delete proposal (move index >= 1)
+  unsigned poll_ns;  // back-off between polls
+  unsigned long long* prof;
 };
 
+// ----------------------------------------------------------------- words
+__device__ __forceinline__ uint64_t tagw(uint32_t r, uint64_t payload) {
+  return ((uint64_t)(r & 0xffffu) << 48) | (payload & kPay);
+}
+__device__ __forceinline__ bool tagged(uint64_t w, uint32_t r) {
+  return (uint32_t)(w >> 48) == (r & 0xffffu);
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void nap() { __nanosleep(20); }
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+// Phase timers (GCMC_ENGINE_PROFILE=1): prof[role*16 + phase] accumulates ns.
+struct PhaseClock {
+  unsigned long long acc[12] = {0};
+  unsigned long long t = 0;
+  bool on = false;
+  __device__ __forceinline__ void start(bool enable) {
+    on = enable;
+    if (on) t = clock64();
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if (!on) return;
+    const unsigned long long n = clock64();
+    acc[k] += n - t;
+    t = n;
+  }
+  __device__ __forceinline__ void flush(unsigned long long* p) {
+    if (!on) return;
+    for (int k = 0; k < 12; ++k) p[k] = acc[k];
+  }
+};
+
+// ----------------------------------------------------------------- variants
+// Variant v of a pid-based move evaluates N + off(v): 0, +bias, -bias,
+// +2 bias, -2 bias, ...
+__device__ __forceinline__ int var_off(int v, int bias) {
+  if (v == 0) return 0;
+  const int k = (v + 1) >> 1;
+  return (v & 1) ? bias * k : -bias * k;
+}
+// Centre of the candidate N offsets at move i: the expected drift rate*i
+// (rate in 1/256 per move, published by the sequencer), rounded.
+__device__ __forceinline__ int var_centre(int rate, int i) { return (rate * i + 128) >> 8; }
+__device__ __forceinline__ int var_of(int d, int bias) {
+  if (d == 0) return 0;
+  const int k = d < 0 ? -d : d;
+  return ((d > 0) == (bias > 0)) ? 2 * k - 1 : 2 * k;
+}
+
+// Slot layout of a round with base B: slot 0 is move 0 (its true N is known);
+// move i >= 1 takes need(i) consecutive slots, 1 for an insertion and nvar
+// (one per candidate N) otherwise. Moves are included while all of their
+// slots fit in nslots, up to kMaxMoves and the end of the batch. Both sides
+// derive it from the prefix Q[k] = sum_{m<k} need(B0 + m) over the proposal
+// ring, so an evaluator can place its slot for any base B = B0 + len with one
+// binary search (no assignment step after the decision arrives).
+__device__ __forceinline__ int need_of(const EngineArgs& a, const Proposal* ring, uint64_t mv) {
+  if (mv >= a.nmoves) return 1 << 16;
+  return ring[mv % kRing].kind == 1 ? 1 : a.nvar;
+}
+
+// One warp: Q[0..kPre) over moves B0, B0+1, ...
+__device__ __forceinline__ void prefix_warp(const EngineArgs& a, const Proposal* ring, uint64_t b0,
+                                           int* Q, int lane) {
+  constexpr int PER = (kPre + 31) / 32;  // 5
+  int v[PER], run = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int k = lane * PER + j;
+    v[j] = k < kPre - 1 ? need_of(a, ring, b0 + (uint64_t)k) : 0;
+    run += v[j];
+  }
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int ex = incl - run;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int k = lane * PER + j;
+    if (k < kPre) Q[k] = ex;
+    ex += v[j];
+  }
+}
+
+// Moves / slots of the round at base B0 + len (Q relative to B0).
+__device__ __forceinline__ void round_shape(const EngineArgs& a, const int* Q, int len,
+                                            uint64_t b, int& fit, int& used) {
+  if (b >= a.nmoves) {
+    fit = used = 0;
+    return;
+  }
+  // largest f with 1 + Q[len+f] - Q[len+1] <= nslots, f <= kMaxMoves, b+f <= nmoves
+  int lo = 1, hi = kMaxMoves;
+  const uint64_t left = a.nmoves - b;
+  if ((uint64_t)hi > left) hi = (int)left;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (1 + Q[len + mid] - Q[len + 1] <= a.nslots) lo = mid; else hi = mid - 1;
+  }
+  fit = lo;
+  used = 1 + Q[len + lo] - Q[len + 1];
+}
+
+// Slot s of the round at base B0 + len -> (move i, variant v); false if unused.
+__device__ __forceinline__ bool slot_move(const int* Q, int len, int s, int fit, int& i, int& v) {
+  if (s == 0) {
+    i = 0;
+    v = 0;
+    return fit > 0;
+  }
+  const int target = Q[len + 1] + (s - 1);
+  int lo = len + 1, hi = len + fit - 1;  // k with Q[k] <= target
+  if (hi < lo) return false;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (Q[mid] <= target) lo = mid; else hi = mid - 1;
+  }
+  i = lo - len;
+  v = target - Q[lo];
+  return Q[lo + 1] > target;  // inside move lo (the last move may be partial -> beyond used)
+}
+
+// ----------------------------------------------------------------- conflicts
+struct RW {  // what an evaluation read / a commit wrote
+  uint64_t pt[3];  // brick points: new, old, last particle (delete)
+  int64_t ia, ib;  // particle indices: pid / insert index, q
+};
+
+// Read set of move i (later) vs write set of accepted move j (earlier).
+__device__ __forceinline__ bool conflict(const Mirror& m, bool all_pairs, const RW& r,
+                                         const RW& w) {
+  if (all_pairs) return true;
+  if (r.ia >= 0 && (r.ia == w.ia || r.ia == w.ib)) return true;
+  if (r.ib >= 0 && (r.ib == w.ia || r.ib == w.ib)) return true;
+#pragma unroll
+  for (int x = 0; x < 3; ++x)
+#pragma unroll
+    for (int y = 0; y < 3; ++y)
+      if (mnear(m, r.pt[x], w.pt[y])) return true;
+  return false;
+}
+
+// ----------------------------------------------------------------- decision
+struct Dec {
+  uint64_t base, n;
+  int nacc, bias, stop, rate;
+  RW acc[kMaxAcc];
+  int kind[kMaxAcc];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Ring refill by one warp: proposals [lo, hi) (8-byte async copies).
+__device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, uint64_t lo,
+                                         uint64_t hi, int lane) {
+  constexpr unsigned W = sizeof(Proposal) / 8;
+  const unsigned cnt = (unsigned)(hi - lo) * W;
+  for (unsigned k = lane; k < cnt; k += 32) {
+    const uint64_t mv = lo + k / W;
+    const unsigned w = k % W;
+    cp_async8(reinterpret_cast<uint64_t*>(&ring[mv % kRing]) + w,
+              reinterpret_cast<const uint64_t*>(a.props + mv) + w);
+  }
+  cp_async_commit();
+}
+
+// Warp: wait for D_r and decode it. The D words are self-validating (round
+// tag per word); the loads that follow go to L2 (ld.cg), which holds every
+// commit the sequencer's helpers completed (and fenced) before D_r was
+// written.
+__device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane) {
+  constexpr int PER = (kDecWords + 31) / 32;
+  uint64_t w[PER];
+  for (;;) {
+    w[0] = ld_relaxed(a.dec + lane);
+    w[1] = ld_relaxed(a.dec + 32 + lane);
+    const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2);
+    const bool h2ok = tagged(h2, r);
+    const int nacc = h2ok ? (int)(h2 & 0xff) : 0;
+    const int need = kDecHdr + kDecEnt * nacc;
+    if (need > 64) {
+#pragma unroll
+      for (int j = 2; j < PER; ++j) {
+        const int idx = lane + 32 * j;
+        w[j] = idx < need ? ld_relaxed(a.dec + idx) : 0;
+      }
+    }
+    bool ok = h2ok;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int idx = lane + 32 * j;
+      if (idx < need && !tagged(w[j], r)) ok = false;
+    }
+    if (__all_sync(0xffffffffu, ok)) break;
+    __nanosleep(a.poll_ns);
+  }
+  const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2) & kPay;
+  const int nacc = (int)(h2 & 0xff);
+  const int need = kDecHdr + kDecEnt * nacc;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int idx = lane + 32 * j;
+    if (idx >= need) continue;
+    const uint64_t p = w[j] & kPay;
+    if (idx == 0) d.base = p;
+    else if (idx == 1) d.n = p;
+    else if (idx == 2) {
+      d.nacc = nacc;
+      d.bias = (p >> 8) & 1 ? 1 : -1;
+      d.stop = (int)((p >> 9) & 1);
+      d.rate = (int)(int16_t)(uint16_t)((p >> 10) & 0xffff);
+    } else if (idx >= kDecHdr) {
+      const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
+      if (f < 3) d.acc[e].pt[f] = p;
+      else if (f == 3) {
+        d.kind[e] = (int)(p >> 32) & 3;
+        const uint32_t ia = (uint32_t)p;
+        d.acc[e].ia = ia == 0xffffffffu ? -1 : (int64_t)ia;
+      } else {
+        const uint32_t ib = (uint32_t)p;
+        d.acc[e].ib = ib == 0xffffffffu ? -1 : (int64_t)ib;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// =================================================================== evaluator
+template <int T>
+struct EvalShared {
+  Proposal ring[kRing];
+  Dec d;
+  int Q[kPre];
+  WinWs<T> ws[kThreads / T];
+  struct G {
+    int i, v, kind, empty;
+    uint64_t pid, q, nv;
+    MoveData md;
+    double acc;
+  } gs[kThreads / T];
+};
+
+template <int T>
+__device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
+  constexpr int MG = kThreads / T;
+  auto& sh = *reinterpret_cast<EvalShared<T>*>(smem);
+  uint8_t* occ_s = a.smem_occ ? smem + ((sizeof(EvalShared<T>) + 15) & ~size_t(15)) : nullptr;
+  uint32_t* occ_w = reinterpret_cast<uint32_t*>(occ_s);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = tid / T, gt = tid % T, gw = gt >> 5;
+  const int bar_id = 1 + g;
+  const int cta_slot0 = (blockIdx.x - 1) * MG;  // slots >= nslots are never used
+  WinWs<T>& ws = sh.ws[g];
+  auto& G = sh.gs[g];
+  const bool all_pairs = a.g.kind == GCMC_ALL_PAIRS;
+
+  // initial replica, ring, slot prefix
+  if (occ_s)
+    for (uint32_t i = tid; i < a.m.nb; i += kThreads) occ_s[i] = (uint8_t)__ldcg(a.m.occ + i);
+  uint64_t ring_hi = a.nmoves < (uint64_t)kRing ? a.nmoves : (uint64_t)kRing;
+  if (tid < 32) {
+    ring_fill(a, sh.ring, 0, ring_hi, lane);
+    cp_async_wait();
+    __syncwarp();
+    prefix_warp(a, sh.ring, 0, sh.Q, lane);
+  }
+  __syncthreads();
+  uint64_t b0 = 0;  // base the prefix Q refers to
+  uint32_t r = 1;
+  PhaseClock pc;
+  pc.start(a.prof && blockIdx.x == 1 && tid == 0);
+  for (;; ++r) {
+    pc.mark(0);
+    if (tid < 32) {
+      poll_dec(a, r, sh.d, lane);
+      pc.mark(1);  // D observed
+      const Dec& d = sh.d;
+      // replica: the previous round's commits (a--, b++)
+      if (occ_s && lane < d.nacc) {
+        const int k = d.kind[lane];
+        const RW& e = d.acc[lane];
+        if (k != 1) {
+          const uint32_t ba = mbrick(a.m, e.pt[1]);
+          atomicSub(occ_w + (ba >> 2), 1u << (8 * (ba & 3)));
+        }
+        if (k != 2) {
+          const uint32_t bb = mbrick(a.m, e.pt[0]);
+          atomicAdd(occ_w + (bb >> 2), 1u << (8 * (bb & 3)));
+        }
+      }
+      // slots of this CTA
+      if (lane < MG && !d.stop) {
+        const int len = (int)(d.base - b0);
+        int fit, used, i = -1, v = 0;
+        round_shape(a, sh.Q, len, d.base, fit, used);
+        const int s = cta_slot0 + lane;
+        if (!(s < used && slot_move(sh.Q, len, s, fit, i, v))) i = -1;
+        sh.gs[lane].i = i;
+        sh.gs[lane].v = v;
+      }
+      cp_async_wait();
+    }
+    __syncthreads();
+    const Dec& d = sh.d;
+    if (d.stop) break;
+    pc.mark(2);  // replica + slot
+    uint64_t* rw = a.res + ((size_t)(r & 1) * a.nslots + cta_slot0 + g) * kResWords;
+    SlotExt* ex = a.ext + (size_t)(r & 1) * a.nslots + cta_slot0 + g;
+    if (G.i >= 0) {
+      int ocb = 0;
+      // ---- setup (warp 0 of the group)
+      if (gw == 0) {
+        const uint64_t mv = d.base + (uint64_t)G.i;
+        const Proposal& pr = sh.ring[mv % kRing];
+        const int kind = pr.kind;
+        int empty = 0;
+        int64_t nv = (int64_t)d.n;
+        uint64_t pid = 0, q = 0;
+        if (kind != 1) {
+          nv += var_centre(d.rate, G.i) + var_off(G.v, d.bias);
+          empty = nv <= 0;
+        }
+        MoveData md;
+        md.nx = pr.x;
+        md.ny = pr.y;
+        md.nz = pr.z;
+        md.rslot_pid = md.bslot_pid = -1;
+        md.ox = md.oy = md.oz = 0.0;
+        if (kind != 1 && !empty) {
+          pid = index_from(pr.pick, (uint64_t)nv);
+          q = (uint64_t)nv - 1;
+          // the mover's position and back-pointers (one L2 hop)
+          if (lane == 0) {
+            const double4 o = ld_cg(a.s.pos + pid);
+            md.ox = o.x;
+            md.oy = o.y;
+            md.oz = o.z;
+            md.rslot_pid = __ldcg(a.s.rslot + pid);
+            md.bslot_pid = __ldcg(a.s.bslot + pid);
+          }
+          md.ox = __shfl_sync(0xffffffffu, md.ox, 0);
+          md.oy = __shfl_sync(0xffffffffu, md.oy, 0);
+          md.oz = __shfl_sync(0xffffffffu, md.oz, 0);
+          md.rslot_pid = __shfl_sync(0xffffffffu, md.rslot_pid, 0);
+          md.bslot_pid = __shfl_sync(0xffffffffu, md.bslot_pid, 0);
+          if (kind == 0 && a.max_disp > 0.0) {  // engine.hpp:359-365
+            const double c = a.max_disp;
+            md.nx = wrap_axis(__dadd_rn(md.ox, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.x), 1.0), c)), a.b.l);
+            md.ny = wrap_axis(__dadd_rn(md.oy, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.y), 1.0), c)), a.b.l);
+            md.nz = wrap_axis(__dadd_rn(md.oz, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.z), 1.0), c)), a.b.l);
+          }
+        }
+        if (lane == 0) {
+          G.kind = kind;
+          G.empty = empty;
+          G.pid = pid;
+          G.q = q;
+          G.nv = (uint64_t)(nv < 0 ? 0 : nv);
+          G.md = md;
+          G.acc = pr.acc;
+          ws.excl = (kind != 1 && !empty) ? md.bslot_pid : -1;
+          if (kind == 2) {
+            ws.nwin = 1;
+            ws.sign1 = 1;
+            ws.cx[0] = md.ox;
+            ws.cy[0] = md.oy;
+            ws.cz[0] = md.oz;
+          } else {
+            ws.nwin = kind == 0 ? 2 : 1;
+            ws.sign1 = -1;
+            ws.cx[0] = md.nx;
+            ws.cy[0] = md.ny;
+            ws.cz[0] = md.nz;
+            ws.cx[1] = md.ox;
+            ws.cy[1] = md.oy;
+            ws.cz[1] = md.oz;
+          }
+          if (empty) ws.total = 0;
+        }
+        __syncwarp();
+        if (!empty && !all_pairs) win_setup_warp<T>(a.m, a.b, ws, occ_s, lane);
+        // occupancy of the reference cell entered (overflow test): issued now,
+        // consumed after the sums
+        if (lane == 0 && !empty && kind != 2 && !all_pairs)
+          ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
+      }
+      group_sync(bar_id, T);
+      pc.mark(3);  // setup (pid hop + window)
+      // ---- sums
+      double du = 0.0, dw = 0.0;
+      if (!G.empty) {
+        if (all_pairs)
+          allpairs_sums<T>(a.b, a.s.pos, d.n, ws, G.kind == 1 ? -1 : (long long)G.pid, gt, du, dw);
+        else
+          win_sums<T>(a.m, a.b, ws, gt, du, dw);
+      }
+      group_reduce<T>(ws, du, dw, bar_id, gt);
+      pc.mark(4);  // sums + reduce
+      // ---- acceptance bits, conflicts, publish (warp 0)
+      if (gw == 0) {
+        const int kind = G.kind;
+        const MoveData& md = G.md;
+        // read set and conflicts with the previous round's commits (lanes over entries)
+        RW rs;
+        rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
+        rs.pt[1] = kind != 1 && !G.empty ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
+        rs.pt[2] = kNoPoint;  // a deletion's last particle is read by its commit, not here
+        rs.ia = kind != 1 && !G.empty ? (int64_t)G.pid : -1;
+        rs.ib = -1;
+        bool cf = false;
+        if (!G.empty && lane < d.nacc) cf = conflict(a.m, all_pairs, rs, d.acc[lane]);
+        cf = __any_sync(0xffffffffu, cf);
+        du = __shfl_sync(0xffffffffu, du, 0);
+        dw = __shfl_sync(0xffffffffu, dw, 0);
+        uint32_t bits = 0;
+        double pe = 0.0;
+        double rdu = du, rdw = dw;
+        if (G.empty) {
+          rdu = rdw = 0.0;
+        } else if (kind == 1) {
+          pe = exp(__dmul_rn(a.beta, __dsub_rn(a.mu, du)));  // engine.hpp:49
+          const int64_t nj = (int64_t)d.n + lane - kInsSpan / 2;
+          bool ok = false;
+          if (nj >= 0) {
+            const double p = metropolis(__dmul_rn(
+                __ddiv_rn(a.vol, __dmul_rn(a.lambda3, (double)(nj + 1))), pe));
+            ok = G.acc < p;
+          }
+          bits = __ballot_sync(0xffffffffu, ok);
+        } else if (kind == 0) {
+          pe = displacement_acceptance(du, a.beta);
+          bits = G.acc < pe ? 1u : 0u;
+        } else {
+          rdu = -du;
+          rdw = -dw;
+          pe = deletion_acceptance(rdu, G.nv, a.vol, a.beta, a.mu, a.lambda3);
+          bits = G.acc < pe ? 1u : 0u;
+        }
+        // overflow of the commit (occupancies read this round; exact unless cf)
+        bool ovf = false;
+        int cb = -1, bb = -1, ob = 0;
+        if (lane == 0 && !G.empty && kind != 2) {
+          bb = (int)mbrick(a.m, rs.pt[0]);
+          const bool same_b = kind == 0 && (uint32_t)bb == mbrick(a.m, rs.pt[1]);
+          ob = occ_s ? (int)occ_s[bb] : __ldcg(a.m.occ + bb);
+          if (!same_b && ob >= a.m.cap) ovf = true;
+          if (!all_pairs) {
+            cb = cell_of(a.g, md.nx, md.ny, md.nz);
+            const bool same_c = kind == 0 && cb == cell_of(a.g, md.ox, md.oy, md.oz);
+            if (!same_c && ocb >= a.g.cap) ovf = true;
+          }
+        }
+        ovf = __shfl_sync(0xffffffffu, ovf, 0);
+        const uint32_t flags = (uint32_t)kind | (cf ? kFConflict : 0u) | (ovf ? kFOverflow : 0u) |
+                               (G.empty ? kFEmpty : 0u);
+        if (lane < 6) {
+          uint64_t p;
+          switch (lane) {
+            case 0: p = (uint64_t)flags | ((uint64_t)bits << 16); break;
+            case 1: p = rs.pt[0]; break;
+            case 2: p = rs.pt[1]; break;
+            case 3: p = rs.pt[2]; break;
+            case 4:
+              p = (uint64_t)(rs.ia < 0 ? 0xffffffffu : (uint32_t)rs.ia) |
+                  ((uint64_t)G.i << 32) | ((uint64_t)G.v << 38);
+              break;
+            default: p = (uint32_t)(rs.ib < 0 ? 0xffffffffu : (uint32_t)rs.ib); break;
+          }
+          st_relaxed(rw + lane, tagw(r, p));
+        }
+        pc.mark(5);  // bits + publish
+        // off the critical path: payload, then its own tag after a release
+        if (lane == 0) {
+          ex->du = rdu;
+          ex->dw = rdw;
+          ex->pe = pe;
+          ex->md = md;
+          ex->cb = cb;
+          ex->ocb = ocb;
+          ex->bb = bb;
+          ex->obb = ob;
+          fence_gpu();
+          st_relaxed(&ex->tag, (uint64_t)r);
+        }
+      }
+    }
+    // warp 0: prefix for the next round and ring refill (off the critical path)
+    if (tid < 32) {
+      b0 = d.base;
+      const uint64_t want = b0 + kRing < a.nmoves ? b0 + kRing : a.nmoves;
+      prefix_warp(a, sh.ring, b0, sh.Q, lane);
+      __syncwarp();
+      if (want > ring_hi) {
+        ring_fill(a, sh.ring, ring_hi, want, lane);
+        ring_hi = want;
+      }
+    }
+    pc.mark(6);
+  }
+  if (a.prof && blockIdx.x == 1 && tid == 0) {
+    pc.flush(a.prof + 16);
+    a.prof[16 + 15] = r;
+  }
+}
+
+// =================================================================== sequencer
+struct Round {  // a decided round, handed to the helper warps
+  uint64_t base, n;
+  uint32_t r;
+  int len, nacc, par;
+  int acc_i[kMaxAcc], acc_s[kMaxAcc], acc_n[kMaxAcc], acc_kind[kMaxAcc];
+  uint32_t acc_pid[kMaxAcc];
+  int res_s[kMaxMoves], res_d[kMaxMoves];
+  uint8_t kind[kMaxMoves], empty[kMaxMoves];
+};
+
+enum Stop { kStopEnd, kStopVariant, kStopPrev, kStopVerify, kStopFull, kStopOverflow, kNStop };
+
+struct SeqShared {
+  Proposal ring[kRing];
+  uint64_t sw[kMaxSlots][6];  // slot words of the current round (payload)
+  int Q[kPre];
+  int fit, used;
+  // per-move masks built by the pollers
+  uint32_t macc[kMaxMoves], mcf[kMaxMoves], mov[kMaxMoves];
+  uint8_t mkind[kMaxMoves];
+  // walk output
+  int len, nacc, err, cmin, err_slot, why;
+  int acc_i[kMaxAcc], acc_s[kMaxAcc], acc_d[kMaxAcc];
+  int res_s[kMaxMoves];  // resolved slot of each consumed move
+  int res_d[kMaxMoves];  // N offset at each consumed move
+  Round done;            // previous round, processed by the helpers
+  double acc_du[kMaxAcc], acc_dw[kMaxAcc];
+  unsigned long long stops[kNStop];
+  ChainState ks;
+};
+
+__device__ __forceinline__ RW rw_of(const uint64_t* w) {
+  RW x;
+  x.pt[0] = w[1];
+  x.pt[1] = w[2];
+  x.pt[2] = w[3];
+  const uint32_t ia = (uint32_t)w[4], ib = (uint32_t)w[5];
+  x.ia = ia == 0xffffffffu ? -1 : (int64_t)ia;
+  x.ib = ib == 0xffffffffu ? -1 : (int64_t)ib;
+  return x;
 }
 
 struct Observables {
@@ -86,321 +692,458 @@ __device__ __forceinline__ Observables observables(const EngineArgs& a, uint64_t
   return {ru, p};
 }
 
-struct Eval {
-  int kind;
-  int flag;
-  int empty;
-  int pad;
-  uint64_t pid;
-  double du, dw, p, acc;
-  double4 old;
-  double nx, ny, nz;
-};
+// One warp: decision D_r (base, N, the previous round's accepted moves).
+// No fence here: the helpers fenced their commit stores before the barrier
+// that precedes this call, so every commit is in L2 before any D word is.
+__device__ __forceinline__ void publish(const EngineArgs& a, uint32_t r, uint64_t base,
+                                        uint64_t n, int nacc, int bias, int stop, int rate,
+                                        const SeqShared& sh, int lane) {
+  for (int idx = lane; idx < kDecHdr + kDecEnt * nacc; idx += 32) {
+    uint64_t p = 0;
+    if (idx == 0) p = base;
+    else if (idx == 1) p = n;
+    else if (idx == 2)
+      p = (uint64_t)nacc | ((uint64_t)(bias > 0) << 8) | ((uint64_t)stop << 9) |
+          ((uint64_t)(uint16_t)(int16_t)rate << 10);
+    else if (idx >= kDecHdr) {
+      const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
+      const uint64_t* w = sh.sw[sh.acc_s[e]];
+      const int kind = (int)(w[0] & 3);
+      if (f < 3) p = w[1 + f];
+      else if (f == 3) p = ((uint64_t)kind << 32) | (kind == 1 ? (uint32_t)sh.acc_d[e] : (uint32_t)w[4]);
+      else p = (uint32_t)w[5];
+    }
+    st_relaxed(a.dec + idx, tagw(r, p));
+  }
+}
 
-// One move, one group of T threads. Warp 0 of the group builds the move
-// context from the prefetched proposal (pid, old position, target, window
-// runs); the group's last warp prefetches the commit plan; every thread scans
-// its window rows; the leader finishes the acceptance test.
-template <int T>
-__device__ __forceinline__ void evaluate(const EngineArgs& a, const Proposal& pr, uint64_t n,
-                                         MoveCtx& ctx, GroupReduce<T>& red, CommitPlan& cp,
-                                         Eval& ev, int bar_id, unsigned long long* ep) {
-  const int gt = threadIdx.x % T, lane = threadIdx.x & 31, gw = gt >> 5;
-  unsigned long long t0 = 0;
-  if (ep && threadIdx.x == 0) t0 = gtimer();
-  if (gw == 0) {
-    if (lane == 0) {
-      ev.kind = pr.kind;
-      ev.flag = 0;
-      ev.pid = 0;
-      ev.du = ev.dw = ev.p = 0.0;
-      ev.old = make_double4(0, 0, 0, 0);
-      ev.nx = pr.x;
-      ev.ny = pr.y;
-      ev.nz = pr.z;
-      ev.acc = pr.acc;
-      ctx.np = 1;
-      ctx.exclude = (long long)n;
-      ctx.x[0] = pr.x;
-      ctx.y[0] = pr.y;
-      ctx.z[0] = pr.z;
-      ev.empty = (pr.kind != 1 && n == 0);  // counted rejection (engine.hpp:355,399)
-      if (!ev.empty && pr.kind != 1) {
-        ev.pid = index_from(pr.pick, n);
-        ev.old = ld_cg(a.pos + ev.pid);
-        ctx.exclude = (long long)ev.pid;
-        if (pr.kind == 0) {
-          if (a.max_disp > 0.0) {  // engine.hpp:359-365
-            const double c = a.max_disp;
-            ev.nx = wrap_axis(__dadd_rn(ev.old.x, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.x), 1.0), c)), a.b.l);
-            ev.ny = wrap_axis(__dadd_rn(ev.old.y, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.y), 1.0), c)), a.b.l);
-            ev.nz = wrap_axis(__dadd_rn(ev.old.z, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.z), 1.0), c)), a.b.l);
-          }
-          ctx.np = 2;
-          ctx.x[0] = ev.nx;
-          ctx.y[0] = ev.ny;
-          ctx.z[0] = ev.nz;
-          ctx.x[1] = ev.old.x;
-          ctx.y[1] = ev.old.y;
-          ctx.z[1] = ev.old.z;
-        } else {
-          ctx.x[0] = ev.old.x;
-          ctx.y[0] = ev.old.y;
-          ctx.z[0] = ev.old.z;
-        }
+// Helper warps (kPollWarps .. 15): commits, statistics and trace of the
+// round in sh.done, while the poll warps wait for the next round.
+__device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) {
+  const Round& D = sh.done;
+  if (D.len == 0) return;
+  auto ext_of = [&](int s) -> const SlotExt* {
+    const SlotExt* ex = a.ext + (size_t)D.par * a.nslots + s;
+    while (ld_acquire(&ex->tag) != (uint64_t)D.r) nap();
+    return ex;
+  };
+  if (warp == kPollWarps) {  // commits (commit.cuh): one lane per accepted move
+    // All lanes load their commit's inputs in parallel; a commit whose
+    // cells / bricks / particles overlap an earlier one of the round is
+    // re-loaded and applied after it, in move order; the rest apply at once.
+    const bool mine = lane < D.nacc;
+    MoveData md{};
+    CommitIn c{};
+    Touch t{};
+    int kind = 0;
+    uint64_t pid = 0, nn = 0;
+    if (mine) {
+      const SlotExt* ex = ext_of(D.acc_s[lane]);
+      md = ex->md;
+      kind = D.acc_kind[lane];
+      pid = D.acc_pid[lane];
+      nn = (uint64_t)D.acc_n[lane];
+      commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
+      t = touch_of(a.m, kind, pid, nn, c);
+    }
+    bool dep = false;
+    for (int j = 0; j < D.nacc - 1; ++j) {  // does my commit overlap commit j < lane?
+      Touch tj;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        tj.cell[x] = __shfl_sync(0xffffffffu, t.cell[x], j);
+        tj.brick[x] = __shfl_sync(0xffffffffu, t.brick[x], j);
       }
+#pragma unroll
+      for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, t.part[x], j);
+      if (mine && j < lane && touches(t, tj)) dep = true;
+    }
+    long long e1, e2, e3;
+    if (mine && !dep) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+    const unsigned deps = __ballot_sync(0xffffffffu, dep);
+    if (deps) {
+      __threadfence();  // independent commits are in L2 before the ordered ones reload
+      __syncwarp();
+      for (int j = 0; j < D.nacc; ++j) {
+        if (((deps >> j) & 1u) && lane == j)
+          commit_move(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, e1, e2, e3);
+        __syncwarp();
+      }
+    }
+    if (mine) fence_gpu();  // every commit is in L2 before the next decision is published
+  } else if (warp == kPollWarps + 1) {  // statistics (engine.hpp:293-308, 413-426)
+    if (lane < D.nacc) {
+      const SlotExt* ex = ext_of(D.acc_s[lane]);
+      sh.acc_du[lane] = ex->du;
+      sh.acc_dw[lane] = ex->dw;
     }
     __syncwarp();
-    setup_runs(a.g, a.b, ctx);
-  }
-  if (ep && threadIdx.x == 0) { const unsigned long long t = gtimer(); ep[0] += t - t0; t0 = t; }
-  group_sync(bar_id, T);
-  if (ep && threadIdx.x == 0) { const unsigned long long t = gtimer(); ep[1] += t - t0; t0 = t; }
-  if (ev.empty) return;  // uniform across the group
-  if (gw == T / 32 - 1)
-    commit_prefetch(a.g, a.pos, n, ev.kind, ev.pid, ev.old, ev.nx, ev.ny, ev.nz, cp);
-  double du, dw;
-  {
-    const int gt2 = threadIdx.x % T;
-    du = 0.0;
-    dw = 0.0;
-    if (a.g.kind == GCMC_MICROCELL)
-      sums_microcell<T>(a.g, a.b, ctx, gt2, du, dw);
-    else if (a.g.kind == GCMC_CELL_LIST)
-      sums_cell_list<T>(a.g, a.b, ctx, gt2, du, dw);
-    else
-      sums_all_pairs<T>(a.b, a.pos, n, ctx, gt2, du, dw);
-    if (ep && threadIdx.x == 0) { const unsigned long long t = gtimer(); ep[2] += t - t0; t0 = t; }
-    group_reduce2<T>(du, dw, red, bar_id);
-    if (ep && threadIdx.x == 0) { const unsigned long long t = gtimer(); ep[3] += t - t0; t0 = t; }
-  }
-  if (gt == 0) {
-    if (ev.kind == 0) {
-      ev.du = du;
-      ev.dw = dw;
-      ev.p = displacement_acceptance(du, a.beta);
-    } else if (ev.kind == 1) {
-      ev.du = du;
-      ev.dw = dw;
-      ev.p = insertion_acceptance(du, n, a.vol, a.beta, a.mu, a.lambda3);
-    } else {
-      ev.du = -du;
-      ev.dw = -dw;
-      ev.p = deletion_acceptance(ev.du, n, a.vol, a.beta, a.mu, a.lambda3);
-    }
-    ev.flag = ev.acc < ev.p;
-  }
-}
-
-__device__ __forceinline__ bool sampled(const EngineArgs& a, uint64_t step) {
-  return step > a.equil && (a.interval == 1 || (step - a.equil) % a.interval == 0);
-}
-
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
-}
-
-// K-bit rotate right (move order from group order).
-__device__ __forceinline__ uint64_t rotr(uint64_t v, int s, int K) {
-  const uint64_t mask = K == 64 ? ~0ull : ((1ull << K) - 1);
-  if (s == 0) return v & mask;
-  return ((v >> s) | (v << (K - s))) & mask;
-}
-
-template <int M>
-__global__ void __launch_bounds__(512, 1) k_engine(EngineArgs a) {
-  constexpr int T = 512 / M;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int g = tid / T, gt = tid % T, gw = gt >> 5;
-  const int rank = (int)cluster.block_rank();
-  const int C = (int)cluster.num_blocks();
-  const int K = C * M;  // <= 64
-  const int G = rank * M + g;
-  const int bar_id = 1 + g;
-  __shared__ uint32_t flagw[2];  // group g: bit 4g accept, bits 4g+1..2 kind; bit 31 stop
-  __shared__ Eval ev[M];
-  __shared__ MoveCtx ctx[M];
-  __shared__ GroupReduce<T> red[M];
-  __shared__ CommitPlan cp[M];
-  __shared__ ChainState ks;  // bookkeeper's copy (CTA 0)
-
-  uint64_t n = __ldcg(&a.st->n);
-  const bool keeper = rank == 0 && tid >= 32 && tid < 64;
-  if (keeper && lane == 0) ks = *a.st;
-  if (tid == 0) flagw[0] = flagw[1] = 0;
-  // group-owned move and its proposals (leader registers)
-  uint64_t mg = (uint64_t)G;
-  Proposal cur, nxt;
-  if (gt == 0) {
-    if (mg < a.nmoves) cur = a.props[mg];
-    if (mg + K < a.nmoves) nxt = a.props[mg + K];
-  }
-  cluster.sync();
-
-  uint64_t base = 0, rounds = 0;
-  unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned long long ep[4] = {0, 0, 0, 0};
-  unsigned long long tl = a.prof ? gtimer() : 0;
-  auto mark = [&](int ph) {
-    if (a.prof && tid == 0) {
-      const unsigned long long t = gtimer();
-      tp[ph] += t - tl;
-      tl = t;
-    }
-  };
-  while (base < a.nmoves) {
-    const int par = (int)(rounds & 1);
-    if (tid == 0) flagw[par ^ 1] = 0;
-    const bool active = mg < a.nmoves;
-    if (active) {
-      evaluate<T>(a, cur, n, ctx[g], red[g], cp[g], ev[g], bar_id, a.prof ? ep : nullptr);
-      mark(0);
-      if (gt == 0)
-        atomicOr(&flagw[par], ((uint32_t)ev[g].flag | ((uint32_t)ev[g].kind << 1)) << (4 * g));
-    }
-    cluster_arrive();  // B1
-    mark(1);
-    cluster_wait();
-    mark(2);
-    // ---- decide: move-order masks from the C flag words
-    uint32_t fw = 0;
-    if (lane < C) fw = *cluster.map_shared_rank(&flagw[par], lane);
-    if (__any_sync(0xffffffffu, (fw >> 31) & 1u)) break;  // a commit failed last round
-    uint64_t acc = 0, k0 = 0, k1 = 0;
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-      const uint64_t bit = 1ull << (lane * M + q);
-      if (lane < C) {
-        if ((fw >> (4 * q)) & 1u) acc |= bit;
-        if ((fw >> (4 * q + 1)) & 1u) k0 |= bit;
-        if ((fw >> (4 * q + 2)) & 1u) k1 |= bit;
-      }
-    }
-    auto or64 = [](uint64_t v) {
-      const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
-      const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
-      return ((uint64_t)hi << 32) | lo;
-    };
-    acc = or64(acc);
-    k0 = or64(k0);
-    k1 = or64(k1);
-    const int off = (int)(base % (uint64_t)K);
-    const uint64_t valid = min((uint64_t)K, a.nmoves - base);
-    const uint64_t vmask = valid >= 64 ? ~0ull : ((1ull << valid) - 1);
-    const uint64_t racc = rotr(acc, off, K) & vmask;
-    uint64_t len = valid;
-    int j = -1, jG = -1, dn = 0, jkind = 0;
-    if (racc) {
-      j = __ffsll((long long)racc) - 1;
-      len = (uint64_t)j + 1;
-      jG = (off + j) % K;
-      jkind = (int)(((k0 >> jG) & 1ull) | (((k1 >> jG) & 1ull) << 1));
-      dn = jkind == 1 ? 1 : (jkind == 2 ? -1 : 0);
-    }
-    const int my_off = (G - off + K) % K;
-    mark(3);
-    // ---- commit (group jG's leader; plan prefetched during evaluation)
-    if (jG == G && gt == 0) {
-      const Eval& e = ev[g];
-      const int s = commit_apply(a.g, a.pos, a.st, n, e.kind, e.pid, e.nx, e.ny, e.nz, cp[g]);
-      if (s != GCMC_OK) {
-        a.st->error = s;
-        a.st->err_a = cp[g].e1;
-        a.st->err_b = cp[g].e2;
-        a.st->err_c = (long long)(base + j);
-        atomicOr(&flagw[par ^ 1], 0x80000000u);
-      }
-    }
-    // ---- trace + advance of consumed groups
-    const bool consumed = active && (uint64_t)my_off < len;
-    if (gt == 0 && consumed) {
-      if (a.trace) {
-        gcmc_trace_rec t;
-        t.kind = ev[g].kind;
-        t.accepted = jG == G;
-        t.delta_u = ev[g].du;
-        t.delta_w = ev[g].dw;
-        t.acceptance_prob = ev[g].p;
-        t.n_after = n + (jG == G ? (int64_t)dn : 0);
-        a.trace[mg] = t;
-      }
-      cur = nxt;
-      if (mg + 2 * K < a.nmoves) nxt = a.props[mg + 2 * K];
-    }
-    if (consumed) mg += K;  // every thread of the group tracks its move
-    if (keeper) {  // engine.hpp:293-308, 413-426
-      double jdu = 0.0, jdw = 0.0;
-      if (jG >= 0 && lane == 0) {
-        const Eval* re = cluster.map_shared_rank(&ev[jG % M], jG / M);
-        jdu = re->du;
-        jdw = re->dw;
-      }
-      if (lane == 0) {
-        const uint64_t lm = len >= 64 ? ~0ull : ((1ull << len) - 1);
-        const int c1 = __popcll(rotr(k0, off, K) & lm), c2 = __popcll(rotr(k1, off, K) & lm);
-        ks.attempted[0] += len - c1 - c2;
-        ks.attempted[1] += c1;
-        ks.attempted[2] += c2;
-        const uint64_t pre = j >= 0 ? len - 1 : len;  // steps sampled in the pre-move state
-        uint64_t step = ks.step, samples = ks.samples;
-        double sum_n = ks.sum_n, sum_n2 = ks.sum_n2, sum_u = ks.sum_u, sum_p = ks.sum_p;
-        if (pre) {
-          const Observables ob = observables(a, n, ks.energy, ks.virial);
-          const double nd = (double)n, nd2 = __dmul_rn(nd, nd);
-          for (uint64_t t = 0; t < pre; ++t) {
-            if (sampled(a, step + t + 1)) {
-              ++samples;
-              sum_n = __dadd_rn(sum_n, nd);
-              sum_n2 = __dadd_rn(sum_n2, nd2);
-              sum_u = __dadd_rn(sum_u, ob.rep_u);
-              sum_p = __dadd_rn(sum_p, ob.pres);
-            }
-          }
+    if (lane == 0) {
+      ChainState& ks = sh.ks;
+      uint64_t step = ks.step, samples = ks.samples;
+      uint64_t att0 = 0, att1 = 0, att2 = 0;
+      double sum_n = ks.sum_n, sum_n2 = ks.sum_n2, sum_u = ks.sum_u, sum_p = ks.sum_p;
+      double energy = ks.energy, virial = ks.virial;
+      uint64_t cur = D.n;
+      Observables ob = observables(a, cur, energy, virial);
+      double nd = (double)cur, nd2 = __dmul_rn(nd, nd);
+      // sampled(step) = step > equil && (step - equil) % interval == 0, tracked incrementally
+      uint64_t rem = step > a.equil ? (step - a.equil) % a.interval : 0;
+      int k = 0;
+      for (int i = 0; i < D.len; ++i) {
+        const int kind = D.kind[i];
+        att0 += kind == 0;
+        att1 += kind == 1;
+        att2 += kind == 2;
+        if (k < D.nacc && D.acc_i[k] == i) {
+          energy = __dadd_rn(energy, sh.acc_du[k]);
+          virial = __dadd_rn(virial, sh.acc_dw[k]);
+          ++ks.accepted[kind];
+          cur = kind == 1 ? cur + 1 : (kind == 2 ? cur - 1 : cur);
+          ob = observables(a, cur, energy, virial);
+          nd = (double)cur;
+          nd2 = __dmul_rn(nd, nd);
+          ++k;
         }
-        step += pre;
-        if (j >= 0) {
-          ks.energy = __dadd_rn(ks.energy, jdu);
-          ks.virial = __dadd_rn(ks.virial, jdw);
-          ++ks.accepted[jkind];
-          const uint64_t n2 = n + dn;
-          ++step;
-          if (sampled(a, step)) {
-            const Observables ob = observables(a, n2, ks.energy, ks.virial);
-            const double m1 = (double)n2;
+        ++step;
+        if (step > a.equil) {
+          rem = step == a.equil + 1 ? (a.interval == 1 ? 0 : 1) : (rem + 1 == a.interval ? 0 : rem + 1);
+          if (rem == 0) {
             ++samples;
-            sum_n = __dadd_rn(sum_n, m1);
-            sum_n2 = __dadd_rn(sum_n2, __dmul_rn(m1, m1));
+            sum_n = __dadd_rn(sum_n, nd);
+            sum_n2 = __dadd_rn(sum_n2, nd2);
             sum_u = __dadd_rn(sum_u, ob.rep_u);
             sum_p = __dadd_rn(sum_p, ob.pres);
           }
         }
-        ks.step = step;
-        ks.samples = samples;
-        ks.sum_n = sum_n;
-        ks.sum_n2 = sum_n2;
-        ks.sum_u = sum_u;
-        ks.sum_p = sum_p;
+      }
+      ks.attempted[0] += att0;
+      ks.attempted[1] += att1;
+      ks.attempted[2] += att2;
+      ks.step = step;
+      ks.samples = samples;
+      ks.sum_n = sum_n;
+      ks.sum_n2 = sum_n2;
+      ks.sum_u = sum_u;
+      ks.sum_p = sum_p;
+      ks.energy = energy;
+      ks.virial = virial;
+    }
+  } else if (a.trace) {  // trace records (MoveOutcome, engine.hpp:104-110)
+    const int nt = (kThreads / 32 - kPollWarps - 2) * 32;
+    for (int i = (warp - kPollWarps - 2) * 32 + lane; i < D.len; i += nt) {
+      const int s = D.res_s[i];
+      const SlotExt* ex = ext_of(s);
+      const int kind = D.kind[i];
+      int accepted = 0, dn = 0;
+      for (int k = 0; k < D.nacc; ++k) {
+        if (D.acc_i[k] == i) accepted = 1;
+        if (D.acc_i[k] <= i) dn += D.acc_kind[k] == 1 ? 1 : (D.acc_kind[k] == 2 ? -1 : 0);
+      }
+      const uint64_t nm = (uint64_t)((int64_t)D.n + D.res_d[i]);
+      gcmc_trace_rec t;
+      t.kind = kind;
+      t.accepted = accepted;
+      t.delta_u = ex->du;
+      t.delta_w = ex->dw;
+      double p = ex->pe;
+      if (kind == 1)
+        p = metropolis(__dmul_rn(__ddiv_rn(a.vol, __dmul_rn(a.lambda3, (double)(nm + 1))), ex->pe));
+      if (D.empty[i]) p = 0.0;
+      t.acceptance_prob = p;
+      t.n_after = (uint64_t)((int64_t)D.n + dn);
+      a.trace[D.base + i] = t;
+    }
+  }
+}
+
+__device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
+  auto& sh = *reinterpret_cast<SeqShared*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool all_pairs = a.g.kind == GCMC_ALL_PAIRS;
+  constexpr int kPollThreads = kPollWarps * 32;
+  if (tid == 0) {
+    sh.ks = *a.st;
+    sh.done.len = 0;
+    sh.err = 0;
+    for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
+  }
+  if (tid < kMaxMoves) {
+    sh.macc[tid] = sh.mcf[tid] = sh.mov[tid] = 0;
+  }
+  uint64_t ring_hi = a.nmoves < (uint64_t)kRing ? a.nmoves : (uint64_t)kRing;
+  if (warp == 0) {
+    ring_fill(a, sh.ring, 0, ring_hi, lane);
+    cp_async_wait();
+    __syncwarp();
+    prefix_warp(a, sh.ring, 0, sh.Q, lane);
+    __syncwarp();
+    if (lane == 0) round_shape(a, sh.Q, 0, 0, sh.fit, sh.used);
+  }
+  __syncthreads();
+  uint64_t base = 0, n = sh.ks.n;
+  int bias = a.bias0;
+  uint64_t rounds = 0;
+  uint32_t r = 1;
+  int rate = 0;         // drift of N per move, 1/256 units
+  float rate_f = 0.0f;
+  if (warp == 0) publish(a, r, base, n, 0, bias, 0, rate, sh, lane);
+  PhaseClock pc, ph;
+  pc.start(a.prof && tid == 0);
+  ph.start(a.prof && tid == kPollWarps * 32);
+  for (;;) {
+    const int par = (int)(r & 1);
+    if (warp < kPollWarps) {
+      // -------------------- poll: slot words + per-move masks
+      const int used = sh.used;
+      if (tid < used) {
+        const uint64_t* rw = a.res + ((size_t)par * a.nslots + tid) * kResWords;
+        uint64_t w[6];
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            w[j] = ld_relaxed(rw + j);
+            ok &= tagged(w[j], r);
+          }
+          if (ok) break;
+          __nanosleep(a.poll_ns);
+        }
+#pragma unroll
+        for (int j = 0; j < 6; ++j) sh.sw[tid][j] = w[j] & kPay;
+        const uint32_t w0 = (uint32_t)w[0];
+        const uint32_t bits = (uint32_t)((w[0] & kPay) >> 16);
+        const int i = (int)((w[4] >> 32) & 63), v = (int)((w[4] >> 38) & 31);
+        const int kind = (int)(w0 & 3);
+        if (v == 0) sh.mkind[i] = (uint8_t)kind;
+        if (kind == 1) {
+          sh.macc[i] = bits;
+          sh.mcf[i] = (w0 & kFConflict) ? 1u : 0u;
+          sh.mov[i] = (w0 & kFOverflow) ? 1u : 0u;
+        } else {
+          if (bits & 1u) atomicOr(&sh.macc[i], 1u << v);
+          if (w0 & kFConflict) atomicOr(&sh.mcf[i], 1u << v);
+          if (w0 & kFOverflow) atomicOr(&sh.mov[i], 1u << v);
+        }
+      }
+      group_sync(1, kPollThreads);
+      pc.mark(1);  // poll (waiting for the evaluators)
+      if (warp == 0) {  // ---- walk
+        const int fit = sh.fit;
+        uint32_t accm[2], cfm[2], ovm[2];
+        int kind[2], cntv[2], fs[2];
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          accm[h] = cfm[h] = ovm[h] = 0;
+          kind[h] = cntv[h] = fs[h] = 0;
+          if (i < fit) {
+            accm[h] = sh.macc[i];
+            cfm[h] = sh.mcf[i];
+            ovm[h] = sh.mov[i];
+            kind[h] = sh.mkind[i];
+            cntv[h] = (i == 0 || kind[h] == 1) ? 1 : a.nvar;
+            fs[h] = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
+          }
+        }
+        pc.mark(6);  // walk: masks
+        int d = 0, start = 0, nacc = 0, len = fit, err = 0, eslot = -1, why = kStopEnd;
+        for (;;) {
+          bool ev[2], stp[2];
+          int slot[2], vi[2], why_l[2];
+          for (int h = 0; h < 2; ++h) {
+            const int i = lane + 32 * h;
+            ev[h] = stp[h] = false;
+            slot[h] = -1;
+            vi[h] = 0;
+            why_l[h] = kStopEnd;
+            if (i >= start && i < fit) {
+              bool acc = false, st = false;
+              if (kind[h] == 1) {
+                const int j = d + kInsSpan / 2;
+                if (j < 0 || j >= kInsSpan) { st = true; why_l[h] = kStopVariant; }
+                else if (cfm[h]) { st = true; why_l[h] = kStopPrev; }
+                else acc = (accm[h] >> j) & 1u;
+              } else {
+                vi[h] = var_of(d - var_centre(rate, i), bias);
+                if (vi[h] >= cntv[h]) { st = true; why_l[h] = kStopVariant; }
+                else if ((cfm[h] >> vi[h]) & 1u) { st = true; why_l[h] = kStopPrev; }
+                else acc = (accm[h] >> vi[h]) & 1u;
+              }
+              if (!st) {
+                slot[h] = fs[h] + (kind[h] == 1 ? 0 : vi[h]);
+                sh.res_s[i] = slot[h];
+                sh.res_d[i] = d;
+              }
+              stp[h] = st;
+              ev[h] = st || acc;
+            }
+          }
+          const unsigned b0 = __ballot_sync(0xffffffffu, ev[0]);
+          const unsigned b1 = __ballot_sync(0xffffffffu, ev[1]);
+          if (!b0 && !b1) {
+            len = fit;
+            why = kStopEnd;
+            break;
+          }
+          const int e = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
+          const int eh = e >> 5, el = e & 31;
+          const bool est = __shfl_sync(0xffffffffu, eh ? stp[1] : stp[0], el);
+          if (est) {
+            len = e;
+            why = __shfl_sync(0xffffffffu, eh ? why_l[1] : why_l[0], el);
+            break;
+          }
+          const int es = __shfl_sync(0xffffffffu, eh ? slot[1] : slot[0], el);
+          const int ek = __shfl_sync(0xffffffffu, eh ? kind[1] : kind[0], el);
+          const int eo = __shfl_sync(0xffffffffu,
+                                     (int)(eh ? (ovm[1] >> (kind[1] == 1 ? 0 : vi[1])) & 1u
+                                              : (ovm[0] >> (kind[0] == 1 ? 0 : vi[0])) & 1u), el);
+          if (eo) {  // the reference throws inside the commit of move e
+            len = e;
+            err = 1;
+            eslot = es;
+            why = kStopOverflow;
+            break;
+          }
+          if (lane == 0) {
+            sh.acc_i[nacc] = e;
+            sh.acc_s[nacc] = es;
+            sh.acc_d[nacc] = (int)((int64_t)n + d);  // store size before move e
+          }
+          ++nacc;
+          d += ek == 1 ? 1 : (ek == 2 ? -1 : 0);
+          start = e + 1;
+          if (nacc == kMaxAcc) {
+            len = e + 1;
+            why = kStopFull;
+            break;
+          }
+        }
+        pc.mark(7);  // walk: iterations
+        if (lane == 0) {
+          sh.len = len;
+          sh.nacc = nacc;
+          sh.cmin = len;
+          sh.err = err;
+          sh.err_slot = eslot;
+          sh.why = why;
+        }
+      }
+      group_sync(1, kPollThreads);
+      pc.mark(2);  // walk
+      {  // ---- verify: every consumed move against the accepted moves before it
+        const int len = sh.len, nacc = sh.nacc;
+        const int i = tid & 63;
+        if (i < len)
+          for (int j = tid >> 6; j < nacc; j += kPollThreads / 64) {
+            if (i <= sh.acc_i[j]) continue;
+            const RW ri = rw_of(sh.sw[sh.res_s[i]]);
+            RW wj = rw_of(sh.sw[sh.acc_s[j]]);
+            if ((sh.sw[sh.acc_s[j]][0] & 3) == 1) wj.ia = sh.acc_d[j];  // insertion index
+            if (conflict(a.m, all_pairs, ri, wj)) atomicMin(&sh.cmin, i);
+          }
+      }
+      group_sync(1, kPollThreads);
+      pc.mark(3);  // verify
+      if (tid == 0 && sh.cmin < sh.len) {
+        const int c = sh.cmin;
+        sh.len = c;
+        int k = 0;
+        while (k < sh.nacc && sh.acc_i[k] < c) ++k;
+        sh.nacc = k;
+        sh.err = 0;  // the overflowing move is not reached this round
+        sh.why = kStopVerify;
+      }
+    } else {
+      helpers(a, sh, warp, lane);  // previous round, concurrently with the poll
+      ph.mark(0);
+    }
+    __syncthreads();
+    pc.mark(4);  // wait for helpers
+    // -------------------- close the round
+    const int len = sh.len, nacc = sh.nacc;
+    int dn = 0;
+    for (int k = 0; k < nacc; ++k) {
+      const int kd = (int)(sh.sw[sh.acc_s[k]][0] & 3);
+      dn += kd == 1 ? 1 : (kd == 2 ? -1 : 0);
+    }
+    const uint64_t nbase = base + (uint64_t)len;
+    const uint64_t nn = (uint64_t)((int64_t)n + dn);
+    if (dn != 0) bias = dn > 0 ? 1 : -1;
+    if (len > 0) {  // exponential average of the drift of N per move
+      rate_f = 0.9f * rate_f + 0.1f * (float)dn / (float)len;
+      int rr = __float2int_rn(rate_f * 256.0f);
+      rate = rr < -128 ? -128 : (rr > 128 ? 128 : rr);
+    }
+    const bool stop = nbase >= a.nmoves || sh.err;
+    if (warp == 0) {
+      publish(a, r + 1, nbase, nn, nacc, bias, stop, rate, sh, lane);
+    } else if (warp == 1 || warp == 2) {  // hand the round to the helpers
+      Round& D = sh.done;
+      const int i = tid - 32;
+      if (i < len) {
+        D.res_s[i] = sh.res_s[i];
+        D.res_d[i] = sh.res_d[i];
+        const uint64_t w0 = sh.sw[sh.res_s[i]][0];
+        D.kind[i] = (uint8_t)(w0 & 3);
+        D.empty[i] = (uint8_t)((w0 & kFEmpty) ? 1 : 0);
+      }
+      if (i < nacc) {
+        const uint64_t* w = sh.sw[sh.acc_s[i]];
+        D.acc_i[i] = sh.acc_i[i];
+        D.acc_s[i] = sh.acc_s[i];
+        D.acc_n[i] = sh.acc_d[i];
+        D.acc_kind[i] = (int)(w[0] & 3);
+        D.acc_pid[i] = (uint32_t)w[4];
+      }
+      if (i == 0) {
+        D.base = base;
+        D.n = n;
+        D.r = r;
+        D.len = len;
+        D.nacc = nacc;
+        D.par = par;
+        ++sh.stops[sh.why];
       }
     }
-    mark(4);
-    cluster_arrive();  // B2
-    mark(5);
-    cluster_wait();
-    mark(6);
-    base += len;
-    n += dn;
+    __syncthreads();
+    // next round's shape, masks, ring (while the evaluators work)
+    if (warp == 0) {
+      const uint64_t want = nbase + kRing < a.nmoves ? nbase + kRing : a.nmoves;
+      prefix_warp(a, sh.ring, nbase, sh.Q, lane);
+      __syncwarp();
+      if (lane == 0) round_shape(a, sh.Q, 0, nbase, sh.fit, sh.used);
+      if (want > ring_hi) {
+        ring_fill(a, sh.ring, ring_hi, want, lane);
+        ring_hi = want;
+      }
+      cp_async_wait();
+    } else if (tid < 32 + kMaxMoves) {
+      sh.macc[tid - 32] = sh.mcf[tid - 32] = sh.mov[tid - 32] = 0;
+    }
+    __syncthreads();
+    pc.mark(5);  // close + publish + next shape
+    ph.mark(1);
+    base = nbase;
+    n = nn;
     ++rounds;
+    ++r;
+    if (stop) break;
   }
-  if (a.prof && tid == 0)
-    for (int k = 0; k < 8; ++k) a.prof[rank * 16 + k] = tp[k];
-  if (a.prof && tid == 0)
-    for (int k = 0; k < 4; ++k) a.prof[rank * 16 + 9 + k] = ep[k];
-  if (a.prof && tid == 0) a.prof[rank * 16 + 8] = rounds;
-  if (keeper && lane == 0) {
+  // the last round's commits / statistics / trace
+  if (warp >= kPollWarps) helpers(a, sh, warp, lane);
+  __syncthreads();
+  if (a.prof && tid == 0) {
+    pc.flush(a.prof);
+    a.prof[15] = rounds;
+    for (int k = 0; k < kNStop; ++k) a.prof[40 + k] = sh.stops[k];
+  }
+  if (a.prof && tid == kPollWarps * 32) {
+    a.prof[32] = ph.acc[0];
+    a.prof[33] = ph.acc[1];
+  }
+  if (tid == 0) {
+    ChainState& ks = sh.ks;
     a.st->n = n;
     a.st->step = ks.step;
     a.st->energy = ks.energy;
@@ -416,8 +1159,25 @@ __global__ void __launch_bounds__(512, 1) k_engine(EngineArgs a) {
     a.st->sum_n2 = ks.sum_n2;
     a.st->moves_done = base;
     a.st->rounds = rounds;
+    if (sh.err) {  // overflow at move `base`: report the cell as insert_id would
+      const SlotExt* ex = a.ext + (size_t)((r - 1) & 1) * a.nslots + sh.err_slot;
+      while (ld_acquire(&ex->tag) != (uint64_t)(r - 1)) nap();
+      const bool ref = ex->cb >= 0 && ex->ocb >= a.g.cap;
+      a.st->error = GCMC_CELL_OVERFLOW;
+      a.st->err_a = ref ? ex->cb : ex->bb;
+      a.st->err_b = ref ? ex->ocb : ex->obb;
+      a.st->err_c = ref ? 0 : 1;
+    }
   }
-  (void)gw;
+}
+
+template <int T>
+__global__ void __launch_bounds__(kThreads, 1) k_engine(EngineArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (blockIdx.x == 0)
+    sequencer(a, smem);
+  else
+    evaluator<T>(a, smem);
 }
 
 }  // namespace
@@ -427,8 +1187,9 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
   const gcmc_params& P = c.params;
   EngineArgs a{};
   a.g = c.grid;
+  a.m = c.mirror;
   a.b = c.box;
-  a.pos = c.pos;
+  a.s = Store{c.pos, c.rslot, c.bslot};
   a.st = c.st;
   a.props = c.props;
   a.trace = trace_d;
@@ -456,25 +1217,51 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
     a.tail_bu = sr9 / 3.0 - sr3;
     a.tail_bp = 2.0 / 3.0 * sr9 - sr3;
   }
-  const int C = c.engine_ctas;
-  const int M = c.engine_warps;  // moves per CTA (1, 2, 4)
-  void (*kern)(EngineArgs) = M == 1 ? k_engine<1> : M == 2 ? k_engine<2> : k_engine<4>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, 1, 1);
-  cfg.blockDim = dim3(512, 1, 1);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  const int T = c.engine_group;  // threads per slot
+  const int MG = kThreads / T;
+  const int G = c.engine_ctas;   // total CTAs (1 sequencer + evaluators)
+  a.nslots = (G - 1) * MG;
+  if (a.nslots > kMaxSlots) a.nslots = kMaxSlots;  // (G is clamped in api.cu)
+  a.dec = c.eng_dec;
+  a.res = c.eng_res;
+  a.ext = reinterpret_cast<SlotExt*>(c.eng_ext);
+  a.bias0 = c.engine_bias;
+  a.nvar = c.engine_variants;
+  {
+    const char* e = std::getenv("GCMC_POLL_NS");
+    a.poll_ns = e ? (unsigned)std::atoi(e) : 64u;
+  }
+  size_t eval_bytes = T == 128 ? sizeof(EvalShared<128>) : (T == 256 ? sizeof(EvalShared<256>) : sizeof(EvalShared<512>));
+  eval_bytes = (eval_bytes + 15) & ~size_t(15);
+  size_t smem = eval_bytes + ((c.mirror.nb + 15) & ~15u);
+  a.smem_occ = 1;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
+  if (smem > (size_t)max_optin) {
+    a.smem_occ = 0;
+    smem = eval_bytes;
+  }
+  if (smem < sizeof(SeqShared)) smem = sizeof(SeqShared);
+  void (*kern)(EngineArgs) = T == 128 ? k_engine<128> : (T == 256 ? k_engine<256> : k_engine<512>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e) return cuda_error(e, "engine smem");
+  const size_t res_bytes = 2 * (size_t)a.nslots * kResWords * sizeof(uint64_t);
+  if ((e = cudaMemsetAsync(c.eng_dec, 0, kDecWords * sizeof(uint64_t), s))) return cuda_error(e, "engine");
+  if ((e = cudaMemsetAsync(c.eng_res, 0, res_bytes, s))) return cuda_error(e, "engine");
+  if ((e = cudaMemsetAsync(c.eng_ext, 0, 2 * (size_t)a.nslots * sizeof(SlotExt), s))) return cuda_error(e, "engine");
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kThreads), args, smem, s);
   if (e) return cuda_error(e, "engine launch");
   return GCMC_OK;
 }
+
+size_t engine_buffer_bytes(int nslots, size_t* dec, size_t* res, size_t* ext) {
+  *dec = kDecWords * sizeof(uint64_t);
+  *res = 2 * (size_t)nslots * kResWords * sizeof(uint64_t);
+  *ext = 2 * (size_t)nslots * sizeof(SlotExt);
+  return *dec + *res + *ext;
+}
+
+int engine_max_slots() { return kMaxSlots; }
 
 }  // namespace gcmcb

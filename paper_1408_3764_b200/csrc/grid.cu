@@ -31,7 +31,7 @@ __global__ void k_bin(Grid g, const double4* __restrict__ pos, uint64_t n, int* 
 
 // Per cell: ascending insertion sort of the ids (grid_common.hpp:11-21
 // ordering), mirror records, peak occupancy.
-__global__ void k_sort_cells(Grid g, const double4* __restrict__ pos, ChainState* st) {
+__global__ void k_sort_cells(Grid g, int32_t* rslot, ChainState* st) {
   const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   int occ = 0;
   if (c < g.ncells) {
@@ -49,15 +49,55 @@ __global__ void k_sort_cells(Grid g, const double4* __restrict__ pos, ChainState
       ids[j + 1] = v;
     }
     for (int k = 0; k < occ; ++k) {
-      const uint64_t s = slot_index(g, (int)c, k);
-      const double4 p = pos[ids[k]];
-      g.slots[s] = ids[k];
-      g.cellpos[s] = make_double4(p.x, p.y, p.z, pid_bits((uint64_t)ids[k]));
+      g.slots[slot_index(g, (int)c, k)] = ids[k];
+      rslot[ids[k]] = k;
     }
   }
   // block max -> peak
   for (int o = 16; o > 0; o >>= 1) occ = max(occ, __shfl_xor_sync(0xffffffffu, occ, o));
   if ((threadIdx.x & 31) == 0 && occ > 0) atomicMax(&st->peak, occ);
+}
+
+
+// Mirror build: bin by brick (atomic slot), then per brick sort the ids
+// ascending (deterministic record order) and write the record planes and
+// the back-pointers.
+__global__ void k_mbin(Mirror m, const double4* __restrict__ pos, uint64_t n, int32_t* bslot,
+                       int* overflow) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = pos[i];
+  const uint32_t b = mbrick(m, mpoint(m, p.x, p.y, p.z));
+  const int k = atomicAdd(m.occ + b, 1);
+  if (k < m.cap)
+    m.rid[(size_t)b * m.cap + k] = (int32_t)i;
+  else
+    atomicMax(overflow, (int)b + 1);
+}
+
+__global__ void k_msort(Mirror m, const double4* __restrict__ pos, int32_t* bslot) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= m.nb) return;
+  int occ = m.occ[b];
+  if (occ > m.cap) occ = m.cap;
+  int32_t* ids = m.rid + (size_t)b * m.cap;
+  for (int i = 1; i < occ; ++i) {
+    const int32_t v = ids[i];
+    int j = i - 1;
+    while (j >= 0 && ids[j] > v) {
+      ids[j + 1] = ids[j];
+      --j;
+    }
+    ids[j + 1] = v;
+  }
+  for (int k = 0; k < occ; ++k) {
+    const size_t s = (size_t)b * m.cap + k;
+    const double4 p = pos[ids[k]];
+    m.rx[s] = p.x;
+    m.ry[s] = p.y;
+    m.rz[s] = p.z;
+    bslot[ids[k]] = (int32_t)s;
+  }
 }
 
 // Overflow diagnosis (error path only): for every overflowing cell, the
@@ -133,11 +173,31 @@ __global__ void k_check_cells(Grid g, const double4* __restrict__ pos, uint64_t 
       if (cell_of(g, p.x, p.y, p.z) != (int)c) code = 3;
       for (int j = 0; j < k; ++j)
         if (g.slots[slot_index(g, (int)c, j)] == id) code = 3;
-      const double4 r = g.cellpos[s];
-      if (!code && (r.x != p.x || r.y != p.y || r.z != p.z || bits_pid(r.w) != id)) code = 4;
     }
   }
   if (code) atomicMin(first, ((unsigned long long)c << 8) | (unsigned long long)code);
+}
+
+// Mirror + back-pointers against the store (engine-internal consistency;
+// reported by rebuild_check as a stale coordinate mirror).
+__global__ void k_check_mirror(Grid g, Mirror m, const double4* __restrict__ pos,
+                               const int32_t* rslot, const int32_t* bslot, uint64_t n,
+                               unsigned long long* first) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 p = pos[i];
+  bool bad = false;
+  const int32_t bs = bslot[i];
+  const uint32_t b = mbrick(m, mpoint(m, p.x, p.y, p.z));
+  if (bs < 0 || (uint32_t)(bs / m.cap) != b || bs % m.cap >= m.occ[b] || m.rid[bs] != (int32_t)i ||
+      m.rx[bs] != p.x || m.ry[bs] != p.y || m.rz[bs] != p.z)
+    bad = true;
+  if (g.kind != GCMC_ALL_PAIRS) {
+    const int c = cell_of(g, p.x, p.y, p.z);
+    const int k = rslot[i];
+    if (k < 0 || k >= g.occ[c] || g.slots[slot_index(g, c, k)] != (int32_t)i) bad = true;
+  }
+  if (bad) atomicMin(first, (unsigned long long)i);
 }
 
 struct CommitArgs {
@@ -146,20 +206,20 @@ struct CommitArgs {
   double x, y, z;
 };
 
-__global__ void k_commit_one(Grid g, double4* pos, ChainState* st, CommitArgs a,
+__global__ void k_commit_one(Grid g, Mirror m, Store s, ChainState* st, CommitArgs a,
                              long long* out) {
-  __shared__ CommitPlan cp;
-  double4 old = make_double4(0, 0, 0, 0);
-  if (a.kind != 1) old = ld_cg(pos + a.pid);
-  commit_prefetch(g, pos, a.n, a.kind, a.pid, old, a.x, a.y, a.z, cp);
-  __syncwarp();
-  if (threadIdx.x == 0) {
-    const int s = commit_apply(g, pos, st, a.n, a.kind, a.pid, a.x, a.y, a.z, cp);
-    if (s == GCMC_OK) st->n = a.kind == 1 ? a.n + 1 : (a.kind == 2 ? a.n - 1 : a.n);
-    out[0] = s;
-    out[1] = cp.e1;
-    out[2] = cp.e2;
-  }
+  MoveData d;
+  d.nx = a.x;
+  d.ny = a.y;
+  d.nz = a.z;
+  load_move(s, a.kind, a.pid, d);
+  long long e1, e2, e3;
+  const int r = commit_move(g, m, s, &st->peak, a.kind, a.pid, a.n, d, e1, e2, e3);
+  if (r == GCMC_OK) st->n = a.kind == 1 ? a.n + 1 : (a.kind == 2 ? a.n - 1 : a.n);
+  out[0] = r;
+  out[1] = e1;
+  out[2] = e2;
+  out[3] = e3;
 }
 
 inline unsigned blocks(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -179,13 +239,33 @@ std::string overflow_message(const Chain& c, int64_t cell, int64_t occ) {
   return os.str();
 }
 
+gcmc_status mirror_build(Chain& c) {
+  const uint64_t n = c.st_host->n;
+  cudaStream_t s = c.stream;
+  int* flag = c.iscratch;
+  cudaError_t e;
+  Mirror& m = c.mirror;
+  if ((e = cudaMemsetAsync(m.occ, 0, (size_t)m.nb * sizeof(int32_t), s))) return cuda_error(e, "mirror");
+  if ((e = cudaMemsetAsync(flag, 0, sizeof(int), s))) return cuda_error(e, "mirror");
+  if (n) k_mbin<<<blocks(n, 256), 256, 0, s>>>(m, c.pos, n, c.bslot, flag);
+  k_msort<<<blocks(m.nb, 256), 256, 0, s>>>(m, c.pos, c.bslot);
+  int overflow = 0;
+  if ((e = cudaMemcpyAsync(&overflow, flag, sizeof(int), cudaMemcpyDeviceToHost, s))) return cuda_error(e, "mirror");
+  if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "mirror");
+  if (overflow) {
+    std::ostringstream os;
+    os << "mirror: brick " << overflow - 1 << " exceeds capacity " << m.cap
+       << " (density too high for the evaluation mirror)";
+    return set_error(GCMC_CELL_OVERFLOW, os.str());
+  }
+  c.built = true;
+  return GCMC_OK;
+}
+
 gcmc_status grid_build(Chain& c) {
   const uint64_t n = c.st_host->n;
   c.built = false;
-  if (c.grid.kind == GCMC_ALL_PAIRS) {
-    c.built = true;
-    return GCMC_OK;
-  }
+  if (c.grid.kind == GCMC_ALL_PAIRS) return mirror_build(c);
   cudaStream_t s = c.stream;
   int* flag = c.iscratch;
   cudaError_t e;
@@ -229,28 +309,32 @@ gcmc_status grid_build(Chain& c) {
     if (e) return cuda_error(e, "build overflow");
     return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, (int64_t)(b & 0xffffffffu), c.grid.cap));
   }
-  k_sort_cells<<<blocks(c.grid.ncells, 256), 256, 0, s>>>(c.grid, c.pos, c.st);
+  k_sort_cells<<<blocks(c.grid.ncells, 256), 256, 0, s>>>(c.grid, c.rslot, c.st);
   if ((e = cudaGetLastError())) return cuda_error(e, "build");
-  if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "build");
-  c.built = true;
-  return GCMC_OK;
+  return mirror_build(c);
 }
 
 gcmc_status grid_check(Chain& c, std::string* issue) {
   issue->clear();
-  if (c.grid.kind == GCMC_ALL_PAIRS) return GCMC_OK;
   const uint64_t n = c.st_host->n;
   const uint64_t nc = c.grid.ncells;
   cudaStream_t s = c.stream;
   int* fresh = nullptr;
   unsigned long long* first = nullptr;
   cudaError_t e;
-  if ((e = cudaMalloc(&fresh, nc * sizeof(int)))) return cuda_error(e, "rebuild_check");
+  if ((e = cudaMalloc(&fresh, (nc ? nc : 1) * sizeof(int)))) return cuda_error(e, "rebuild_check");
   if ((e = cudaMalloc(&first, sizeof(unsigned long long)))) return cuda_error(e, "rebuild_check");
-  cudaMemsetAsync(fresh, 0, nc * sizeof(int), s);
+  cudaMemsetAsync(fresh, 0, (nc ? nc : 1) * sizeof(int), s);
   cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), s);
-  if (n) k_fresh_count<<<blocks(n, 256), 256, 0, s>>>(c.grid, c.pos, n, fresh);
-  k_check_cells<<<blocks(nc, 256), 256, 0, s>>>(c.grid, c.pos, n, fresh, first);
+  if (nc) {
+    if (n) k_fresh_count<<<blocks(n, 256), 256, 0, s>>>(c.grid, c.pos, n, fresh);
+    k_check_cells<<<blocks(nc, 256), 256, 0, s>>>(c.grid, c.pos, n, fresh, first);
+  }
+  unsigned long long* mfirst = reinterpret_cast<unsigned long long*>(c.iscratch);
+  cudaMemsetAsync(mfirst, 0xff, sizeof(unsigned long long), s);
+  if (n) k_check_mirror<<<blocks(n, 256), 256, 0, s>>>(c.grid, c.mirror, c.pos, c.rslot, c.bslot, n, mfirst);
+  unsigned long long mf = 0;
+  cudaMemcpyAsync(&mf, mfirst, sizeof mf, cudaMemcpyDeviceToHost, s);
   unsigned long long f = 0;
   int fr = 0, oc = 0;
   cudaMemcpyAsync(&f, first, sizeof f, cudaMemcpyDeviceToHost, s);
@@ -263,7 +347,14 @@ gcmc_status grid_check(Chain& c, std::string* issue) {
   cudaFree(fresh);
   cudaFree(first);
   if (e) return cuda_error(e, "rebuild_check");
-  if (f == ~0ull) return GCMC_OK;
+  if (f == ~0ull) {
+    if (mf != ~0ull) {
+      std::ostringstream os;
+      os << "coordinate mirror differs from the store (particle " << mf << ")";
+      *issue = os.str();
+    }
+    return GCMC_OK;
+  }
   const uint64_t cell = f >> 8;
   const int code = (int)(f & 0xff);
   const bool micro = c.grid.kind == GCMC_MICROCELL;
@@ -284,19 +375,20 @@ gcmc_status commit_one(Chain& c, int kind, uint64_t pid, const double* p, uint64
   const uint64_t n = c.st_host->n;
   CommitArgs a{kind, pid, n, p ? p[0] : 0.0, p ? p[1] : 0.0, p ? p[2] : 0.0};
   long long* out = reinterpret_cast<long long*>(c.dscratch);
-  k_commit_one<<<1, 32, 0, c.stream>>>(c.grid, c.pos, c.st, a, out);
-  long long h[3];
+  k_commit_one<<<1, 1, 0, c.stream>>>(c.grid, c.mirror, Store{c.pos, c.rslot, c.bslot}, c.st, a,
+                                      out);
+  long long h[4];
   cudaError_t e = cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, c.stream);
   if (!e) e = cudaStreamSynchronize(c.stream);
   if (e) return cuda_error(e, "commit");
   if (h[0] == GCMC_CELL_OVERFLOW) {
     if (kind == 1) c.st_host->n = n + 1;  // store already appended (microcell_grid.hpp:254)
+    if (h[3]) {
+      std::ostringstream os;
+      os << "mirror: brick " << h[1] << " exceeds capacity " << c.mirror.cap;
+      return set_error(GCMC_CELL_OVERFLOW, os.str());
+    }
     return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, h[1], h[2]));
-  }
-  if (h[0] == GCMC_NOT_FOUND) {
-    std::ostringstream os;
-    os << strategy_name(c.grid.kind) << ": particle " << h[1] << " not found in cell " << h[2];
-    return set_error(GCMC_NOT_FOUND, os.str());
   }
   if (kind == 1) {
     if (new_pid) *new_pid = n;

@@ -15,7 +15,10 @@ struct Chain {
   gcmc_params params{};
   Box box{};
   Grid grid{};
+  Mirror mirror{};               // evaluation mirror (bricks >= r_cut)
   double4* pos = nullptr;        // [capn]
+  int32_t* rslot = nullptr;      // [capn] slot of particle i in its reference cell
+  int32_t* bslot = nullptr;      // [capn] record index of particle i in the mirror
   uint64_t capn = 0;
   ChainState* st = nullptr;      // device
   ChainState* st_host = nullptr; // pinned mirror
@@ -37,10 +40,15 @@ struct Chain {
   cudaStream_t gen_stream = nullptr;
   cudaEvent_t ev[4] = {};
   int sm_count = 0;
-  int engine_ctas = 0;
-  int engine_warps = 0;
+  int engine_ctas = 0;        // sequencer + evaluator CTAs
+  int engine_group = 256;     // threads per evaluation slot
+  int engine_variants = 5;    // N-variants per displace/delete proposal (after the first)
+  int engine_bias = -1;       // initial variant order (+1: N expected to grow)
+  uint64_t* eng_dec = nullptr;  // engine communication buffers (engine.cu)
+  uint64_t* eng_res = nullptr;
+  void* eng_ext = nullptr;
   bool built = false;
-  unsigned long long* prof = nullptr;  // engine phase timers (GCMC_ENGINE_PROFILE=1)
+  unsigned long long* prof = nullptr;
 };
 
 // Thread-local error plumbing (api.cu).
@@ -48,7 +56,8 @@ gcmc_status set_error(gcmc_status s, const std::string& msg);
 gcmc_status cuda_error(cudaError_t e, const char* where);
 
 // grid.cu
-gcmc_status grid_build(Chain& c);                              // occ/slots/cellpos from pos
+gcmc_status grid_build(Chain& c);                              // occ/slots + mirror from pos
+gcmc_status mirror_build(Chain& c);
 gcmc_status grid_check(Chain& c, std::string* issue);          // rebuild_check
 gcmc_status commit_one(Chain& c, int kind, uint64_t pid, const double* p, uint64_t* new_pid);
 
@@ -64,6 +73,8 @@ gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s);
 
 // engine.cu: run n moves from c.props; optional device trace.
 gcmc_status engine_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
+size_t engine_buffer_bytes(int nslots, size_t* dec, size_t* res, size_t* ext);
+int engine_max_slots();
 
 // Error text in the reference's wording.
 std::string overflow_message(const Chain& c, int64_t cell, int64_t occ);

@@ -180,7 +180,8 @@ def random_initial_configuration(n: int, box_length: float, min_sep: float, seed
                                     draws.value)
 
 
-def _params(cfg: RunConfig, cluster_ctas=0, warps_per_cta=0, max_particles=0) -> L.GcmcParams:
+def _params(cfg: RunConfig, engine_ctas=0, engine_group=0, engine_variants=0, engine_bias=0,
+            max_particles=0) -> L.GcmcParams:
     return L.GcmcParams(
         box_length=cfg.box_length, epsilon=cfg.epsilon, sigma=cfg.sigma, r_cut=cfg.r_cut,
         temperature=cfg.temperature, chemical_potential=cfg.chemical_potential,
@@ -189,7 +190,8 @@ def _params(cfg: RunConfig, cluster_ctas=0, warps_per_cta=0, max_particles=0) ->
         sampling_interval=cfg.sampling_interval, strategy=STRATEGIES.index(cfg.strategy),
         cell_capacity=cfg.cell_capacity, microcell_capacity=cfg.microcell_capacity,
         tail_corrections=int(cfg.tail_corrections), max_particles=max_particles,
-        cluster_ctas=cluster_ctas, warps_per_cta=warps_per_cta)
+        engine_ctas=engine_ctas, engine_group=engine_group, engine_variants=engine_variants,
+        engine_bias=engine_bias)
 
 
 class _Device:

@@ -1,0 +1,5 @@
+#!/bin/bash
+TAG=${1:-p}
+O=gpurun_out/$TAG
+mkdir -p $O
+GCMC_ENGINE_PROFILE=1 timeout 600 python tools/prof_engine.py --n0 1048576 --mu 1 --moves 262144 --warm 262144 ${@:2} > $O/prof1m.log 2>&1

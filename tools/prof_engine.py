@@ -26,7 +26,7 @@ print(f"init {time.time()-t:.1f}s", flush=True)
 cfg = RunConfig(temperature=2.0, chemical_potential=a.mu, box_length=box, strategy=a.strategy)
 
 def one(ctas, warps):
-    sim = E.Simulation(cfg, xyz, rng, cluster_ctas=ctas, warps_per_cta=warps)
+    sim = E.Simulation(cfg, xyz, rng, engine_ctas=ctas, engine_group=warps)
     sim.run(a.warm)
     sim.run(a.moves)
     r = sim.last_run
