@@ -29,11 +29,16 @@ _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
 
 
+SHIM = os.path.join(HERE, "_ref", "shim_check")
+
+
 def build(ref: bool = True) -> None:
-    """Compile the restatement, and the reference when its headers exist."""
+    """Compile the restatement, and the reference (plus the drop-in shim
+    check, which links the product library) when its headers exist."""
     subprocess.run(["make", "-s", "-C", HERE, "liboracle.so"], check=True)
     if ref and os.path.isdir(REF_INC):
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", HERE, "shim"], check=True)
 
 
 def ref_available() -> bool:

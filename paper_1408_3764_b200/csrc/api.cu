@@ -175,7 +175,8 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   c->sm_count = prop.multiProcessorCount;
   // Engine shape (engine.cu): one persistent CTA per SM, 1 sequencer + evaluators.
   c->engine_group = P.engine_group == 128 || P.engine_group == 512 ? P.engine_group : 256;
-  c->engine_ctas = P.engine_ctas > 1 && P.engine_ctas <= c->sm_count ? P.engine_ctas : c->sm_count;
+  // one SM is left to generate the next batch of proposals concurrently
+  c->engine_ctas = P.engine_ctas > 1 && P.engine_ctas <= c->sm_count ? P.engine_ctas : c->sm_count - 1;
   {
     const int mg = 512 / c->engine_group;
     const int max_ctas = 1 + engine_max_slots() / mg;
@@ -209,6 +210,8 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
   CK(cudaStreamCreateWithFlags(&c->gen_stream, cudaStreamNonBlocking), "stream");
   for (auto& ev : c->ev) CK(cudaEventCreate(&ev), "event");
+  CK(cudaEventCreateWithFlags(&c->ev_mt, cudaEventDisableTiming), "event");
+  CK(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming), "event");
   CK(cudaMalloc(&c->pos, capn * sizeof(double4)), "alloc pos");
   CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
   CK(cudaMalloc(&c->rslot, capn * sizeof(int32_t)), "alloc rslot");
@@ -238,6 +241,7 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   CK(cudaMallocHost(&c->st_host, sizeof(ChainState)), "alloc state");
   std::memset(c->st_host, 0, sizeof(ChainState));
   CK(cudaMalloc(&c->mt, 314 * sizeof(uint64_t)), "alloc rng");
+  CK(cudaMalloc(&c->mt_next, 314 * sizeof(uint64_t)), "alloc rng");
   if ((s = ensure_batch(*c, 1024))) return s;
   sync_state_to_device(*c);
   *out = reinterpret_cast<gcmc_dev*>(c);
@@ -249,7 +253,12 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   Chain* c = H(h);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(c->gen_stream);
   cudaFree(c->pos);
+  cudaFree(c->props_next);
+  cudaFree(c->mt_next);
+  cudaEventDestroy(c->ev_mt);
+  cudaEventDestroy(c->ev_ahead);
   cudaFree(c->grid.occ);
   cudaFree(c->grid.slots);
   cudaFree(c->rslot);
@@ -471,6 +480,8 @@ gcmc_status gcmc_set_rng_state(gcmc_dev* h, const uint64_t words[312], uint64_t 
   std::memcpy(buf, words, 312 * 8);
   buf[312] = index;
   buf[313] = draws;
+  c.ahead_n = 0;  // proposals generated ahead belong to the old stream
+  CK(cudaStreamSynchronize(c.gen_stream), "rng");
   CK(cudaMemcpyAsync(c.mt, buf, sizeof buf, cudaMemcpyHostToDevice, c.stream), "rng");
   CK(cudaStreamSynchronize(c.stream), "rng");
   return GCMC_OK;
@@ -543,10 +554,14 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
   const uint64_t kChunk = 1ull << 21;
   const uint64_t chunk_cap = n < kChunk ? (n ? n : 1) : kChunk;
   if (chunk_cap > c.props_cap) {
+    CK(cudaStreamSynchronize(c.gen_stream), "proposals");
     cudaFree(c.props);
-    c.props = nullptr;
+    cudaFree(c.props_next);
+    c.props = c.props_next = nullptr;
     CK(cudaMalloc(&c.props, chunk_cap * sizeof(Proposal)), "alloc proposals");
+    CK(cudaMalloc(&c.props_next, chunk_cap * sizeof(Proposal)), "alloc proposals");
     c.props_cap = chunk_cap;
+    c.ahead_n = 0;
   }
   if (trace && chunk_cap > c.trace_cap) {
     cudaFree(c.trace);
@@ -560,7 +575,25 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
   while (done < n) {
     const uint64_t m = std::min(chunk_cap, n - done);
     CK(cudaEventRecord(c.ev[0], c.stream), "event");
-    if ((s = gen_proposals(c, m, c.stream))) return s;
+    if (c.ahead_n == m) {  // generated during the previous batch
+      CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
+      std::swap(c.props, c.props_next);
+      std::swap(c.mt, c.mt_next);
+    } else if ((s = gen_proposals(c, m, c.stream))) {
+      return s;
+    }
+    c.ahead_n = 0;
+    {  // the next batch, on the SM the engine leaves free
+      const uint64_t left = n - done - m;
+      const uint64_t mn = left ? std::min(chunk_cap, left) : m;
+      CK(cudaEventRecord(c.ev_mt, c.stream), "ahead");
+      CK(cudaStreamWaitEvent(c.gen_stream, c.ev_mt, 0), "ahead");
+      CK(cudaMemcpyAsync(c.mt_next, c.mt, 314 * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                         c.gen_stream), "ahead");
+      if ((s = gen_proposals_into(c, c.mt_next, c.props_next, mn, c.gen_stream))) return s;
+      CK(cudaEventRecord(c.ev_ahead, c.gen_stream), "ahead");
+      c.ahead_n = mn;
+    }
     if (std::getenv("GCMC_ENGINE_PROFILE") && !c.prof) {
       CK(cudaMalloc(&c.prof, 48 * sizeof(unsigned long long)), "prof");
     }

@@ -45,6 +45,7 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kMaxMoves = 64;    // moves per round
+constexpr int kMH = kMaxMoves / 32;  // moves per walk lane
 constexpr int kMaxAcc = 32;      // accepted moves per round
 constexpr int kRing = 256;       // proposal ring (moves)
 constexpr int kPre = 2 * kMaxMoves + 2;  // slot prefix entries
@@ -53,7 +54,8 @@ constexpr int kDecEnt = 5;
 constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 164
 constexpr int kResWords = 8;     // 6 used
 constexpr int kPollWarps = 12;   // sequencer warps that poll / walk / verify
-constexpr int kMaxSlots = kPollWarps * 32;
+constexpr int kSlotsPerPoller = 2;
+constexpr int kMaxSlots = kPollWarps * 32 * kSlotsPerPoller;
 constexpr int kInsSpan = 32;     // insertion accept mask covers d in [-16, 15]
 
 constexpr uint64_t kPay = 0xffffffffffffull;
@@ -354,14 +356,33 @@ struct EvalShared {
   Proposal ring[kRing];
   Dec d;
   int Q[kPre];
+  int16_t stab[kMaxMoves + 1][kThreads / T];  // slot of group g for a round of length len: i | v << 8
   WinWs<T> ws[kThreads / T];
   struct G {
-    int i, v, kind, empty;
+    int i, v, kind, empty, cf;
     uint64_t pid, q, nv;
     MoveData md;
     double acc;
   } gs[kThreads / T];
 };
+
+// Warp: for every possible length of the round in progress (next base =
+// b0 + len), the (move, variant) of this CTA's MG slots.
+template <int MG>
+__device__ __forceinline__ void slot_table_warp(const EngineArgs& a, const int* Q, uint64_t b0,
+                                                int cta_slot0, int16_t (*stab)[MG], int lane) {
+  for (int len = lane; len <= kMaxMoves; len += 32) {
+    int fit, used;
+    round_shape(a, Q, len, b0 + (uint64_t)len, fit, used);
+#pragma unroll
+    for (int g = 0; g < MG; ++g) {
+      int i = -1, v = 0;
+      const int s = cta_slot0 + g;
+      if (!(s < used && slot_move(Q, len, s, fit, i, v))) i = -1;
+      stab[len][g] = (int16_t)(i < 0 ? -1 : (i | (v << 8)));
+    }
+  }
+}
 
 template <int T>
 __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
@@ -386,9 +407,11 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     cp_async_wait();
     __syncwarp();
     prefix_warp(a, sh.ring, 0, sh.Q, lane);
+    __syncwarp();
+    slot_table_warp<MG>(a, sh.Q, 0, cta_slot0, sh.stab, lane);
   }
   __syncthreads();
-  uint64_t b0 = 0;  // base the prefix Q refers to
+  uint64_t b0 = 0;  // base the prefix Q / slot table refer to
   uint32_t r = 1;
   PhaseClock pc;
   pc.start(a.prof && blockIdx.x == 1 && tid == 0);
@@ -411,15 +434,11 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           atomicAdd(occ_w + (bb >> 2), 1u << (8 * (bb & 3)));
         }
       }
-      // slots of this CTA
+      // slots of this CTA (precomputed for every round length)
       if (lane < MG && !d.stop) {
-        const int len = (int)(d.base - b0);
-        int fit, used, i = -1, v = 0;
-        round_shape(a, sh.Q, len, d.base, fit, used);
-        const int s = cta_slot0 + lane;
-        if (!(s < used && slot_move(sh.Q, len, s, fit, i, v))) i = -1;
-        sh.gs[lane].i = i;
-        sh.gs[lane].v = v;
+        const int t = sh.stab[(int)(d.base - b0)][lane];
+        sh.gs[lane].i = t < 0 ? -1 : (t & 0xff);
+        sh.gs[lane].v = t < 0 ? 0 : (t >> 8);
       }
       cp_async_wait();
     }
@@ -449,23 +468,33 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         md.nz = pr.z;
         md.rslot_pid = md.bslot_pid = -1;
         md.ox = md.oy = md.oz = 0.0;
-        if (kind != 1 && !empty) {
+        double4 o = make_double4(0, 0, 0, 0);
+        int rsl = -1, bsl = -1;
+        const bool loads = kind != 1 && !empty;
+        if (loads) {
           pid = index_from(pr.pick, (uint64_t)nv);
           q = (uint64_t)nv - 1;
-          // the mover's position and back-pointers (one L2 hop)
-          if (lane == 0) {
-            const double4 o = ld_cg(a.s.pos + pid);
-            md.ox = o.x;
-            md.oy = o.y;
-            md.oz = o.z;
-            md.rslot_pid = __ldcg(a.s.rslot + pid);
-            md.bslot_pid = __ldcg(a.s.bslot + pid);
+          if (lane == 0) {  // the mover's position and back-pointers: one L2 hop, in flight
+            o = ld_cg(a.s.pos + pid);
+            rsl = __ldcg(a.s.rslot + pid);
+            bsl = __ldcg(a.s.bslot + pid);
           }
-          md.ox = __shfl_sync(0xffffffffu, md.ox, 0);
-          md.oy = __shfl_sync(0xffffffffu, md.oy, 0);
-          md.oz = __shfl_sync(0xffffffffu, md.oz, 0);
-          md.rslot_pid = __shfl_sync(0xffffffffu, md.rslot_pid, 0);
-          md.bslot_pid = __shfl_sync(0xffffffffu, md.bslot_pid, 0);
+        }
+        // the new-position window does not need the mover (unless max_displacement)
+        const bool early = kind != 2 && !empty && !(kind == 0 && a.max_disp > 0.0) && !all_pairs;
+        int nent = 0, nent0 = 0;
+        if (early) {
+          nent = win_add<T>(a.m, a.b, ws, 0, md.nx, md.ny, md.nz, lane);
+          nent0 = nent;
+        }
+        if (lane == 0 && !empty && kind != 2 && !all_pairs && early)  // reference cell entered
+          ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
+        if (loads) {
+          md.ox = __shfl_sync(0xffffffffu, o.x, 0);
+          md.oy = __shfl_sync(0xffffffffu, o.y, 0);
+          md.oz = __shfl_sync(0xffffffffu, o.z, 0);
+          md.rslot_pid = __shfl_sync(0xffffffffu, rsl, 0);
+          md.bslot_pid = __shfl_sync(0xffffffffu, bsl, 0);
           if (kind == 0 && a.max_disp > 0.0) {  // engine.hpp:359-365
             const double c = a.max_disp;
             md.nx = wrap_axis(__dadd_rn(md.ox, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.x), 1.0), c)), a.b.l);
@@ -473,15 +502,38 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
             md.nz = wrap_axis(__dadd_rn(md.oz, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.z), 1.0), c)), a.b.l);
           }
         }
+        if (!all_pairs && !empty) {
+          if (kind == 0 && !early) {  // max_displacement: new window now
+            nent = win_add<T>(a.m, a.b, ws, 0, md.nx, md.ny, md.nz, lane);
+            nent0 = nent;
+            if (lane == 0) ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
+          }
+          if (kind != 1) {
+            nent = win_add<T>(a.m, a.b, ws, nent, md.ox, md.oy, md.oz, lane);
+            if (kind == 2) nent0 = nent;
+          }
+          win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
+        }
+        // read set and conflicts with the previous round's commits (lanes over entries)
+        RW rs;
+        rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
+        rs.pt[1] = loads ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
+        rs.pt[2] = kNoPoint;  // a deletion's last particle is read by its commit, not here
+        rs.ia = loads ? (int64_t)pid : -1;
+        rs.ib = -1;
+        bool cf = false;
+        if (!empty && lane < d.nacc) cf = conflict(a.m, all_pairs, rs, d.acc[lane]);
+        cf = __any_sync(0xffffffffu, cf);
         if (lane == 0) {
           G.kind = kind;
           G.empty = empty;
+          G.cf = cf;
           G.pid = pid;
           G.q = q;
           G.nv = (uint64_t)(nv < 0 ? 0 : nv);
           G.md = md;
           G.acc = pr.acc;
-          ws.excl = (kind != 1 && !empty) ? md.bslot_pid : -1;
+          ws.excl = loads ? md.bslot_pid : -1;
           if (kind == 2) {
             ws.nwin = 1;
             ws.sign1 = 1;
@@ -500,12 +552,6 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           }
           if (empty) ws.total = 0;
         }
-        __syncwarp();
-        if (!empty && !all_pairs) win_setup_warp<T>(a.m, a.b, ws, occ_s, lane);
-        // occupancy of the reference cell entered (overflow test): issued now,
-        // consumed after the sums
-        if (lane == 0 && !empty && kind != 2 && !all_pairs)
-          ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
       }
       group_sync(bar_id, T);
       pc.mark(3);  // setup (pid hop + window)
@@ -523,16 +569,13 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       if (gw == 0) {
         const int kind = G.kind;
         const MoveData& md = G.md;
-        // read set and conflicts with the previous round's commits (lanes over entries)
         RW rs;
         rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
         rs.pt[1] = kind != 1 && !G.empty ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
-        rs.pt[2] = kNoPoint;  // a deletion's last particle is read by its commit, not here
+        rs.pt[2] = kNoPoint;
         rs.ia = kind != 1 && !G.empty ? (int64_t)G.pid : -1;
         rs.ib = -1;
-        bool cf = false;
-        if (!G.empty && lane < d.nacc) cf = conflict(a.m, all_pairs, rs, d.acc[lane]);
-        cf = __any_sync(0xffffffffu, cf);
+        const bool cf = G.cf;
         du = __shfl_sync(0xffffffffu, du, 0);
         dw = __shfl_sync(0xffffffffu, dw, 0);
         uint32_t bits = 0;
@@ -585,7 +628,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
             case 3: p = rs.pt[2]; break;
             case 4:
               p = (uint64_t)(rs.ia < 0 ? 0xffffffffu : (uint32_t)rs.ia) |
-                  ((uint64_t)G.i << 32) | ((uint64_t)G.v << 38);
+                  ((uint64_t)G.i << 32) | ((uint64_t)G.v << 39);
               break;
             default: p = (uint32_t)(rs.ib < 0 ? 0xffffffffu : (uint32_t)rs.ib); break;
           }
@@ -613,6 +656,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       const uint64_t want = b0 + kRing < a.nmoves ? b0 + kRing : a.nmoves;
       prefix_warp(a, sh.ring, b0, sh.Q, lane);
       __syncwarp();
+      slot_table_warp<MG>(a, sh.Q, b0, cta_slot0, sh.stab, lane);
       if (want > ring_hi) {
         ring_fill(a, sh.ring, ring_hi, want, lane);
         ring_hi = want;
@@ -645,7 +689,7 @@ struct SeqShared {
   int Q[kPre];
   int fit, used;
   // per-move masks built by the pollers
-  uint32_t macc[kMaxMoves], mcf[kMaxMoves], mov[kMaxMoves];
+  uint32_t macc[kMaxMoves], mcov[kMaxMoves], mcf[kMaxMoves], mov[kMaxMoves];
   uint8_t mkind[kMaxMoves];
   // walk output
   int len, nacc, err, cmin, err_slot, why;
@@ -869,7 +913,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
   }
   if (tid < kMaxMoves) {
-    sh.macc[tid] = sh.mcf[tid] = sh.mov[tid] = 0;
+    sh.macc[tid] = sh.mcov[tid] = sh.mcf[tid] = sh.mov[tid] = 0;
   }
   uint64_t ring_hi = a.nmoves < (uint64_t)kRing ? a.nmoves : (uint64_t)kRing;
   if (warp == 0) {
@@ -896,8 +940,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     if (warp < kPollWarps) {
       // -------------------- poll: slot words + per-move masks
       const int used = sh.used;
-      if (tid < used) {
-        const uint64_t* rw = a.res + ((size_t)par * a.nslots + tid) * kResWords;
+      for (int sl = tid; sl < used; sl += kPollThreads) {
+        const uint64_t* rw = a.res + ((size_t)par * a.nslots + sl) * kResWords;
         uint64_t w[6];
         for (;;) {
           bool ok = true;
@@ -910,108 +954,107 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           __nanosleep(a.poll_ns);
         }
 #pragma unroll
-        for (int j = 0; j < 6; ++j) sh.sw[tid][j] = w[j] & kPay;
+        for (int j = 0; j < 6; ++j) sh.sw[sl][j] = w[j] & kPay;
         const uint32_t w0 = (uint32_t)w[0];
         const uint32_t bits = (uint32_t)((w[0] & kPay) >> 16);
-        const int i = (int)((w[4] >> 32) & 63), v = (int)((w[4] >> 38) & 31);
+        const int i = (int)((w[4] >> 32) & 127), v = (int)((w[4] >> 39) & 31);
         const int kind = (int)(w0 & 3);
         if (v == 0) sh.mkind[i] = (uint8_t)kind;
-        if (kind == 1) {
+        // walk masks indexed by the N offset: bit j <-> d = j - kInsSpan/2
+        if (kind == 1) {  // one slot, an accept bit per N
+          const bool cf = (w0 & kFConflict) != 0;
           sh.macc[i] = bits;
-          sh.mcf[i] = (w0 & kFConflict) ? 1u : 0u;
-          sh.mov[i] = (w0 & kFOverflow) ? 1u : 0u;
-        } else {
-          if (bits & 1u) atomicOr(&sh.macc[i], 1u << v);
-          if (w0 & kFConflict) atomicOr(&sh.mcf[i], 1u << v);
-          if (w0 & kFOverflow) atomicOr(&sh.mov[i], 1u << v);
+          sh.mcov[i] = cf ? 0u : 0xffffffffu;
+          sh.mcf[i] = cf ? 0xffffffffu : 0u;
+          sh.mov[i] = (w0 & kFOverflow) ? 0xffffffffu : 0u;
+        } else {  // variant v evaluated d = centre(i) + off(v)
+          const int j = var_centre(rate, i) + var_off(v, bias) + kInsSpan / 2;
+          if (j >= 0 && j < kInsSpan) {
+            const uint32_t b = 1u << j;
+            if (bits & 1u) atomicOr(&sh.macc[i], b);
+            if (w0 & kFConflict) atomicOr(&sh.mcf[i], b);
+            else atomicOr(&sh.mcov[i], b);
+            if (w0 & kFOverflow) atomicOr(&sh.mov[i], b);
+          }
         }
       }
       group_sync(1, kPollThreads);
       pc.mark(1);  // poll (waiting for the evaluators)
-      if (warp == 0) {  // ---- walk
+      if (warp == 0) {  // ---- walk (table-driven: bit j of a mask <-> d = j - 16)
         const int fit = sh.fit;
-        uint32_t accm[2], cfm[2], ovm[2];
-        int kind[2], cntv[2], fs[2];
-        for (int h = 0; h < 2; ++h) {
+        uint32_t accm[kMH], stopm[kMH], ovfm[kMH], cfmk[kMH];
+        unsigned kins[kMH], kdel[kMH];
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) {
           const int i = lane + 32 * h;
-          accm[h] = cfm[h] = ovm[h] = 0;
-          kind[h] = cntv[h] = fs[h] = 0;
-          if (i < fit) {
-            accm[h] = sh.macc[i];
-            cfm[h] = sh.mcf[i];
-            ovm[h] = sh.mov[i];
-            kind[h] = sh.mkind[i];
-            cntv[h] = (i == 0 || kind[h] == 1) ? 1 : a.nvar;
-            fs[h] = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
-          }
+          const bool in = i < fit;
+          const int kd = in ? sh.mkind[i] : 0;
+          accm[h] = in ? sh.macc[i] : 0u;
+          stopm[h] = in ? ~sh.mcov[i] : 0xffffffffu;
+          cfmk[h] = in ? sh.mcf[i] : 0u;
+          ovfm[h] = in ? sh.mov[i] : 0u;
+          kins[h] = __ballot_sync(0xffffffffu, kd == 1);
+          kdel[h] = __ballot_sync(0xffffffffu, kd == 2);
         }
         pc.mark(6);  // walk: masks
-        int d = 0, start = 0, nacc = 0, len = fit, err = 0, eslot = -1, why = kStopEnd;
+        int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
+        int di[kMH];
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) di[h] = 0;  // N offset at my moves
+        int acc_e = -1, acc_dd = 0;  // lane k < nacc holds accepted move k and its d
         for (;;) {
-          bool ev[2], stp[2];
-          int slot[2], vi[2], why_l[2];
-          for (int h = 0; h < 2; ++h) {
+          const int j = d + kInsSpan / 2;
+          const bool inr = j >= 0 && j < kInsSpan;
+          int e = -1, eh = 0;
+          bool est = false, eov = false, ecf = false;
+#pragma unroll
+          for (int h = 0; h < kMH; ++h) {
+            if (e >= 0) break;
             const int i = lane + 32 * h;
-            ev[h] = stp[h] = false;
-            slot[h] = -1;
-            vi[h] = 0;
-            why_l[h] = kStopEnd;
-            if (i >= start && i < fit) {
-              bool acc = false, st = false;
-              if (kind[h] == 1) {
-                const int j = d + kInsSpan / 2;
-                if (j < 0 || j >= kInsSpan) { st = true; why_l[h] = kStopVariant; }
-                else if (cfm[h]) { st = true; why_l[h] = kStopPrev; }
-                else acc = (accm[h] >> j) & 1u;
-              } else {
-                vi[h] = var_of(d - var_centre(rate, i), bias);
-                if (vi[h] >= cntv[h]) { st = true; why_l[h] = kStopVariant; }
-                else if ((cfm[h] >> vi[h]) & 1u) { st = true; why_l[h] = kStopPrev; }
-                else acc = (accm[h] >> vi[h]) & 1u;
-              }
-              if (!st) {
-                slot[h] = fs[h] + (kind[h] == 1 ? 0 : vi[h]);
-                sh.res_s[i] = slot[h];
-                sh.res_d[i] = d;
-              }
-              stp[h] = st;
-              ev[h] = st || acc;
+            const bool act = i >= start && i < fit;
+            const bool st = act && (!inr || ((stopm[h] >> j) & 1u));
+            const bool ac = act && inr && ((accm[h] >> j) & 1u);
+            const unsigned b = __ballot_sync(0xffffffffu, st || ac);
+            if (b) {
+              const int el = __ffs(b) - 1;
+              e = 32 * h + el;
+              eh = h;
+              const unsigned bit = 1u << el;
+              est = (__ballot_sync(0xffffffffu, st) & bit) != 0;
+              eov = (__ballot_sync(0xffffffffu, ac && ((ovfm[h] >> j) & 1u)) & bit) != 0;
+              ecf = (__ballot_sync(0xffffffffu, act && inr && ((cfmk[h] >> j) & 1u)) & bit) != 0;
             }
           }
-          const unsigned b0 = __ballot_sync(0xffffffffu, ev[0]);
-          const unsigned b1 = __ballot_sync(0xffffffffu, ev[1]);
-          if (!b0 && !b1) {
+          if (e < 0) {
             len = fit;
             why = kStopEnd;
             break;
           }
-          const int e = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
-          const int eh = e >> 5, el = e & 31;
-          const bool est = __shfl_sync(0xffffffffu, eh ? stp[1] : stp[0], el);
           if (est) {
             len = e;
-            why = __shfl_sync(0xffffffffu, eh ? why_l[1] : why_l[0], el);
+            why = ecf ? kStopPrev : kStopVariant;
             break;
           }
-          const int es = __shfl_sync(0xffffffffu, eh ? slot[1] : slot[0], el);
-          const int ek = __shfl_sync(0xffffffffu, eh ? kind[1] : kind[0], el);
-          const int eo = __shfl_sync(0xffffffffu,
-                                     (int)(eh ? (ovm[1] >> (kind[1] == 1 ? 0 : vi[1])) & 1u
-                                              : (ovm[0] >> (kind[0] == 1 ? 0 : vi[0])) & 1u), el);
-          if (eo) {  // the reference throws inside the commit of move e
-            len = e;
+          if (eov) {
+            len = e;  // the reference throws inside the commit of move e
             err = 1;
-            eslot = es;
             why = kStopOverflow;
             break;
           }
-          if (lane == 0) {
-            sh.acc_i[nacc] = e;
-            sh.acc_s[nacc] = es;
-            sh.acc_d[nacc] = (int)((int64_t)n + d);  // store size before move e
+          if (lane == nacc) {
+            acc_e = e;
+            acc_dd = d;
           }
           ++nacc;
-          d += ek == 1 ? 1 : (ek == 2 ? -1 : 0);
+          const unsigned bit = 1u << (e & 31);
+          int delta = 0;
+#pragma unroll
+          for (int h = 0; h < kMH; ++h)
+            if (h == eh) delta = (kins[h] & bit) ? 1 : ((kdel[h] & bit) ? -1 : 0);
+#pragma unroll
+          for (int h = 0; h < kMH; ++h)
+            if (lane + 32 * h > e) di[h] += delta;
+          d += delta;
           start = e + 1;
           if (nacc == kMaxAcc) {
             len = e + 1;
@@ -1020,12 +1063,37 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           }
         }
         pc.mark(7);  // walk: iterations
+        // resolved slots of the consumed moves, accepted list
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) {
+          const int i = lane + 32 * h;
+          if (i < len) {
+            const int k = sh.mkind[i];
+            const int dd = di[h];
+            const int fs = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
+            sh.res_s[i] = fs + (k == 1 ? 0 : var_of(dd - var_centre(rate, i), bias));
+            sh.res_d[i] = dd;
+          }
+        }
+        if (lane < nacc) {
+          const int i = acc_e;
+          const int k = sh.mkind[i];
+          const int fs = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
+          sh.acc_i[lane] = i;
+          sh.acc_s[lane] = fs + (k == 1 ? 0 : var_of(acc_dd - var_centre(rate, i), bias));
+          sh.acc_d[lane] = (int)((int64_t)n + acc_dd);  // store size before move i
+        }
+        if (err) {  // the overflowing move's slot
+          const int i = len;
+          const int k = sh.mkind[i];
+          const int fs = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
+          if (lane == 0) sh.err_slot = fs + (k == 1 ? 0 : var_of(d - var_centre(rate, i), bias));
+        }
         if (lane == 0) {
           sh.len = len;
           sh.nacc = nacc;
           sh.cmin = len;
           sh.err = err;
-          sh.err_slot = eslot;
           sh.why = why;
         }
       }
@@ -1033,9 +1101,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       pc.mark(2);  // walk
       {  // ---- verify: every consumed move against the accepted moves before it
         const int len = sh.len, nacc = sh.nacc;
-        const int i = tid & 63;
+        const int i = tid % kMaxMoves;
         if (i < len)
-          for (int j = tid >> 6; j < nacc; j += kPollThreads / 64) {
+          for (int j = tid / kMaxMoves; j < nacc; j += kPollThreads / kMaxMoves) {
             if (i <= sh.acc_i[j]) continue;
             const RW ri = rw_of(sh.sw[sh.res_s[i]]);
             RW wj = rw_of(sh.sw[sh.acc_s[j]]);
@@ -1078,7 +1146,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     const bool stop = nbase >= a.nmoves || sh.err;
     if (warp == 0) {
       publish(a, r + 1, nbase, nn, nacc, bias, stop, rate, sh, lane);
-    } else if (warp == 1 || warp == 2) {  // hand the round to the helpers
+    } else if (warp >= 1 && warp <= kMaxMoves / 32) {  // hand the round to the helpers
       Round& D = sh.done;
       const int i = tid - 32;
       if (i < len) {
@@ -1119,7 +1187,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       cp_async_wait();
     } else if (tid < 32 + kMaxMoves) {
-      sh.macc[tid - 32] = sh.mcf[tid - 32] = sh.mov[tid - 32] = 0;
+      sh.macc[tid - 32] = sh.mcov[tid - 32] = sh.mcf[tid - 32] = sh.mov[tid - 32] = 0;
     }
     __syncthreads();
     pc.mark(5);  // close + publish + next shape

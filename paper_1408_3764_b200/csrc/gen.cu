@@ -219,8 +219,12 @@ __global__ void __launch_bounds__(kThreads) k_gen(GenArgs a) {
 }  // namespace
 
 gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s) {
+  return gen_proposals_into(c, c.mt, c.props, n, s);
+}
+
+gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n, cudaStream_t s) {
   if (n == 0) return GCMC_OK;
-  GenArgs a{c.mt, c.props, n, c.params.displace_percent, c.box.l,
+  GenArgs a{mt, out, n, c.params.displace_percent, c.box.l,
             c.params.max_displacement > 0.0 ? 1 : 0};
   k_gen<<<1, kThreads, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();

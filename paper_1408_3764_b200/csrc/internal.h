@@ -27,6 +27,12 @@ struct Chain {
   // proposal ring (engine input)
   Proposal* props = nullptr;
   uint64_t props_cap = 0;
+  // proposals generated ahead for the next batch (on gen_stream, on the SM
+  // the engine leaves free) and the MT state after them
+  Proposal* props_next = nullptr;
+  uint64_t* mt_next = nullptr;
+  uint64_t ahead_n = 0;
+  cudaEvent_t ev_mt = nullptr, ev_ahead = nullptr;
   gcmc_trace_rec* trace = nullptr;
   uint64_t trace_cap = 0;
   // scratch for single-move API / batches
@@ -70,6 +76,7 @@ gcmc_status total_energy(Chain& c, double* u, double* w);
 
 // gen.cu: parse the next `n` moves of the MT stream into c.props[0..n).
 gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s);
+gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n, cudaStream_t s);
 
 // engine.cu: run n moves from c.props; optional device trace.
 gcmc_status engine_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);

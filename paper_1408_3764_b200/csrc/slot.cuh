@@ -47,20 +47,20 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Warp 0 of the group: windows, occupancy prefix and candidate expansion.
-// Centres and nwin/sign1/excl must already be in ws. occ_s: shared replica
-// (nullptr -> global m.occ).
+// Warp 0 of the group, step 1 (per window): the pruned brick window of a
+// centre appended to ws.brick[nent..]; returns the new entry count.
 template <int T>
-__device__ __forceinline__ void win_setup_warp(const Mirror& m, const Box& b, WinWs<T>& ws,
-                                               const uint8_t* occ_s, int lane) {
-  int nent = 0;
-  for (int w = 0; w < ws.nwin; ++w) {
-    const int c = window_bricks_warp(m, b, ws.cx[w], ws.cy[w], ws.cz[w], ws.brick + nent, lane);
-    if (w == 0 && lane == 0) ws.nent0 = c;
-    nent += c;
-  }
+__device__ __forceinline__ int win_add(const Mirror& m, const Box& b, WinWs<T>& ws, int nent,
+                                       double x, double y, double z, int lane) {
+  return nent + window_bricks_warp(m, b, x, y, z, ws.brick + nent, lane);
+}
+
+// Warp 0 of the group, step 2: occupancies (shared-memory replica or global),
+// exclusive prefix over nent <= 54 entries, candidate expansion.
+template <int T>
+__device__ __forceinline__ void win_finish(const Mirror& m, WinWs<T>& ws, const uint8_t* occ_s,
+                                           int nent, int nent0, int lane) {
   __syncwarp();
-  // occupancies + exclusive prefix over nent <= 54 entries (two per lane)
   int o0 = 0, o1 = 0;
   if (lane < nent) {
     const uint32_t id = ws.brick[lane];
@@ -87,6 +87,7 @@ __device__ __forceinline__ void win_setup_warp(const Mirror& m, const Box& b, Wi
   if (lane + 32 < nent) ws.pre[lane + 32] = e1;
   const int total = __shfl_sync(0xffffffffu, s1, 31);
   if (lane == 0) {
+    ws.nent0 = nent0;
     ws.nent = nent;
     ws.pre[nent] = total;
     ws.total = total;
@@ -96,6 +97,18 @@ __device__ __forceinline__ void win_setup_warp(const Mirror& m, const Box& b, Wi
     if (e0 + k < kCandMax) ws.cand[e0 + k] = (uint16_t)((lane << 7) | k);
   for (int k = 0; k < o1; ++k)
     if (e1 + k < kCandMax) ws.cand[e1 + k] = (uint16_t)(((lane + 32) << 7) | k);
+}
+
+// Both steps for the windows already described in ws (cx/cy/cz, nwin).
+template <int T>
+__device__ __forceinline__ void win_setup_warp(const Mirror& m, const Box& b, WinWs<T>& ws,
+                                               const uint8_t* occ_s, int lane) {
+  int nent = 0, nent0 = 0;
+  for (int w = 0; w < ws.nwin; ++w) {
+    nent = win_add<T>(m, b, ws, nent, ws.cx[w], ws.cy[w], ws.cz[w], lane);
+    if (w == 0) nent0 = nent;
+  }
+  win_finish<T>(m, ws, occ_s, nent, nent0, lane);
 }
 
 __device__ __forceinline__ void lj_accum(const Box& b, double r2, double sign, double& du,

@@ -456,3 +456,19 @@ def test_draw_counts_match_reference():
     expect = 6 * np.sum(kinds == 0) + 6 * np.sum(kinds == 1) + 4 * np.sum(kinds == 2)
     start = E().random_initial_configuration(512, (512 / 0.67) ** (1 / 3), 0.85, 1)[1].draws
     assert r.draws - start == expect
+
+
+@pytest.mark.parametrize("strategy,n0", [("microcell", 4096), ("cell_list", 4096), ("all_pairs", 1024)])
+def test_drop_in_strategy_against_reference(strategy, n0):
+    """include/gcmc_b200_strategy.hpp as a gcmc::NeighborStrategy, driven
+    side by side with the reference's own strategy (oracle/shim_check.cpp):
+    ΔE within 1e-10, identical stores, byte-identical grids after commits,
+    clean rebuild_check, the reference's exception types and messages."""
+    import subprocess
+
+    if not os.path.exists(O.SHIM):
+        pytest.skip("oracle/_ref/shim_check not built (needs the reference headers)")
+    r = subprocess.run([O.SHIM, strategy, str(n0), "3000", "5"], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "fails=0" in r.stdout, r.stdout
