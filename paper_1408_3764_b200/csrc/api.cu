@@ -182,14 +182,14 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     const int max_ctas = 1 + engine_max_slots() / mg;
     if (c->engine_ctas > max_ctas) c->engine_ctas = max_ctas;
   }
-  c->engine_variants = P.engine_variants > 0 ? (P.engine_variants > 31 ? 31 : P.engine_variants) : 7;
+  c->engine_variants = P.engine_variants > 0 ? (P.engine_variants > 31 ? 31 : P.engine_variants) : 9;
   c->engine_bias = P.engine_bias > 0 ? 1 : -1;
   // Evaluation mirror: bricks of side L/dims >= r_cut (1e-9 relative margin).
   {
     Mirror& m = c->mirror;
     int d = (int)std::floor(P.box_length / (P.r_cut * (1.0 + 1e-9)));
     if (d < 1) d = 1;
-    if (d > 1024) d = 1024;
+    if (d > 255) d = 255;  // packed 8-bit brick coordinates (mirror.cuh)
     m.dims = d;
     m.nb = (uint32_t)d * d * d;
     m.side = P.box_length / d;
@@ -595,9 +595,16 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
       c.ahead_n = mn;
     }
     if (std::getenv("GCMC_ENGINE_PROFILE") && !c.prof) {
-      CK(cudaMalloc(&c.prof, 48 * sizeof(unsigned long long)), "prof");
+      CK(cudaMalloc(&c.prof, 4096 * sizeof(unsigned long long)), "prof");
     }
-    if (c.prof) CK(cudaMemsetAsync(c.prof, 0, 48 * sizeof(unsigned long long), c.stream), "prof");
+    if (c.prof) CK(cudaMemsetAsync(c.prof, 0, 4096 * sizeof(unsigned long long), c.stream), "prof");
+    const bool lat = std::getenv("GCMC_ENGINE_LATENCY") != nullptr;
+    if (lat && !c.stamp) CK(cudaMalloc(&c.stamp, 5 * 8192 * sizeof(unsigned long long)), "stamp");
+    if (lat) {
+      std::vector<unsigned long long> init(5 * 8192, 0);
+      for (int k = 0; k < 8192; ++k) init[5 * k + 1] = ~0ull;
+      CK(cudaMemcpyAsync(c.stamp, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c.stream), "stamp");
+    }
     CK(cudaEventRecord(c.ev[1], c.stream), "event");
     if ((s = engine_run(c, m, trace ? c.trace : nullptr, c.stream))) return s;
     CK(cudaEventRecord(c.ev[2], c.stream), "event");
@@ -613,7 +620,7 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     eng_ms += b;
     rounds += c.st_host->rounds;
     if (c.prof) {
-      unsigned long long hp[48];
+      unsigned long long hp[64];
       cudaMemcpy(hp, c.prof, sizeof hp, cudaMemcpyDeviceToHost);
       const double R = (double)(hp[15] ? hp[15] : 1);
       const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "close_publish", "walk_masks", "walk_iter"};
@@ -626,6 +633,24 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
                    hp[33] / R);
       std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",
                    hp[40], hp[41], hp[42], hp[43], hp[44], hp[45]);
+      if (c.stamp) {
+        std::vector<unsigned long long> st(5 * 8192);
+        cudaMemcpy(st.data(), c.stamp, st.size() * 8, cudaMemcpyDeviceToHost);
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        int cnt = 0;
+        for (int k = 2; k < 8192 && k < (int)hp[15]; ++k) {
+          const unsigned long long* e = &st[5 * k];
+          if (!e[0] || e[1] == ~0ull || !e[3] || !e[4]) continue;
+          a0 += (double)(long long)(e[1] - e[0]);
+          a1 += (double)(long long)(e[2] - e[0]);
+          a2 += (double)(long long)(e[3] - e[0]);
+          a3 += (double)(long long)(e[4] - e[3]);
+          ++cnt;
+        }
+        if (cnt)
+          std::fprintf(stderr, "[engine prof] latency ns (%d rounds): publish->first CTA sees D=%.0f publish->last CTA sees D=%.0f publish->last result=%.0f last result->sequencer has all=%.0f\n",
+                       cnt, a0 / cnt, a1 / cnt, a2 / cnt, a3 / cnt);
+      }
     }
     if (c.st_host->error) break;
     done += m;

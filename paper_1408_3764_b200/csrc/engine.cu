@@ -50,9 +50,11 @@ constexpr int kMaxAcc = 32;      // accepted moves per round
 constexpr int kRing = 256;       // proposal ring (moves)
 constexpr int kPre = 2 * kMaxMoves + 2;  // slot prefix entries
 constexpr int kDecHdr = 4;
-constexpr int kDecEnt = 5;
-constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 164
-constexpr int kResWords = 8;     // 6 used
+constexpr int kDecEnt = 2;
+constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 68
+constexpr int kDecStride = 80;
+constexpr int kMaxCtas = 1;
+constexpr int kResWords = 3;     // tagged words per slot result (dense per-word arrays)
 constexpr int kPollWarps = 12;   // sequencer warps that poll / walk / verify
 constexpr int kSlotsPerPoller = 2;
 constexpr int kMaxSlots = kPollWarps * 32 * kSlotsPerPoller;
@@ -89,14 +91,16 @@ struct EngineArgs {
   uint64_t equil, interval;
   int tail, nslots;  // nslots = (gridDim.x - 1) * MG
   double tail_cu, tail_cp, tail_s3, tail_bu, tail_bp;
-  uint64_t* dec;     // [kDecWords]
-  uint64_t* res;     // [2][nslots][kResWords]
+  uint64_t* dec;     // [kDecStride] decision words
+  uint64_t* res;     // [2][kResWords][nslots]
   SlotExt* ext;      // [2][nslots]
   int smem_occ;      // mirror occupancy replicated in shared memory
   int bias0;         // initial variant bias (+1 / -1)
   int nvar;          // variants per displace / delete proposal (move index >= 1)
-  unsigned poll_ns;  // back-off between polls
+  unsigned poll_ns;  // back-off between polls (sequencer)
+  unsigned epoll_ns;  // back-off between polls (evaluators)
   unsigned long long* prof;
+  unsigned long long* stamp;  // profiling: [0] publish time, [1 + slot] (seen, done) pairs
 };
 
 // ----------------------------------------------------------------- words
@@ -252,12 +256,10 @@ __device__ __forceinline__ bool conflict(const Mirror& m, bool all_pairs, const 
   if (all_pairs) return true;
   if (r.ia >= 0 && (r.ia == w.ia || r.ia == w.ib)) return true;
   if (r.ib >= 0 && (r.ib == w.ia || r.ib == w.ib)) return true;
-#pragma unroll
-  for (int x = 0; x < 3; ++x)
-#pragma unroll
-    for (int y = 0; y < 3; ++y)
-      if (mnear(m, r.pt[x], w.pt[y])) return true;
-  return false;
+  // points: new (0) and old (1); pt[2] is unused since deletions no longer
+  // read the last particle during evaluation
+  return mnear(m, r.pt[0], w.pt[0]) || mnear(m, r.pt[0], w.pt[1]) ||
+         mnear(m, r.pt[1], w.pt[0]) || mnear(m, r.pt[1], w.pt[1]);
 }
 
 // ----------------------------------------------------------------- decision
@@ -296,9 +298,10 @@ __device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, u
 __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane) {
   constexpr int PER = (kDecWords + 31) / 32;
   uint64_t w[PER];
+  const uint64_t* dec = a.dec;  // one copy, polled by every evaluator CTA
   for (;;) {
-    w[0] = ld_relaxed(a.dec + lane);
-    w[1] = ld_relaxed(a.dec + 32 + lane);
+    w[0] = ld_relaxed(dec + lane);
+    w[1] = ld_relaxed(dec + 32 + lane);
     const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2);
     const bool h2ok = tagged(h2, r);
     const int nacc = h2ok ? (int)(h2 & 0xff) : 0;
@@ -307,7 +310,7 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
 #pragma unroll
       for (int j = 2; j < PER; ++j) {
         const int idx = lane + 32 * j;
-        w[j] = idx < need ? ld_relaxed(a.dec + idx) : 0;
+        w[j] = idx < need ? ld_relaxed(dec + idx) : 0;
       }
     }
     bool ok = h2ok;
@@ -317,7 +320,7 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
       if (idx < need && !tagged(w[j], r)) ok = false;
     }
     if (__all_sync(0xffffffffu, ok)) break;
-    __nanosleep(a.poll_ns);
+    __nanosleep(a.epoll_ns);
   }
   const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2) & kPay;
   const int nacc = (int)(h2 & 0xff);
@@ -336,14 +339,15 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
       d.rate = (int)(int16_t)(uint16_t)((p >> 10) & 0xffff);
     } else if (idx >= kDecHdr) {
       const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
-      if (f < 3) d.acc[e].pt[f] = p;
-      else if (f == 3) {
+      if (f == 0) {
+        d.acc[e].pt[0] = p & kNoPoint;
+        d.acc[e].pt[1] = (p >> 24) & kNoPoint;
+        d.acc[e].pt[2] = kNoPoint;
+      } else {
         d.kind[e] = (int)(p >> 32) & 3;
         const uint32_t ia = (uint32_t)p;
         d.acc[e].ia = ia == 0xffffffffu ? -1 : (int64_t)ia;
-      } else {
-        const uint32_t ib = (uint32_t)p;
-        d.acc[e].ib = ib == 0xffffffffu ? -1 : (int64_t)ib;
+        d.acc[e].ib = -1;
       }
     }
   }
@@ -420,6 +424,11 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     if (tid < 32) {
       poll_dec(a, r, sh.d, lane);
       pc.mark(1);  // D observed
+      if (a.stamp && lane == 0) {
+        const unsigned long long t = gtimer();
+        atomicMin(a.stamp + 5 * (r & 8191) + 1, t);  // first CTA sees D_r
+        atomicMax(a.stamp + 5 * (r & 8191) + 2, t);  // last CTA sees D_r
+      }
       const Dec& d = sh.d;
       // replica: the previous round's commits (a--, b++)
       if (occ_s && lane < d.nacc) {
@@ -446,10 +455,12 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     const Dec& d = sh.d;
     if (d.stop) break;
     pc.mark(2);  // replica + slot
-    uint64_t* rw = a.res + ((size_t)(r & 1) * a.nslots + cta_slot0 + g) * kResWords;
+    uint64_t* rw = a.res + (size_t)(r & 1) * kResWords * a.nslots + cta_slot0 + g;  // + j * nslots
     SlotExt* ex = a.ext + (size_t)(r & 1) * a.nslots + cta_slot0 + g;
     if (G.i >= 0) {
       int ocb = 0;
+      int setup_nent = 0, setup_nent0 = 0;
+      const int bar_pair = 1 + MG + g;  // warps 0 and 1 of the group
       // ---- setup (warp 0 of the group)
       if (gw == 0) {
         const uint64_t mv = d.base + (uint64_t)G.i;
@@ -512,22 +523,12 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
             nent = win_add<T>(a.m, a.b, ws, nent, md.ox, md.oy, md.oz, lane);
             if (kind == 2) nent0 = nent;
           }
-          win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
         }
-        // read set and conflicts with the previous round's commits (lanes over entries)
-        RW rs;
-        rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
-        rs.pt[1] = loads ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
-        rs.pt[2] = kNoPoint;  // a deletion's last particle is read by its commit, not here
-        rs.ia = loads ? (int64_t)pid : -1;
-        rs.ib = -1;
-        bool cf = false;
-        if (!empty && lane < d.nacc) cf = conflict(a.m, all_pairs, rs, d.acc[lane]);
-        cf = __any_sync(0xffffffffu, cf);
+        setup_nent = nent;
+        setup_nent0 = nent0;
         if (lane == 0) {
           G.kind = kind;
           G.empty = empty;
-          G.cf = cf;
           G.pid = pid;
           G.q = q;
           G.nv = (uint64_t)(nv < 0 ? 0 : nv);
@@ -552,6 +553,25 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           }
           if (empty) ws.total = 0;
         }
+        group_sync(bar_pair, 64);  // G published to warp 1
+        if (!all_pairs && !G.empty) win_finish<T>(a.m, ws, occ_s, setup_nent, setup_nent0, lane);
+      } else if (gw == 1) {
+        // read set and conflicts with the previous round's commits, in
+        // parallel with warp 0's window finish
+        group_sync(bar_pair, 64);
+        const int kind = G.kind;
+        const MoveData& md = G.md;
+        const bool loads = kind != 1 && !G.empty;
+        RW rs;
+        rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
+        rs.pt[1] = loads ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
+        rs.pt[2] = kNoPoint;
+        rs.ia = loads ? (int64_t)G.pid : -1;
+        rs.ib = -1;
+        bool cf = false;
+        if (!G.empty && lane < d.nacc) cf = conflict(a.m, all_pairs, rs, d.acc[lane]);
+        cf = __any_sync(0xffffffffu, cf);
+        if (lane == 0) G.cf = cf;
       }
       group_sync(bar_id, T);
       pc.mark(3);  // setup (pid hop + window)
@@ -619,21 +639,16 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         ovf = __shfl_sync(0xffffffffu, ovf, 0);
         const uint32_t flags = (uint32_t)kind | (cf ? kFConflict : 0u) | (ovf ? kFOverflow : 0u) |
                                (G.empty ? kFEmpty : 0u);
-        if (lane < 6) {
+        if (lane < kResWords) {
           uint64_t p;
-          switch (lane) {
-            case 0: p = (uint64_t)flags | ((uint64_t)bits << 16); break;
-            case 1: p = rs.pt[0]; break;
-            case 2: p = rs.pt[1]; break;
-            case 3: p = rs.pt[2]; break;
-            case 4:
-              p = (uint64_t)(rs.ia < 0 ? 0xffffffffu : (uint32_t)rs.ia) |
-                  ((uint64_t)G.i << 32) | ((uint64_t)G.v << 39);
-              break;
-            default: p = (uint32_t)(rs.ib < 0 ? 0xffffffffu : (uint32_t)rs.ib); break;
-          }
-          st_relaxed(rw + lane, tagw(r, p));
+          if (lane == 0) p = (uint64_t)flags | ((uint64_t)bits << 8);
+          else if (lane == 1) p = (rs.pt[0] & kNoPoint) | ((rs.pt[1] & kNoPoint) << 24);
+          else
+            p = (uint64_t)(rs.ia < 0 ? 0xffffffffu : (uint32_t)rs.ia) | ((uint64_t)G.i << 32) |
+                ((uint64_t)G.v << 39);
+          st_relaxed(rw + (size_t)lane * a.nslots, tagw(r, p));
         }
+        if (a.stamp && lane == 0) atomicMax(a.stamp + 5 * (r & 8191) + 3, gtimer());  // last result
         pc.mark(5);  // bits + publish
         // off the critical path: payload, then its own tag after a release
         if (lane == 0) {
@@ -685,7 +700,7 @@ enum Stop { kStopEnd, kStopVariant, kStopPrev, kStopVerify, kStopFull, kStopOver
 
 struct SeqShared {
   Proposal ring[kRing];
-  uint64_t sw[kMaxSlots][6];  // slot words of the current round (payload)
+  uint64_t sw[kMaxSlots][kResWords];  // slot words of the current round (payload)
   int Q[kPre];
   int fit, used;
   // per-move masks built by the pollers
@@ -699,17 +714,20 @@ struct SeqShared {
   Round done;            // previous round, processed by the helpers
   double acc_du[kMaxAcc], acc_dw[kMaxAcc];
   unsigned long long stops[kNStop];
+  unsigned long long lat[6];
+  uint64_t dw[kDecWords];  // decision words being broadcast
+  int dneed;
   ChainState ks;
 };
 
 __device__ __forceinline__ RW rw_of(const uint64_t* w) {
   RW x;
-  x.pt[0] = w[1];
-  x.pt[1] = w[2];
-  x.pt[2] = w[3];
-  const uint32_t ia = (uint32_t)w[4], ib = (uint32_t)w[5];
+  x.pt[0] = w[1] & kNoPoint;
+  x.pt[1] = (w[1] >> 24) & kNoPoint;
+  x.pt[2] = kNoPoint;
+  const uint32_t ia = (uint32_t)w[2];
   x.ia = ia == 0xffffffffu ? -1 : (int64_t)ia;
-  x.ib = ib == 0xffffffffu ? -1 : (int64_t)ib;
+  x.ib = -1;
   return x;
 }
 
@@ -736,12 +754,13 @@ __device__ __forceinline__ Observables observables(const EngineArgs& a, uint64_t
   return {ru, p};
 }
 
-// One warp: decision D_r (base, N, the previous round's accepted moves).
-// No fence here: the helpers fenced their commit stores before the barrier
-// that precedes this call, so every commit is in L2 before any D word is.
-__device__ __forceinline__ void publish(const EngineArgs& a, uint32_t r, uint64_t base,
-                                        uint64_t n, int nacc, int bias, int stop, int rate,
-                                        const SeqShared& sh, int lane) {
+// Decision D_r (base, N, the previous round's accepted moves): one warp
+// composes the words in shared memory, then one thread per word stores them. No fence here: the helpers fenced their commit
+// stores before the barrier that precedes the broadcast, so every commit is
+// in L2 before any D word is.
+__device__ __forceinline__ void compose_dec(uint32_t r, uint64_t base, uint64_t n, int nacc,
+                                            int bias, int stop, int rate, SeqShared& sh,
+                                            int lane) {
   for (int idx = lane; idx < kDecHdr + kDecEnt * nacc; idx += 32) {
     uint64_t p = 0;
     if (idx == 0) p = base;
@@ -753,12 +772,15 @@ __device__ __forceinline__ void publish(const EngineArgs& a, uint32_t r, uint64_
       const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
       const uint64_t* w = sh.sw[sh.acc_s[e]];
       const int kind = (int)(w[0] & 3);
-      if (f < 3) p = w[1 + f];
-      else if (f == 3) p = ((uint64_t)kind << 32) | (kind == 1 ? (uint32_t)sh.acc_d[e] : (uint32_t)w[4]);
-      else p = (uint32_t)w[5];
+      if (f == 0) p = w[1];
+      else p = ((uint64_t)kind << 32) | (kind == 1 ? (uint32_t)sh.acc_d[e] : (uint32_t)w[2]);
     }
-    st_relaxed(a.dec + idx, tagw(r, p));
+    sh.dw[idx] = tagw(r, p);
   }
+  if (lane == 0) sh.dneed = kDecHdr + kDecEnt * nacc;
+}
+__device__ __forceinline__ void broadcast_dec(const EngineArgs& a, const SeqShared& sh, int tid) {
+  if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
 }
 
 // Helper warps (kPollWarps .. 15): commits, statistics and trace of the
@@ -911,6 +933,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     sh.done.len = 0;
     sh.err = 0;
     for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
+    for (int k = 0; k < 6; ++k) sh.lat[k] = 0;
   }
   if (tid < kMaxMoves) {
     sh.macc[tid] = sh.mcov[tid] = sh.mcf[tid] = sh.mov[tid] = 0;
@@ -931,7 +954,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   uint32_t r = 1;
   int rate = 0;         // drift of N per move, 1/256 units
   float rate_f = 0.0f;
-  if (warp == 0) publish(a, r, base, n, 0, bias, 0, rate, sh, lane);
+  if (warp == 0) compose_dec(r, base, n, 0, bias, 0, rate, sh, lane);
+  __syncthreads();
+  broadcast_dec(a, sh, tid);
   PhaseClock pc, ph;
   pc.start(a.prof && tid == 0);
   ph.start(a.prof && tid == kPollWarps * 32);
@@ -941,23 +966,23 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // -------------------- poll: slot words + per-move masks
       const int used = sh.used;
       for (int sl = tid; sl < used; sl += kPollThreads) {
-        const uint64_t* rw = a.res + ((size_t)par * a.nslots + sl) * kResWords;
-        uint64_t w[6];
+        const uint64_t* rw = a.res + (size_t)par * kResWords * a.nslots + sl;
+        uint64_t w[kResWords];
         for (;;) {
           bool ok = true;
 #pragma unroll
-          for (int j = 0; j < 6; ++j) {
-            w[j] = ld_relaxed(rw + j);
+          for (int j = 0; j < kResWords; ++j) {
+            w[j] = ld_relaxed(rw + (size_t)j * a.nslots);
             ok &= tagged(w[j], r);
           }
           if (ok) break;
           __nanosleep(a.poll_ns);
         }
 #pragma unroll
-        for (int j = 0; j < 6; ++j) sh.sw[sl][j] = w[j] & kPay;
+        for (int j = 0; j < kResWords; ++j) sh.sw[sl][j] = w[j] & kPay;
         const uint32_t w0 = (uint32_t)w[0];
-        const uint32_t bits = (uint32_t)((w[0] & kPay) >> 16);
-        const int i = (int)((w[4] >> 32) & 127), v = (int)((w[4] >> 39) & 31);
+        const uint32_t bits = (uint32_t)((w[0] & kPay) >> 8);
+        const int i = (int)((w[2] >> 32) & 127), v = (int)((w[2] >> 39) & 31);
         const int kind = (int)(w0 & 3);
         if (v == 0) sh.mkind[i] = (uint8_t)kind;
         // walk masks indexed by the N offset: bit j <-> d = j - kInsSpan/2
@@ -980,6 +1005,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(1);  // poll (waiting for the evaluators)
+      if (a.stamp && tid == 0) a.stamp[5 * (r & 8191) + 4] = gtimer();  // sequencer has all
       if (warp == 0) {  // ---- walk (table-driven: bit j of a mask <-> d = j - 16)
         const int fit = sh.fit;
         uint32_t accm[kMH], stopm[kMH], ovfm[kMH], cfmk[kMH];
@@ -1145,7 +1171,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     }
     const bool stop = nbase >= a.nmoves || sh.err;
     if (warp == 0) {
-      publish(a, r + 1, nbase, nn, nacc, bias, stop, rate, sh, lane);
+      compose_dec(r + 1, nbase, nn, nacc, bias, stop, rate, sh, lane);
     } else if (warp >= 1 && warp <= kMaxMoves / 32) {  // hand the round to the helpers
       Round& D = sh.done;
       const int i = tid - 32;
@@ -1162,7 +1188,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         D.acc_s[i] = sh.acc_s[i];
         D.acc_n[i] = sh.acc_d[i];
         D.acc_kind[i] = (int)(w[0] & 3);
-        D.acc_pid[i] = (uint32_t)w[4];
+        D.acc_pid[i] = (uint32_t)w[2];
       }
       if (i == 0) {
         D.base = base;
@@ -1175,6 +1201,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
     }
     __syncthreads();
+    if (a.stamp && tid == 0) a.stamp[5 * ((r + 1) & 8191)] = gtimer();  // publish of D_{r+1}
+    broadcast_dec(a, sh, tid);
     // next round's shape, masks, ring (while the evaluators work)
     if (warp == 0) {
       const uint64_t want = nbase + kRing < a.nmoves ? nbase + kRing : a.nmoves;
@@ -1205,6 +1233,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     pc.flush(a.prof);
     a.prof[15] = rounds;
     for (int k = 0; k < kNStop; ++k) a.prof[40 + k] = sh.stops[k];
+    for (int k = 0; k < 6; ++k) a.prof[48 + k] = sh.lat[k];
   }
   if (a.prof && tid == kPollWarps * 32) {
     a.prof[32] = ph.acc[0];
@@ -1272,6 +1301,7 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
   a.interval = P.sampling_interval;
   a.tail = P.tail_corrections;
   a.prof = c.prof;
+  a.stamp = c.stamp;
   {
     // potential.hpp:63-72 factored into constants with the same rounding:
     // u = (8/3)*pi * rho * eps * s3 * (sr9/3 - sr3)
@@ -1298,6 +1328,8 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
   {
     const char* e = std::getenv("GCMC_POLL_NS");
     a.poll_ns = e ? (unsigned)std::atoi(e) : 64u;
+    const char* f = std::getenv("GCMC_EPOLL_NS");
+    a.epoll_ns = f ? (unsigned)std::atoi(f) : 64u;
   }
   size_t eval_bytes = T == 128 ? sizeof(EvalShared<128>) : (T == 256 ? sizeof(EvalShared<256>) : sizeof(EvalShared<512>));
   eval_bytes = (eval_bytes + 15) & ~size_t(15);
@@ -1314,7 +1346,8 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return cuda_error(e, "engine smem");
   const size_t res_bytes = 2 * (size_t)a.nslots * kResWords * sizeof(uint64_t);
-  if ((e = cudaMemsetAsync(c.eng_dec, 0, kDecWords * sizeof(uint64_t), s))) return cuda_error(e, "engine");
+  if ((e = cudaMemsetAsync(c.eng_dec, 0, (size_t)kMaxCtas * kDecStride * sizeof(uint64_t), s)))
+    return cuda_error(e, "engine");
   if ((e = cudaMemsetAsync(c.eng_res, 0, res_bytes, s))) return cuda_error(e, "engine");
   if ((e = cudaMemsetAsync(c.eng_ext, 0, 2 * (size_t)a.nslots * sizeof(SlotExt), s))) return cuda_error(e, "engine");
   void* args[] = {&a};
@@ -1324,7 +1357,7 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
 }
 
 size_t engine_buffer_bytes(int nslots, size_t* dec, size_t* res, size_t* ext) {
-  *dec = kDecWords * sizeof(uint64_t);
+  *dec = (size_t)kMaxCtas * kDecStride * sizeof(uint64_t);
   *res = 2 * (size_t)nslots * kResWords * sizeof(uint64_t);
   *ext = 2 * (size_t)nslots * sizeof(SlotExt);
   return *dec + *res + *ext;

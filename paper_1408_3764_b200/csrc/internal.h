@@ -48,13 +48,14 @@ struct Chain {
   int sm_count = 0;
   int engine_ctas = 0;        // sequencer + evaluator CTAs
   int engine_group = 256;     // threads per evaluation slot
-  int engine_variants = 5;    // N-variants per displace/delete proposal (after the first)
+  int engine_variants = 9;    // N-variants per displace/delete proposal (after the first)
   int engine_bias = -1;       // initial variant order (+1: N expected to grow)
   uint64_t* eng_dec = nullptr;  // engine communication buffers (engine.cu)
   uint64_t* eng_res = nullptr;
   void* eng_ext = nullptr;
   bool built = false;
   unsigned long long* prof = nullptr;
+  unsigned long long* stamp = nullptr;  // per-round global timestamps (GCMC_ENGINE_LATENCY=1)
 };
 
 // Thread-local error plumbing (api.cu).

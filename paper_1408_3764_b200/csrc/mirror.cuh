@@ -3,7 +3,7 @@
 // commit.cuh).
 //
 // A point is summarised by its packed brick coordinates
-//   bx | by << 16 | bz << 32            (48 bits, kNoPoint = none)
+//   bx | by << 8 | bz << 16             (24 bits, kNoPoint = none; dims <= 255)
 // so that speculative evaluations can be checked against the positions an
 // accepted move changed: two points are "near" when their cyclic brick
 // distance is <= reach on every axis (reach >= 1 covers the 3x3x3 window and
@@ -13,19 +13,19 @@
 
 namespace gcmcb {
 
-constexpr uint64_t kNoPoint = 0xffffffffffffull;
+constexpr uint64_t kNoPoint = 0xffffffull;
 
 __device__ __forceinline__ int mcoord(const Mirror& m, double v) {
   const int c = (int)__dmul_rn(v, m.inv);
   return c < m.dims ? (c < 0 ? 0 : c) : m.dims - 1;
 }
 __device__ __forceinline__ uint64_t mpoint(const Mirror& m, double x, double y, double z) {
-  return (uint64_t)mcoord(m, x) | ((uint64_t)mcoord(m, y) << 16) |
-         ((uint64_t)mcoord(m, z) << 32);
+  return (uint64_t)mcoord(m, x) | ((uint64_t)mcoord(m, y) << 8) |
+         ((uint64_t)mcoord(m, z) << 16);
 }
-__device__ __forceinline__ int pt_x(uint64_t p) { return (int)(p & 0xffff); }
-__device__ __forceinline__ int pt_y(uint64_t p) { return (int)((p >> 16) & 0xffff); }
-__device__ __forceinline__ int pt_z(uint64_t p) { return (int)((p >> 32) & 0xffff); }
+__device__ __forceinline__ int pt_x(uint64_t p) { return (int)(p & 0xff); }
+__device__ __forceinline__ int pt_y(uint64_t p) { return (int)((p >> 8) & 0xff); }
+__device__ __forceinline__ int pt_z(uint64_t p) { return (int)((p >> 16) & 0xff); }
 __device__ __forceinline__ uint32_t mbrick(const Mirror& m, uint64_t p) {
   return (uint32_t)pt_x(p) + (uint32_t)m.dims * ((uint32_t)pt_y(p) + (uint32_t)m.dims * (uint32_t)pt_z(p));
 }

@@ -15,6 +15,7 @@ ap.add_argument("--moves", type=int, default=100000)
 ap.add_argument("--strategy", default="microcell")
 ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--warps", type=int, default=0)
+ap.add_argument("--variants", type=int, default=0)
 ap.add_argument("--sweep", action="store_true")
 ap.add_argument("--warm", type=int, default=20000)
 a = ap.parse_args()
@@ -26,7 +27,7 @@ print(f"init {time.time()-t:.1f}s", flush=True)
 cfg = RunConfig(temperature=2.0, chemical_potential=a.mu, box_length=box, strategy=a.strategy)
 
 def one(ctas, warps):
-    sim = E.Simulation(cfg, xyz, rng, engine_ctas=ctas, engine_group=warps)
+    sim = E.Simulation(cfg, xyz, rng, engine_ctas=ctas, engine_group=warps, engine_variants=a.variants)
     sim.run(a.warm)
     sim.run(a.moves)
     r = sim.last_run

@@ -81,6 +81,45 @@ __global__ void k_lat(const int* chase, int steps, const double4* recs, Box b, u
   sink[0] = x + y + acc + p + q + pid;
 }
 
+__device__ __forceinline__ unsigned long long ldr(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void str(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Two CTAs on different SMs bounce a counter through global memory:
+// per iteration = two one-way store->load visibility latencies.
+__global__ void k_pingpong(unsigned long long* flag, unsigned long long* ack, int iters,
+                           unsigned long long* out) {
+  if (threadIdx.x) return;
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (blockIdx.x == 0) {
+    const unsigned long long t0 = clock64();
+    for (int i = 1; i <= iters; ++i) {
+      str(flag, i);
+      while (ldr(ack) != (unsigned long long)i) {}
+    }
+    out[0] = (clock64() - t0) / iters;
+    out[2] = smid;
+  } else {
+    for (int i = 1; i <= iters; ++i) {
+      while (ldr(flag) != (unsigned long long)i) {}
+      str(ack, i);
+    }
+    out[3] = smid;
+  }
+}
+__global__ void k_relaxed_chase(const unsigned long long* chase, int steps, unsigned long long* out) {
+  if (threadIdx.x) return;
+  unsigned long long p = 0;
+  const unsigned long long t0 = clock64();
+  for (int i = 0; i < steps; ++i) p = ldr(chase + p);
+  out[1] = (clock64() - t0) / steps + (p == 12345678 ? 1 : 0);
+}
+
 int main() {
   const int N = 1 << 16;
   int* h = new int[N];
@@ -104,6 +143,26 @@ int main() {
   cudaMemcpy(ho, o, 16 * 8, cudaMemcpyDeviceToHost);
   const char* names[] = {"ld.cg chase", "ld chase", "dadd", "rint+dadd", "ddiv+dadd", "pair_term", "exp", "8x ld.cg batch", "double4 ld.cg chase"};
   for (int i = 0; i < 9; ++i) printf("%-22s %6llu cycles\n", names[i], ho[i]);
+  {
+    unsigned long long *flag, *ack, *po, *ch;
+    cudaMalloc(&flag, 4096); cudaMalloc(&ack, 4096); cudaMalloc(&po, 64); cudaMalloc(&ch, N * 8);
+    unsigned long long* hc = new unsigned long long[N];
+    for (int i = 0; i < N; ++i) hc[perm[i]] = perm[(i + 1) % N];
+    cudaMemcpy(ch, hc, N * 8, cudaMemcpyHostToDevice);
+    for (int grid : {2, 74, 148}) {
+      cudaMemset(flag, 0, 4096); cudaMemset(ack, 0, 4096);
+      k_pingpong<<<grid, 32>>>(flag, ack + 64, 2000, po);  // (blocks >1 idle)
+      cudaDeviceSynchronize();
+      unsigned long long hp[4];
+      cudaMemcpy(hp, po, 32, cudaMemcpyDeviceToHost);
+      printf("pingpong grid %3d (sm %llu <-> sm %llu): %llu cycles per round trip\n", grid, hp[2], hp[3], hp[0]);
+    }
+    k_relaxed_chase<<<1, 32>>>(ch, 4096, po);
+    cudaDeviceSynchronize();
+    unsigned long long hp[2];
+    cudaMemcpy(hp, po, 16, cudaMemcpyDeviceToHost);
+    printf("ld.relaxed.gpu chase: %llu cycles\n", hp[1]);
+  }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
