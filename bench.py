@@ -50,7 +50,9 @@ def parse_args():
     ap.add_argument("--strategy", default="microcell")
     ap.add_argument("--moves-per-step", type=int, default=1 << 18)
     ap.add_argument("--cpu-moves", type=int, default=100000,
-                    help="bounded CPU reference sample (moves)")
+                    help="(--impl reference) unused; kept for compatibility")
+    ap.add_argument("--cpu-steps", type=int, default=0,
+                    help="timed steps of the CPU baseline (0 = --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -132,28 +134,38 @@ def config_dict(a, world):
 
 
 def cpu_baseline(xyz, rng_hex, u0, w0, a, box):
-    """The reference's own Simulation::step loop (oracle/_ref) on this host,
-    resumed from the same start state (engine.hpp:244-252), 1 core."""
+    """The reference's own Simulation::step loop (oracle/_ref, g++ -O3 with the
+    reference's Release flags, 1 core) resumed from the GPU chain's start state
+    (engine.hpp:244-252) and timed on EXACTLY the moves the GPU timed: the
+    warm-up moves run untimed, then --steps x --moves-per-step timed. Returns the
+    baseline dict and the reference's final N (the same trajectory)."""
     import oracle as O
 
+    warm = a.warmup * a.moves_per_step
+    timed = a.cpu_steps * a.moves_per_step
     if os.path.exists(O.REF_SO):
         kind = "reference"
         cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
                            strategy=a.strategy)
         sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=rng_hex, step=0, energy=u0, virial=w0)
-        secs, _ = sim.run(a.cpu_moves)
+        sim.run(warm)
+        secs, _ = sim.run(timed)
+        n_after = int(sim.state().n)
     else:
         kind = "port"
         p = O.port_params(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
                           strategy=a.strategy)
         sim = O.PortSim(p, xyz, O.rng_from_hex(rng_hex), energy=u0, virial=w0)
+        sim.run(warm)
         t0 = time.perf_counter()
-        sim.run(a.cpu_moves)
+        sim.run(timed)
         secs = time.perf_counter() - t0
-    return {"value": a.cpu_moves / secs, "unit": "moves/s", "cores": 1, "kind": kind,
-            "sample": f"{a.cpu_moves} Simulation::step() moves of the same 1M workload from the "
-                      f"same start state (resume ctor), {secs:.2f} s, host {os.cpu_count()} cores, "
-                      "1 used"}
+        n_after = None
+    return ({"value": timed / secs, "unit": "moves/s", "cores": 1, "kind": kind,
+             "sample": f"moves {warm}..{warm + timed} of the same chain (the {a.cpu_steps} steps "
+                       f"after the {a.warmup} warm-up steps the GPU ran), reference "
+                       f"Simulation::step loop resumed from the same start state, {secs:.2f} s, "
+                       f"host {os.cpu_count()} cores, 1 used"}, n_after)
 
 
 def run_reference(a, rank, world):
@@ -169,7 +181,7 @@ def run_reference(a, rank, world):
     # U/W only matter for reported observables, not for the trajectory; the
     # resume ctor avoids the O(N^2) total energy (hours at 1M on one core).
     sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=hexs, step=0, energy=0.0, virial=0.0)
-    per_step = max(1000, a.cpu_moves // 5)
+    per_step = a.moves_per_step  # the same steps as the GPU arm
     for _ in range(a.warmup):
         sim.run(per_step)
     secs = 0.0
@@ -184,8 +196,9 @@ def run_reference(a, rank, world):
             "config": config_dict(a, 1), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "moves/s", "cores": 1,
                              "kind": "reference" if os.path.exists(O.REF_SO) else "port",
-                             "sample": f"{per_step} moves per step, reference Simulation::step loop "
-                                       "(oracle/_ref, g++ -O3, proj/CMakeLists Release flags)"},
+                             "sample": f"{a.warmup} untimed + {a.steps} timed steps of {per_step} moves, "
+                                       "reference Simulation::step loop (oracle/_ref, g++ -O3, "
+                                       "proj/CMakeLists Release flags), same start state as the GPU arm"},
             "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -220,10 +233,12 @@ def main():
     u0, w0 = st0.energy, st0.virial
 
     # CPU baseline from the identical start state (rank 0, N=1 only)
-    cpu = None
+    cpu, cpu_n = None, None
+    if not a.cpu_steps:
+        a.cpu_steps = a.steps
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(xyz, rng.serialize_hex(), u0, w0, a, box)
+            cpu, cpu_n = cpu_baseline(xyz, rng.serialize_hex(), u0, w0, a, box)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -241,6 +256,7 @@ def main():
     dev_ms = eng_ms = 0.0
     rounds = 0
     acc0 = sum(sim.dev.get_state().accepted)
+    moves0 = sim.dev.get_state().step
     with ClockSampler(local) as clk:
         for _ in range(a.steps):
             sim.run(a.moves_per_step)
@@ -250,6 +266,7 @@ def main():
             rounds += r.rounds
     barrier()
     acc1 = sum(sim.dev.get_state().accepted)
+    n_timed_end = sim.dev.get_state().n
     # ---- end-to-end through the C ABI (run + checkpoint read-back of state,
     #      RNG and positions to host memory), wall clock
     barrier()
@@ -309,6 +326,10 @@ def main():
         }
         if cpu and cpu.get("value"):
             line["speedup_vs_cpu_e2e"] = e2e / cpu["value"]
+            line["speedup_vs_cpu_device"] = value / cpu["value"]
+        if cpu_n is not None and a.cpu_steps == a.steps:
+            # the CPU reference ran the identical moves: same N afterwards
+            line["cpu_gpu_same_trajectory"] = bool(cpu_n == n_timed_end)
         print(json.dumps(line), flush=True)
     sim.close()
     if pg:

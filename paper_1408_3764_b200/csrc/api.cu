@@ -2,6 +2,7 @@
 // plumbing only: argument checks with the reference's error wording, device
 // allocation, staging copies, and dispatch to the kernels in grid.cu,
 // delta.cu, energy.cu, gen.cu and engine.cu.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -82,6 +83,28 @@ gcmc_status pull_state(Chain& c) {
      "state");
   CK(cudaStreamSynchronize(c.stream), "state");
   return GCMC_OK;
+}
+
+// Mark the hot arena persisting in L2 for kernels on the chain's stream
+// (best effort: devices without persisting L2 keep the default policy).
+void set_l2_policy(Chain& c) {
+  if (std::getenv("GCMC_NO_L2_POLICY")) return;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess) return;
+  if (prop.persistingL2CacheMaxSize <= 0 || prop.accessPolicyMaxWindowSize <= 0) return;
+  const size_t setaside = (size_t)prop.persistingL2CacheMaxSize;
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = c.arena;
+  v.accessPolicyWindow.num_bytes = std::min(c.arena_bytes, (size_t)prop.accessPolicyMaxWindowSize);
+  v.accessPolicyWindow.hitRatio = 1.0f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(c.stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess)
+    cudaGetLastError();
 }
 
 gcmc_status ensure_batch(Chain& c, uint64_t n) {
@@ -196,7 +219,8 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     m.inv = (double)d / P.box_length;
     // records per brick: generous over the densest LJ states (rho <= ~1.2)
     const double vb = m.side * m.side * m.side / (P.sigma * P.sigma * P.sigma);
-    int cap = (int)std::ceil(vb * 2.0) + 16;
+    // (~2.4x the mean occupancy at rho = 1: 32 at the r_cut = 2.5 sigma bricks)
+    int cap = (int)std::ceil(vb * 1.6);
     if (cap < 32) cap = 32;
     if (cap > 128) cap = 128;
     m.cap = cap;
@@ -212,7 +236,24 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   for (auto& ev : c->ev) CK(cudaEventCreate(&ev), "event");
   CK(cudaEventCreateWithFlags(&c->ev_mt, cudaEventDisableTiming), "event");
   CK(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming), "event");
-  CK(cudaMalloc(&c->pos, capn * sizeof(double4)), "alloc pos");
+  // Hot arena (every trial move reads it): mirror record planes, brick
+  // occupancy and the particle store, contiguous so one L2 access-policy
+  // window can mark it persisting (set_l2_policy).
+  {
+    Mirror& m = c->mirror;
+    const size_t nrec = (size_t)m.nb * m.cap;
+    const size_t plane = (nrec * sizeof(double) + 255) & ~size_t(255);
+    const size_t occb = ((size_t)m.nb * sizeof(int32_t) + 255) & ~size_t(255);
+    const size_t posb = capn * sizeof(double4);
+    c->arena_bytes = 3 * plane + occb + posb;
+    CK(cudaMalloc(&c->arena, c->arena_bytes), "alloc arena");
+    char* p = static_cast<char*>(c->arena);
+    m.rx = reinterpret_cast<double*>(p);
+    m.ry = reinterpret_cast<double*>(p + plane);
+    m.rz = reinterpret_cast<double*>(p + 2 * plane);
+    m.occ = reinterpret_cast<int32_t*>(p + 3 * plane);
+    c->pos = reinterpret_cast<double4*>(p + 3 * plane + occb);
+  }
   CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
   CK(cudaMalloc(&c->rslot, capn * sizeof(int32_t)), "alloc rslot");
   CK(cudaMalloc(&c->bslot, capn * sizeof(int32_t)), "alloc bslot");
@@ -225,12 +266,9 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   {
     Mirror& m = c->mirror;
     const size_t nrec = (size_t)m.nb * m.cap;
-    CK(cudaMalloc(&m.rx, nrec * sizeof(double)), "alloc mirror");
-    CK(cudaMalloc(&m.ry, nrec * sizeof(double)), "alloc mirror");
-    CK(cudaMalloc(&m.rz, nrec * sizeof(double)), "alloc mirror");
     CK(cudaMalloc(&m.rid, nrec * sizeof(int32_t)), "alloc mirror");
-    CK(cudaMalloc(&m.occ, (size_t)m.nb * sizeof(int32_t)), "alloc mirror");
     CK(cudaMemset(m.occ, 0, (size_t)m.nb * sizeof(int32_t)), "memset");
+    set_l2_policy(*c);
     size_t bd, br, be;
     engine_buffer_bytes(engine_max_slots(), &bd, &br, &be);
     CK(cudaMalloc(&c->eng_dec, bd), "alloc engine");
@@ -254,7 +292,7 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   cudaStreamSynchronize(c->gen_stream);
-  cudaFree(c->pos);
+  cudaFree(c->arena);
   cudaFree(c->props_next);
   cudaFree(c->mt_next);
   cudaEventDestroy(c->ev_mt);
@@ -263,11 +301,7 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   cudaFree(c->grid.slots);
   cudaFree(c->rslot);
   cudaFree(c->bslot);
-  cudaFree(c->mirror.rx);
-  cudaFree(c->mirror.ry);
-  cudaFree(c->mirror.rz);
   cudaFree(c->mirror.rid);
-  cudaFree(c->mirror.occ);
   cudaFree(c->eng_dec);
   cudaFree(c->eng_res);
   cudaFree(c->eng_ext);

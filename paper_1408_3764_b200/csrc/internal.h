@@ -16,7 +16,9 @@ struct Chain {
   Box box{};
   Grid grid{};
   Mirror mirror{};               // evaluation mirror (bricks >= r_cut)
-  double4* pos = nullptr;        // [capn]
+  double4* pos = nullptr;        // [capn] (inside the hot arena)
+  void* arena = nullptr;         // mirror planes + brick occupancy + store (L2-persisting)
+  size_t arena_bytes = 0;
   int32_t* rslot = nullptr;      // [capn] slot of particle i in its reference cell
   int32_t* bslot = nullptr;      // [capn] record index of particle i in the mirror
   uint64_t capn = 0;

@@ -1,0 +1,12 @@
+#!/bin/bash
+# bench + ncu launch list + one full ncu capture of k_engine; TAG arg
+TAG=${1:-b}
+O=gpurun_out/$TAG
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
+timeout 900 python bench.py > $O/bench.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/ncu_launch_bench.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_engine -s 2 -c 1 -o $O/engine_full python bench.py --steps 1 --warmup 1 --moves-per-step 65536 --no-cpu-baseline > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_energy -c 1 -o $O/energy_full python bench.py --steps 1 --warmup 1 --moves-per-step 65536 --no-cpu-baseline > $O/ncu_energy.log 2>&1
+echo done
