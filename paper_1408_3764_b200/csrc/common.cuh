@@ -300,4 +300,41 @@ __device__ __forceinline__ double warp_sum_comp(Kahan k) {
   return __dadd_rn(s, e);
 }
 
+
+// Warp-cooperative ascending sort of a short list of distinct ids in place
+// (the reference keeps each cell's ids ascending after build, grid_common.hpp
+// :11-21): lanes hold up to 64 ids, each computes its rank by comparison and
+// scatters; longer lists fall back to one lane's insertion sort. Returns the
+// sorted id for slot `lane` and `lane + 32` via out0/out1 (unused if >= m).
+__device__ __forceinline__ void warp_rank_sort(int32_t* a, int m, int lane) {
+  if (m <= 1) return;
+  if (m > 64) {
+    if (lane == 0)
+      for (int i = 1; i < m; ++i) {
+        const int32_t v = a[i];
+        int j = i - 1;
+        while (j >= 0 && a[j] > v) {
+          a[j + 1] = a[j];
+          --j;
+        }
+        a[j + 1] = v;
+      }
+    __syncwarp();
+    return;
+  }
+  const int32_t v0 = lane < m ? a[lane] : 0x7fffffff;
+  const int32_t v1 = lane + 32 < m ? a[lane + 32] : 0x7fffffff;
+  int r0 = 0, r1 = 0;
+  for (int k = 0; k < 32; ++k) {
+    const int32_t w0 = __shfl_sync(0xffffffffu, v0, k);
+    const int32_t w1 = __shfl_sync(0xffffffffu, v1, k);
+    r0 += (w0 < v0) + (w1 < v0);
+    r1 += (w0 < v1) + (w1 < v1);
+  }
+  __syncwarp();
+  if (lane < m) a[r0] = v0;
+  if (lane + 32 < m) a[r1] = v1;
+  __syncwarp();
+}
+
 }  // namespace gcmcb

@@ -12,6 +12,7 @@
 // reference's single ascending chain: agreement ~1e-14 relative).
 #include <cub/device/device_scan.cuh>
 
+#include <cmath>
 #include <sstream>
 
 #include "internal.h"
@@ -49,50 +50,63 @@ __global__ void k_escatter(uint64_t n, const int* cid, const int* start, int* fi
   ids[start[c] + atomicAdd(fill + c, 1)] = (int)i;
 }
 
+// One warp per cell: ids ascending (deterministic pair order), then the
+// double and float records.
 __global__ void k_esort(uint64_t ncells, const int* start, const int* count, int* ids,
-                        const double4* __restrict__ pos, double4* rec) {
-  const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+                        const double4* __restrict__ pos, double4* rec, float4* recf) {
+  const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (c >= ncells) return;
   int* a = ids + start[c];
   const int m = count[c];
-  for (int i = 1; i < m; ++i) {
-    const int v = a[i];
-    int j = i - 1;
-    while (j >= 0 && a[j] > v) {
-      a[j + 1] = a[j];
-      --j;
-    }
-    a[j + 1] = v;
-  }
-  for (int i = 0; i < m; ++i) {
+  warp_rank_sort(a, m, lane);
+  for (int i = lane; i < m; i += 32) {
     const double4 p = pos[a[i]];
     rec[start[c] + i] = make_double4(p.x, p.y, p.z, pid_bits((uint64_t)a[i]));
+    recf[start[c] + i] = make_float4((float)p.x, (float)p.y, (float)p.z, 0.0f);
   }
 }
 
 constexpr int kEWarps = 4;
 constexpr int kOwnMax = 64;
+constexpr int kECand = 512;
 
+struct Prefilter {
+  float l, inv_l, cut2;  // float box, 1/L and the conservative r^2 bound
+  int on;
+};
+
+// One warp per cell c: pairs (i in c, j in the half shell of c) — c itself
+// (i < j by id) and its 13 forward neighbours — so every pair is visited
+// once. An FP32 minimum image with a conservative bound rejects the ~85% of
+// candidates beyond r_cut; survivors get the reference's exact FP64
+// minimum image and LJ pair (common.cuh), Kahan per lane and a compensated
+// warp tree. Overlap (r^2 < 1e-12 sigma^2) is reported like total_energy's
+// runtime_error (engine.hpp:74-94).
 __global__ void __launch_bounds__(kEWarps * 32)
-    k_energy(EGrid eg, Box b, const int* __restrict__ start, const int* __restrict__ count,
-             const double4* __restrict__ rec, double* part_u, double* part_w,
+    k_energy(EGrid eg, Box b, Prefilter pf, const int* __restrict__ start,
+             const int* __restrict__ count, const double4* __restrict__ rec,
+             const float4* __restrict__ recf, double* part_u, double* part_w,
              unsigned long long* overlap) {
   __shared__ double4 own_s[kEWarps][kOwnMax];
-  __shared__ int pre_s[kEWarps][28];
-  __shared__ int cell_s[kEWarps][27];
+  __shared__ float4 ownf_s[kEWarps][kOwnMax];
+  __shared__ int cand_s[kEWarps][kECand];
+  __shared__ int queue_s[kEWarps][64];  // (record << 6 | own index) of pairs that passed the prefilter
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t c = blockIdx.x * (uint64_t)kEWarps + warp;
   if (c >= eg.ncells) return;
   const int d = eg.dims;
   const int cx = (int)(c % d), cy = (int)((c / d) % d), cz = (int)(c / ((uint64_t)d * d));
-  // 27-cube (distinct for d >= 3, compute_cell_dims guarantees it)
-  int ncnt = 0;
-  if (lane < 27) {
-    const int ox = lane % 3 - 1, oy = (lane / 3) % 3 - 1, oz = lane / 9 - 1;
+  // half shell: offsets 0..13 of the 27-cube in x-fastest order starting at
+  // (0,0,0): {self} + the 13 cells after it in lexicographic (z, y, x) order
+  int ncnt = 0, nstart = 0;
+  if (lane < 14) {
+    const int t = 13 + lane;  // cube index: (ox, oy, oz) = (t % 3, t / 3 % 3, t / 9) - 1
+    const int ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
     const int nx = (cx + ox + d) % d, ny = (cy + oy + d) % d, nz = (cz + oz + d) % d;
     const int nc = nx + d * (ny + d * nz);
-    cell_s[warp][lane] = nc;
     ncnt = count[nc];
+    nstart = start[nc];
   }
   int incl = ncnt;
 #pragma unroll
@@ -100,37 +114,90 @@ __global__ void __launch_bounds__(kEWarps * 32)
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (lane < 27) pre_s[warp][lane + 1] = incl;
-  if (lane == 0) pre_s[warp][0] = 0;
-  const int total = __shfl_sync(0xffffffffu, incl, 26);
-  const int own_start = start[c], own_n = count[c];
-  __syncwarp();
+  const int total = __shfl_sync(0xffffffffu, incl, 13);
+  const int own_start = __shfl_sync(0xffffffffu, nstart, 0);
+  const int own_n = __shfl_sync(0xffffffffu, ncnt, 0);
   Kahan ku = {0, 0}, kw = {0, 0};
   for (int ob = 0; ob < own_n; ob += kOwnMax) {
     const int on = min(kOwnMax, own_n - ob);
-    for (int i = lane; i < on; i += 32) own_s[warp][i] = rec[own_start + ob + i];
-    __syncwarp();
-    for (int t = lane; t < total; t += 32) {
-      int k = 0;
-      while (pre_s[warp][k + 1] <= t) ++k;
-      const int nc = cell_s[warp][k];
-      const double4 q = rec[start[nc] + (t - pre_s[warp][k])];
-      const long long jid = bits_pid(q.w);
-      for (int i = 0; i < on; ++i) {
-        const double4 p = own_s[warp][i];
-        const long long iid = bits_pid(p.w);
-        if (jid <= iid) continue;
-        const double r2 = min_image_dist2(p.x, p.y, p.z, q.x, q.y, q.z, b);
-        if (r2 > b.rc2) continue;
-        if (r2 < __dmul_rn(1e-12, b.sigma2)) {
-          atomicMin(overlap, ((unsigned long long)iid << 32) | (unsigned long long)jid);
-          continue;
+    for (int i = lane; i < on; i += 32) {
+      own_s[warp][i] = rec[own_start + ob + i];
+      ownf_s[warp][i] = recf[own_start + ob + i];
+    }
+    for (int cb = 0; cb < total; cb += kECand) {
+      // expansion of the candidate list (record indices), chunked
+      __syncwarp();
+      {
+        const int e0 = incl - ncnt;
+        for (int k = 0; k < ncnt; ++k) {
+          const int f = e0 + k - cb;
+          if (f >= 0 && f < kECand) cand_s[warp][f] = nstart + k;
         }
-        double u, w;
-        lj_pair_clamped(r2, b, u, w);
-        ku.add(u);
-        kw.add(w);
       }
+      __syncwarp();
+      const int ctot = min(kECand, total - cb);
+      // prefilter every (own i, candidate t) pair; pairs that may lie inside
+      // r_cut are queued and evaluated exactly 32 at a time (full warps)
+      int qn = 0;
+      auto drain = [&](int m) {
+        if (lane < m) {
+          const int pk = queue_s[warp][lane];
+          const double4 p = own_s[warp][pk & 63];
+          const double4 q = rec[(unsigned)pk >> 6];
+          const double r2 = min_image_dist2(p.x, p.y, p.z, q.x, q.y, q.z, b);
+          if (r2 <= b.rc2) {
+            if (r2 < __dmul_rn(1e-12, b.sigma2)) {
+              long long iid = bits_pid(p.w), jid = bits_pid(q.w);
+              if (iid > jid) {
+                const long long t2 = iid;
+                iid = jid;
+                jid = t2;
+              }
+              atomicMin(overlap, ((unsigned long long)iid << 32) | (unsigned long long)jid);
+            } else {
+              double u, w;
+              lj_pair_clamped(r2, b, u, w);
+              ku.add(u);
+              kw.add(w);
+            }
+          }
+        }
+      };
+      for (int t0 = 0; t0 < ctot; t0 += 32) {
+        const int t = t0 + lane;
+        const bool have = t < ctot;
+        const int qi = have ? cand_s[warp][t] : 0;
+        const float4 qf = have ? recf[qi] : make_float4(0, 0, 0, 0);
+        const bool self = have && cb + t < own_n;
+        for (int i = 0; i < on; ++i) {
+          bool pass = have && !(self && ob + i >= cb + t);  // i < j within the cell
+          if (pass && pf.on) {
+            const float4 pff = ownf_s[warp][i];
+            float dx = pff.x - qf.x, dy = pff.y - qf.y, dz = pff.z - qf.z;
+            dx -= pf.l * rintf(dx * pf.inv_l);
+            dy -= pf.l * rintf(dy * pf.inv_l);
+            dz -= pf.l * rintf(dz * pf.inv_l);
+            pass = dx * dx + dy * dy + dz * dz <= pf.cut2;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, pass);
+          if (m) {
+            const int pos = qn + __popc(m & ((1u << lane) - 1u));
+            if (pass) queue_s[warp][pos] = (qi << 6) | i;
+            qn += __popc(m);
+            __syncwarp();
+            if (qn >= 32) {
+              drain(32);
+              qn -= 32;
+              const int carry = queue_s[warp][32 + lane];
+              __syncwarp();
+              if (lane < qn) queue_s[warp][lane] = carry;
+              __syncwarp();
+            }
+          }
+        }
+      }
+      __syncwarp();
+      drain(qn);
     }
     __syncwarp();
   }
@@ -190,8 +257,8 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, (int)nc);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t need = al(n * 4) * 2 + al(nc * 4) * 3 + al(n * 32) + al(nc * 8) * 2 + al(64) +
-                      al(scan_bytes);
+  const size_t need = al(n * 4) * 2 + al(nc * 4) * 3 + al(n * 32) + al(n * 16) + al(nc * 8) * 2 +
+                      al(64) + al(scan_bytes);
   cudaError_t e;
   if (need > c.egrid_bytes) {
     if (c.egrid) cudaFree(c.egrid);
@@ -211,6 +278,7 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   int* start = (int*)take(nc * 4);
   int* fill = (int*)take(nc * 4);
   double4* rec = (double4*)take(n * 32);
+  float4* recf = (float4*)take(n * 16);
   double* pu = (double*)take(nc * 8);
   double* pw = (double*)take(nc * 8);
   char* small = take(64);
@@ -224,9 +292,23 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   k_ecount<<<blocks(n, 256), 256, 0, s>>>(eg, c.pos, n, cid, count);
   cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, count, start, (int)nc, s);
   k_escatter<<<blocks(n, 256), 256, 0, s>>>(n, cid, start, fill, ids);
-  k_esort<<<blocks(nc, 128), 128, 0, s>>>(nc, start, count, ids, c.pos, rec);
-  k_energy<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, start, count, rec, pu, pw,
-                                                         overlap);
+  k_esort<<<blocks(nc * 32, 256), 256, 0, s>>>(nc, start, count, ids, c.pos, rec, recf);
+  // FP32 prefilter: the bound adds 2 sqrt(3) r_cut delta + 3 delta^2 (plus
+  // float rounding of the sum) to r_cut^2. Off when the minimum-image choice
+  // itself could differ between FP32 and FP64 (L close to 2 r_cut).
+  Prefilter pf;
+  {
+    // per-axis error of the FP32 minimum image: inputs, difference, and the
+    // L * rint product each contribute at most L 2^-24 -> delta = 3 * (3 L 2^-24)
+    const double delta = 9.0 * l * std::ldexp(1.0, -24);
+    const double cut2 = c.box.rc2 + 2.0 * rc * std::sqrt(3.0) * delta + 3.0 * delta * delta;
+    pf.l = (float)l;
+    pf.inv_l = (float)(1.0 / l);
+    pf.cut2 = (float)(cut2 * (1.0 + 1e-5) + 1e-6);
+    pf.on = l > 2.0 * rc + 0.5 ? 1 : 0;
+  }
+  k_energy<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
+                                                         pu, pw, overlap);
   k_ereduce<<<1, 1024, 0, s>>>(nc, pu, pw, out);
   double h[2];
   unsigned long long ov = 0;

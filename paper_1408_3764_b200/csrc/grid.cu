@@ -76,21 +76,14 @@ __global__ void k_mbin(Mirror m, const double4* __restrict__ pos, uint64_t n, in
 }
 
 __global__ void k_msort(Mirror m, const double4* __restrict__ pos, int32_t* bslot) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t b = (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (b >= m.nb) return;
   int occ = m.occ[b];
   if (occ > m.cap) occ = m.cap;
   int32_t* ids = m.rid + (size_t)b * m.cap;
-  for (int i = 1; i < occ; ++i) {
-    const int32_t v = ids[i];
-    int j = i - 1;
-    while (j >= 0 && ids[j] > v) {
-      ids[j + 1] = ids[j];
-      --j;
-    }
-    ids[j + 1] = v;
-  }
-  for (int k = 0; k < occ; ++k) {
+  warp_rank_sort(ids, occ, lane);
+  for (int k = lane; k < occ; k += 32) {
     const size_t s = (size_t)b * m.cap + k;
     const double4 p = pos[ids[k]];
     m.rx[s] = p.x;
@@ -248,7 +241,7 @@ gcmc_status mirror_build(Chain& c) {
   if ((e = cudaMemsetAsync(m.occ, 0, (size_t)m.nb * sizeof(int32_t), s))) return cuda_error(e, "mirror");
   if ((e = cudaMemsetAsync(flag, 0, sizeof(int), s))) return cuda_error(e, "mirror");
   if (n) k_mbin<<<blocks(n, 256), 256, 0, s>>>(m, c.pos, n, c.bslot, flag);
-  k_msort<<<blocks(m.nb, 256), 256, 0, s>>>(m, c.pos, c.bslot);
+  k_msort<<<blocks((uint64_t)m.nb * 32, 256), 256, 0, s>>>(m, c.pos, c.bslot);
   int overflow = 0;
   if ((e = cudaMemcpyAsync(&overflow, flag, sizeof(int), cudaMemcpyDeviceToHost, s))) return cuda_error(e, "mirror");
   if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "mirror");
