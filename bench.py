@@ -37,7 +37,7 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 ALG_BYTES_PER_MOVE = 6.5e3
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -54,7 +54,34 @@ def parse_args():
     ap.add_argument("--cpu-steps", type=int, default=0,
                     help="timed steps of the CPU baseline (0 = --steps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE configs[4]: mu isotherm sweep, one 64k chain per GPU "
+                         "(rank g runs mu = -3 + g, seed 1 + g)")
+    a = ap.parse_args(argv)
+    if a.sweep:
+        if a.n0 == 1 << 20:
+            a.n0 = 1 << 16
+    return a
+
+
+def state_point(a, rank):
+    """(mu, seed) of this rank's chain: replicas of the same state point, or
+    the isotherm sweep mu_g = -3 + g. No collective is needed
+    on the hot path: chains are independent."""
+    if a.sweep:
+        return -3.0 + rank, 1 + rank
+    return a.mu, 1 + rank
+
+
+def reduce_max(pg, values, device):
+    """Max over ranks of the timed quantities (the only collective)."""
+    if pg is None:
+        return values
+    import torch
+
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
 
 
 def dist_env():
@@ -122,9 +149,16 @@ def hbm_peak():
 
 
 def config_dict(a, world):
-    return {"workload": f"LJ fluid GCMC ~1M particles on 1 B200 (BASELINE configs[3])"
-                        if a.n0 == 1 << 20 else f"LJ fluid GCMC N0={a.n0}",
-            "n0": a.n0, "density": a.density, "temperature": a.temperature, "mu": a.mu,
+    if a.sweep:
+        wl = (f"mu/T isotherm sweep of {a.n0}-particle GCMC chains, 1 chain per GPU "
+              f"(BASELINE configs[4]); rank g: mu = -3 + g")
+    elif a.n0 == 1 << 20:
+        wl = "LJ fluid GCMC ~1M particles on 1 B200 (BASELINE configs[3])"
+    else:
+        wl = f"LJ fluid GCMC N0={a.n0}"
+    return {"workload": wl,
+            "n0": a.n0, "density": a.density, "temperature": a.temperature,
+            "mu": [-3.0 + g for g in range(world)] if a.sweep else a.mu,
             "r_cut": 2.5, "strategy": a.strategy, "move_mix": "30/35/35",
             "moves_per_step": a.moves_per_step, "chains": world,
             "start": "random sequential insertion, 0.85 sigma (init_config.hpp:19-64)",
@@ -225,9 +259,10 @@ def main():
     from paper_1408_3764_b200.config import RunConfig
 
     box = (a.n0 / a.density) ** (1.0 / 3.0)
-    xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, 1 + rank)
-    cfg = RunConfig(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
-                    strategy=a.strategy, seed=1 + rank)
+    mu, seed = state_point(a, rank)
+    xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed)
+    cfg = RunConfig(temperature=a.temperature, chemical_potential=mu, box_length=box,
+                    strategy=a.strategy, seed=seed)
     sim = E.Simulation(cfg, xyz, rng, device=local)
     st0 = sim.dev.get_state()
     u0, w0 = st0.energy, st0.virial
@@ -281,10 +316,7 @@ def main():
 
     moves_rank = a.moves_per_step * a.steps
     t_dev = dev_ms / 1e3
-    if pg:
-        t = torch.tensor([t_dev, e2e_s], dtype=torch.float64, device="cuda")
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        t_dev, e2e_s = float(t[0]), float(t[1])
+    t_dev, e2e_s = reduce_max(pg, [t_dev, e2e_s], "cuda")
     value = moves_rank * world / t_dev
     e2e = moves_rank * world / e2e_s
     peak, peak_kind = hbm_peak()
