@@ -256,7 +256,6 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   }
   CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
   CK(cudaMalloc(&c->rslot, capn * sizeof(int32_t)), "alloc rslot");
-  CK(cudaMalloc(&c->bslot, capn * sizeof(int32_t)), "alloc bslot");
   if (g.ncells) {
     CK(cudaMalloc(&g.occ, g.ncells * sizeof(int32_t)), "alloc occ");
     CK(cudaMalloc(&g.slots, g.ncells * g.cap * sizeof(int32_t)), "alloc slots");
@@ -300,7 +299,6 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   cudaFree(c->grid.occ);
   cudaFree(c->grid.slots);
   cudaFree(c->rslot);
-  cudaFree(c->bslot);
   cudaFree(c->mirror.rid);
   cudaFree(c->eng_dec);
   cudaFree(c->eng_res);
@@ -660,9 +658,10 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
       const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "close_publish", "walk_masks", "walk_iter"};
       std::fprintf(stderr, "[engine prof] rounds %llu sequencer:", hp[15]);
       for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.0f", sn[k], hp[k] / R);
-      const char* en[] = {"idle", "poll_D", "assign", "setup", "sums", "publish", "tail"};
+      const char* en[] = {"idle", "poll_D", "assign", "setup_sync", "sums", "publish", "tail",
+                          "s_prop", "s_neww", "s_load", "s_oldw", "s_finish"};
       std::fprintf(stderr, "\n[engine prof] evaluator(cta1,g0):");
-      for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %s=%.0f", en[k], hp[16 + k] / R);
+      for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %s=%.0f", en[k], hp[16 + k] / R);
       std::fprintf(stderr, "\n[engine prof] helpers: work=%.0f idle=%.0f (cycles/round)\n", hp[32] / R,
                    hp[33] / R);
       std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",

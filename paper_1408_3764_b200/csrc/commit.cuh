@@ -26,9 +26,8 @@
 namespace gcmcb {
 
 struct Store {
-  double4* pos;
+  double4* pos;    // (x, y, z, mirror back-pointer in the low word of w)
   int32_t* rslot;
-  int32_t* bslot;
 };
 
 struct MoveData {
@@ -45,7 +44,7 @@ __device__ __forceinline__ void load_move(const Store& s, int kind, uint64_t pid
     d.oy = o.y;
     d.oz = o.z;
     d.rslot_pid = __ldcg(s.rslot + pid);
-    d.bslot_pid = __ldcg(s.bslot + pid);
+    d.bslot_pid = bslot_in(o);
   }
 }
 
@@ -53,6 +52,7 @@ __device__ __forceinline__ void load_move(const Store& s, int kind, uint64_t pid
 struct CommitIn {
   double qx, qy, qz;
   int32_t rslot_q, bslot_q;
+  int32_t rslot_pid;  // slot of the mover in its reference cell (loaded here)
   int ca, cb, cl, occ_ca, occ_cb;
   int ba, bb, occ_ba, occ_bb, la;
   int32_t last_ca, last_bid;
@@ -71,13 +71,14 @@ __device__ __forceinline__ void commit_load(const Grid& g, const Mirror& m, cons
   // ---- hop 1: cells, occupancies, the last particle
   c.qx = c.qy = c.qz = 0.0;
   c.rslot_q = c.bslot_q = -1;
+  c.rslot_pid = (kind != 1 && grid) ? __ldcg(s.rslot + pid) : -1;
   if (c.relabel) {
     const double4 o = ld_cg(s.pos + q);
     c.qx = o.x;
     c.qy = o.y;
     c.qz = o.z;
     c.rslot_q = __ldcg(s.rslot + q);
-    c.bslot_q = __ldcg(s.bslot + q);
+    c.bslot_q = bslot_in(o);
   }
   c.ca = c.cb = c.cl = -1;
   c.occ_ca = c.occ_cb = 0;
@@ -128,12 +129,12 @@ __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, cons
   e1 = e2 = e3 = 0;
   int status = GCMC_OK;
   // ---- store (particles.hpp:28-41)
-  if (kind == 0) st_cg(s.pos + pid, make_double4(d.nx, d.ny, d.nz, 0.0));
-  if (kind == 1) st_cg(s.pos + n, make_double4(d.nx, d.ny, d.nz, 0.0));
+  if (kind == 0) st_xyz(s.pos + pid, d.nx, d.ny, d.nz);
+  if (kind == 1) st_xyz(s.pos + n, d.nx, d.ny, d.nz);
   // ---- reference layout
   if (grid) {
     if (c.ref_move) {  // remove_id: the last id fills the hole
-      const int k = d.rslot_pid, last = c.occ_ca - 1;
+      const int k = c.rslot_pid, last = c.occ_ca - 1;
       if (k != last) {
         __stcg(g.slots + slot_index(g, c.ca, k), c.last_ca);
         if (!(c.relabel && c.last_ca == (int32_t)q)) __stcg(s.rslot + c.last_ca, k);
@@ -154,7 +155,7 @@ __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, cons
       }
     }
     if (c.relabel) {  // relabel_id(last -> pid)
-      const int rq = c.last_ca == (int32_t)q ? d.rslot_pid : c.rslot_q;
+      const int rq = c.last_ca == (int32_t)q ? c.rslot_pid : c.rslot_q;
       __stcg(g.slots + slot_index(g, c.cl, rq), (int32_t)pid);
       __stcg(s.rslot + pid, rq);
     }
@@ -172,7 +173,7 @@ __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, cons
         __stcg(m.ry + k, c.ly);
         __stcg(m.rz + k, c.lz);
         __stcg(m.rid + k, c.last_bid);
-        if (!(c.relabel && c.last_bid == (int32_t)q)) __stcg(s.bslot + c.last_bid, k);
+        if (!(c.relabel && c.last_bid == (int32_t)q)) __stcg(bslot_of(s.pos, c.last_bid), k);
       }
       __stcg(m.occ + c.ba, c.occ_ba - 1);
     }
@@ -191,15 +192,15 @@ __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, cons
         __stcg(m.ry + k, d.ny);
         __stcg(m.rz + k, d.nz);
         __stcg(m.rid + k, id);
-        __stcg(s.bslot + id, k);
+        __stcg(bslot_of(s.pos, id), k);
         __stcg(m.occ + c.bb, c.occ_bb + 1);
       }
     }
     if (c.relabel) {
       const int bq = c.last_bid == (int32_t)q ? d.bslot_pid : c.bslot_q;
       __stcg(m.rid + bq, (int32_t)pid);
-      __stcg(s.bslot + pid, bq);
-      st_cg(s.pos + pid, make_double4(c.qx, c.qy, c.qz, 0.0));
+      __stcg(bslot_of(s.pos, pid), bq);
+      st_xyz(s.pos + pid, c.qx, c.qy, c.qz);
     }
   }
   return status;

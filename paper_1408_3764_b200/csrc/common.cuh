@@ -262,6 +262,24 @@ __device__ __forceinline__ void st_cg(double4* p, double4 v) {
   __stcg(reinterpret_cast<double2*>(p) + 1, make_double2(v.z, v.w));
 }
 
+// The mirror back-pointer of particle i (record index brick*cap+k, mirror.cuh)
+// lives in the otherwise unused 4th word of its store record, so the mover's
+// position and its record index arrive in one 32-byte sector.
+__device__ __forceinline__ int32_t* bslot_of(double4* pos, uint64_t i) {
+  return reinterpret_cast<int32_t*>(pos + i) + 6;
+}
+__device__ __forceinline__ const int32_t* bslot_of(const double4* pos, uint64_t i) {
+  return reinterpret_cast<const int32_t*>(pos + i) + 6;
+}
+__device__ __forceinline__ int32_t bslot_in(const double4& r) {
+  return (int32_t)(uint32_t)__double_as_longlong(r.w);
+}
+// Position only: keeps the back-pointer word.
+__device__ __forceinline__ void st_xyz(double4* p, double x, double y, double z) {
+  __stcg(reinterpret_cast<double2*>(p), make_double2(x, y));
+  __stcg(reinterpret_cast<double*>(p) + 2, z);
+}
+
 __device__ __forceinline__ double pid_bits(uint64_t pid) {
   return __longlong_as_double((long long)pid);
 }

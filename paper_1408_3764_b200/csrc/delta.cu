@@ -14,7 +14,7 @@ constexpr int kT = 256;
 
 __global__ void __launch_bounds__(kT)
     k_delta_batch(Mirror m, Box b, const double4* __restrict__ pos,
-                  const int32_t* __restrict__ bslot, uint64_t n, bool all_pairs, uint64_t count,
+                  uint64_t n, bool all_pairs, uint64_t count,
                   const int32_t* __restrict__ kinds, const uint64_t* __restrict__ pids,
                   const double* __restrict__ xyz, double* du, double* dw) {
   __shared__ WinWs<kT> ws;
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kT)
       if (kind != 1) {
         const uint64_t pid = pids[q];
         const double4 o = ld_cg(pos + pid);
-        ws.excl = __ldcg(bslot + pid);
+        ws.excl = bslot_in(o);
         const int e = kind == 0 ? 1 : 0;
         ws.nwin = kind == 0 ? 2 : 1;
         ws.cx[e] = o.x;
@@ -65,7 +65,7 @@ gcmc_status delta_batch(Chain& c, uint64_t count, const int32_t* kinds_d, const 
                         const double* xyz_d, double* du_d, double* dw_d) {
   if (!count) return GCMC_OK;
   k_delta_batch<<<(unsigned)count, kT, 0, c.stream>>>(
-      c.mirror, c.box, c.pos, c.bslot, c.st_host->n, c.grid.kind == GCMC_ALL_PAIRS, count, kinds_d,
+      c.mirror, c.box, c.pos, c.st_host->n, c.grid.kind == GCMC_ALL_PAIRS, count, kinds_d,
       pids_d, xyz_d, du_d, dw_d);
   cudaError_t e = cudaGetLastError();
   if (e) return cuda_error(e, "delta");

@@ -487,8 +487,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           q = (uint64_t)nv - 1;
           if (lane == 0) {  // the mover's position and back-pointers: one L2 hop, in flight
             o = ld_cg(a.s.pos + pid);
-            rsl = __ldcg(a.s.rslot + pid);
-            bsl = __ldcg(a.s.bslot + pid);
+            rsl = -1;  // the commit loads the reference slot itself
+            bsl = bslot_in(o);
           }
         }
         // the new-position window does not need the mover (unless max_displacement)
@@ -1286,7 +1286,7 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
   a.g = c.grid;
   a.m = c.mirror;
   a.b = c.box;
-  a.s = Store{c.pos, c.rslot, c.bslot};
+  a.s = Store{c.pos, c.rslot};
   a.st = c.st;
   a.props = c.props;
   a.trace = trace_d;

@@ -62,7 +62,7 @@ __global__ void k_sort_cells(Grid g, int32_t* rslot, ChainState* st) {
 // Mirror build: bin by brick (atomic slot), then per brick sort the ids
 // ascending (deterministic record order) and write the record planes and
 // the back-pointers.
-__global__ void k_mbin(Mirror m, const double4* __restrict__ pos, uint64_t n, int32_t* bslot,
+__global__ void k_mbin(Mirror m, const double4* __restrict__ pos, uint64_t n,
                        int* overflow) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -75,7 +75,7 @@ __global__ void k_mbin(Mirror m, const double4* __restrict__ pos, uint64_t n, in
     atomicMax(overflow, (int)b + 1);
 }
 
-__global__ void k_msort(Mirror m, const double4* __restrict__ pos, int32_t* bslot) {
+__global__ void k_msort(Mirror m, double4* pos) {
   const uint32_t b = (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= m.nb) return;
@@ -89,7 +89,7 @@ __global__ void k_msort(Mirror m, const double4* __restrict__ pos, int32_t* bslo
     m.rx[s] = p.x;
     m.ry[s] = p.y;
     m.rz[s] = p.z;
-    bslot[ids[k]] = (int32_t)s;
+    *bslot_of(pos, ids[k]) = (int32_t)s;
   }
 }
 
@@ -174,13 +174,13 @@ __global__ void k_check_cells(Grid g, const double4* __restrict__ pos, uint64_t 
 // Mirror + back-pointers against the store (engine-internal consistency;
 // reported by rebuild_check as a stale coordinate mirror).
 __global__ void k_check_mirror(Grid g, Mirror m, const double4* __restrict__ pos,
-                               const int32_t* rslot, const int32_t* bslot, uint64_t n,
+                               const int32_t* rslot, uint64_t n,
                                unsigned long long* first) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double4 p = pos[i];
   bool bad = false;
-  const int32_t bs = bslot[i];
+  const int32_t bs = bslot_in(p);
   const uint32_t b = mbrick(m, mpoint(m, p.x, p.y, p.z));
   if (bs < 0 || (uint32_t)(bs / m.cap) != b || bs % m.cap >= m.occ[b] || m.rid[bs] != (int32_t)i ||
       m.rx[bs] != p.x || m.ry[bs] != p.y || m.rz[bs] != p.z)
@@ -240,8 +240,8 @@ gcmc_status mirror_build(Chain& c) {
   Mirror& m = c.mirror;
   if ((e = cudaMemsetAsync(m.occ, 0, (size_t)m.nb * sizeof(int32_t), s))) return cuda_error(e, "mirror");
   if ((e = cudaMemsetAsync(flag, 0, sizeof(int), s))) return cuda_error(e, "mirror");
-  if (n) k_mbin<<<blocks(n, 256), 256, 0, s>>>(m, c.pos, n, c.bslot, flag);
-  k_msort<<<blocks((uint64_t)m.nb * 32, 256), 256, 0, s>>>(m, c.pos, c.bslot);
+  if (n) k_mbin<<<blocks(n, 256), 256, 0, s>>>(m, c.pos, n, flag);
+  k_msort<<<blocks((uint64_t)m.nb * 32, 256), 256, 0, s>>>(m, c.pos);
   int overflow = 0;
   if ((e = cudaMemcpyAsync(&overflow, flag, sizeof(int), cudaMemcpyDeviceToHost, s))) return cuda_error(e, "mirror");
   if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "mirror");
@@ -325,7 +325,7 @@ gcmc_status grid_check(Chain& c, std::string* issue) {
   }
   unsigned long long* mfirst = reinterpret_cast<unsigned long long*>(c.iscratch);
   cudaMemsetAsync(mfirst, 0xff, sizeof(unsigned long long), s);
-  if (n) k_check_mirror<<<blocks(n, 256), 256, 0, s>>>(c.grid, c.mirror, c.pos, c.rslot, c.bslot, n, mfirst);
+  if (n) k_check_mirror<<<blocks(n, 256), 256, 0, s>>>(c.grid, c.mirror, c.pos, c.rslot, n, mfirst);
   unsigned long long mf = 0;
   cudaMemcpyAsync(&mf, mfirst, sizeof mf, cudaMemcpyDeviceToHost, s);
   unsigned long long f = 0;
@@ -368,7 +368,7 @@ gcmc_status commit_one(Chain& c, int kind, uint64_t pid, const double* p, uint64
   const uint64_t n = c.st_host->n;
   CommitArgs a{kind, pid, n, p ? p[0] : 0.0, p ? p[1] : 0.0, p ? p[2] : 0.0};
   long long* out = reinterpret_cast<long long*>(c.dscratch);
-  k_commit_one<<<1, 1, 0, c.stream>>>(c.grid, c.mirror, Store{c.pos, c.rslot, c.bslot}, c.st, a,
+  k_commit_one<<<1, 1, 0, c.stream>>>(c.grid, c.mirror, Store{c.pos, c.rslot}, c.st, a,
                                       out);
   long long h[4];
   cudaError_t e = cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, c.stream);

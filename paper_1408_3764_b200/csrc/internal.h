@@ -20,7 +20,6 @@ struct Chain {
   void* arena = nullptr;         // mirror planes + brick occupancy + store (L2-persisting)
   size_t arena_bytes = 0;
   int32_t* rslot = nullptr;      // [capn] slot of particle i in its reference cell
-  int32_t* bslot = nullptr;      // [capn] record index of particle i in the mirror
   uint64_t capn = 0;
   ChainState* st = nullptr;      // device
   ChainState* st_host = nullptr; // pinned mirror
