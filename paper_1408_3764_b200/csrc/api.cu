@@ -205,7 +205,7 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     const int max_ctas = 1 + engine_max_slots() / mg;
     if (c->engine_ctas > max_ctas) c->engine_ctas = max_ctas;
   }
-  c->engine_variants = P.engine_variants > 0 ? (P.engine_variants > 31 ? 31 : P.engine_variants) : 9;
+  c->engine_variants = P.engine_variants > 0 ? (P.engine_variants > 15 ? 15 : P.engine_variants) : 11;
   c->engine_bias = P.engine_bias > 0 ? 1 : -1;
   // Evaluation mirror: bricks of side L/dims >= r_cut (1e-9 relative margin).
   {

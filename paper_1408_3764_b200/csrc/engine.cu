@@ -175,9 +175,36 @@ __device__ __forceinline__ int var_of(int d, int bias) {
 // derive it from the prefix Q[k] = sum_{m<k} need(B0 + m) over the proposal
 // ring, so an evaluator can place its slot for any base B = B0 + len with one
 // binary search (no assignment step after the decision arrives).
+// Candidate N of a displacement / deletion at window position i: nvar
+// consecutive values centred on the expected drift (just npub for i = 0,
+// whose N is exact).
+__device__ __forceinline__ void n_window(int64_t npub, int rate, int i, int nvar, int64_t& nlo,
+                                         int& cnt) {
+  if (i == 0) {
+    nlo = npub;
+    cnt = 1;
+  } else {
+    nlo = npub + var_centre(rate, i) - (nvar - 1) / 2;
+    cnt = nvar;
+  }
+}
+// The particle a proposal picks depends on N only through
+// pid = index_from(pick, N); over nvar consecutive N it takes at most
+// floor(pick (nvar - 1)) + 2 distinct values, one evaluation slot each.
+__device__ __forceinline__ int pid_slots(double pick, int nvar) {
+  return (int)__dmul_rn(pick, (double)(nvar - 1)) + 2;
+}
+// First particle of the window (lowest N >= 1), or -1 if every N <= 0.
+__device__ __forceinline__ int64_t pid_lo(double pick, int64_t nlo, int cnt) {
+  const int64_t n1 = nlo < 1 ? 1 : nlo;
+  if (n1 > nlo + cnt - 1) return -1;
+  return (int64_t)index_from(pick, (uint64_t)n1);
+}
+
 __device__ __forceinline__ int need_of(const EngineArgs& a, const Proposal* ring, uint64_t mv) {
   if (mv >= a.nmoves) return 1 << 16;
-  return ring[mv % kRing].kind == 1 ? 1 : a.nvar;
+  const Proposal& p = ring[mv % kRing];
+  return p.kind == 1 ? 1 : pid_slots(p.pick, a.nvar);
 }
 
 // One warp: Q[0..kPre) over moves B0, B0+1, ...
@@ -242,6 +269,19 @@ __device__ __forceinline__ bool slot_move(const int* Q, int len, int s, int fit,
   i = lo - len;
   v = target - Q[lo];
   return Q[lo + 1] > target;  // inside move lo (the last move may be partial -> beyond used)
+}
+
+// Slot of move i resolved at N offset dd (sequencer; fs = first slot of i).
+__device__ __forceinline__ int resolved_slot(const EngineArgs& a, const Proposal& pr, int i, int fs,
+                                             int64_t npub, int rate, int dd) {
+  if (pr.kind == 1) return fs;
+  int64_t nlo;
+  int cnt;
+  n_window(npub, rate, i, a.nvar, nlo, cnt);
+  const int64_t nn = npub + dd;
+  if (nn <= 0) return fs;
+  const int64_t plo = pid_lo(pr.pick, nlo, cnt);
+  return fs + (int)((int64_t)index_from(pr.pick, (uint64_t)nn) - plo);
 }
 
 // ----------------------------------------------------------------- conflicts
@@ -364,6 +404,8 @@ struct EvalShared {
   WinWs<T> ws[kThreads / T];
   struct G {
     int i, v, kind, empty, cf;
+    uint32_t cov;    // candidate N (window-relative bits) this slot decides
+    long long nlo;   // lowest candidate N
     uint64_t pid, q, nv;
     MoveData md;
     double acc;
@@ -469,9 +511,28 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         int empty = 0;
         int64_t nv = (int64_t)d.n;
         uint64_t pid = 0, q = 0;
+        uint32_t cov = 0;  // candidate N (window-relative bits) this slot decides
+        int64_t nlo = 0;
         if (kind != 1) {
-          nv += var_centre(d.rate, G.i) + var_off(G.v, d.bias);
-          empty = nv <= 0;
+          int cnt;
+          n_window((int64_t)d.n, d.rate, G.i, a.nvar, nlo, cnt);
+          const int64_t plo = pid_lo(pr.pick, nlo, cnt);
+          const int64_t p = plo + G.v;
+          bool real = false;
+          if (lane < cnt) {
+            const int64_t nl = nlo + lane;
+            bool c = false;
+            if (nl <= 0) c = G.v == 0;  // empty store: counted rejection (engine.hpp:355, 399)
+            else if (plo >= 0 && (int64_t)index_from(pr.pick, (uint64_t)nl) == p) {
+              c = true;
+              real = true;
+            }
+            cov = c ? 1u : 0u;
+          }
+          cov = __ballot_sync(0xffffffffu, cov != 0);
+          const bool any_real = __any_sync(0xffffffffu, real);
+          empty = !any_real;   // nothing to evaluate (rejection-only or no coverage)
+          nv = any_real ? p + 1 : 0;  // any N that maps to p (only for the loads below)
         }
         MoveData md;
         md.nx = pr.x;
@@ -483,8 +544,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         int rsl = -1, bsl = -1;
         const bool loads = kind != 1 && !empty;
         if (loads) {
-          pid = index_from(pr.pick, (uint64_t)nv);
-          q = (uint64_t)nv - 1;
+          pid = (uint64_t)(nv - 1);  // the slot's particle p (nv = p + 1 above)
+          q = 0;
           if (lane == 0) {  // the mover's position and back-pointers: one L2 hop, in flight
             o = ld_cg(a.s.pos + pid);
             rsl = -1;  // the commit loads the reference slot itself
@@ -529,6 +590,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         if (lane == 0) {
           G.kind = kind;
           G.empty = empty;
+          G.cov = cov;
+          G.nlo = nlo;
           G.pid = pid;
           G.q = q;
           G.nv = (uint64_t)(nv < 0 ? 0 : nv);
@@ -615,12 +678,24 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           bits = __ballot_sync(0xffffffffu, ok);
         } else if (kind == 0) {
           pe = displacement_acceptance(du, a.beta);
-          bits = G.acc < pe ? 1u : 0u;
+          bits = G.acc < pe ? G.cov : 0u;  // N-independent
+          for (int l = 0; l < 32; ++l)       // rejection-only bits (N <= 0) never accept
+            if (((G.cov >> l) & 1u) && G.nlo + l <= 0) bits &= ~(1u << l);
         } else {
           rdu = -du;
           rdw = -dw;
-          pe = deletion_acceptance(rdu, G.nv, a.vol, a.beta, a.mu, a.lambda3);
-          bits = G.acc < pe ? 1u : 0u;
+          // deletion_acceptance with each candidate N mapping to this particle
+          const int64_t nl = G.nlo + lane;
+          bool ok = false;
+          double pl = 0.0;
+          if (((G.cov >> lane) & 1u) && nl > 0) {
+            pl = deletion_acceptance(rdu, (uint64_t)nl, a.vol, a.beta, a.mu, a.lambda3);
+            ok = G.acc < pl;
+          }
+          bits = __ballot_sync(0xffffffffu, ok);
+          // the trace reports p for the N the walk resolves; publish the one at
+          // the lowest covered N (recomputed by the trace writer otherwise)
+          pe = __shfl_sync(0xffffffffu, pl, __ffs(G.cov & 0x7fffffffu) ? __ffs(G.cov) - 1 : 0);
         }
         // overflow of the commit (occupancies read this round; exact unless cf)
         bool ovf = false;
@@ -641,7 +716,10 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
                                (G.empty ? kFEmpty : 0u);
         if (lane < kResWords) {
           uint64_t p;
-          if (lane == 0) p = (uint64_t)flags | ((uint64_t)bits << 8);
+          if (lane == 0)
+            p = kind == 1 ? (uint64_t)flags | ((uint64_t)bits << 8)
+                          : (uint64_t)flags | ((uint64_t)(bits & 0xffffu) << 8) |
+                                ((uint64_t)(G.cov & 0xffffu) << 24);
           else if (lane == 1) p = (rs.pt[0] & kNoPoint) | ((rs.pt[1] & kNoPoint) << 24);
           else
             p = (uint64_t)(rs.ia < 0 ? 0xffffffffu : (uint32_t)rs.ia) | ((uint64_t)G.i << 32) |
@@ -915,7 +993,9 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
       double p = ex->pe;
       if (kind == 1)
         p = metropolis(__dmul_rn(__ddiv_rn(a.vol, __dmul_rn(a.lambda3, (double)(nm + 1))), ex->pe));
-      if (D.empty[i]) p = 0.0;
+      if (kind == 2 && (int64_t)nm > 0)
+        p = deletion_acceptance(ex->du, nm, a.vol, a.beta, a.mu, a.lambda3);
+      if (D.empty[i] || (kind != 1 && (int64_t)nm <= 0)) p = 0.0;
       t.acceptance_prob = p;
       t.n_after = (uint64_t)((int64_t)D.n + dn);
       a.trace[D.base + i] = t;
@@ -992,14 +1072,22 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           sh.mcov[i] = cf ? 0u : 0xffffffffu;
           sh.mcf[i] = cf ? 0xffffffffu : 0u;
           sh.mov[i] = (w0 & kFOverflow) ? 0xffffffffu : 0u;
-        } else {  // variant v evaluated d = centre(i) + off(v)
-          const int j = var_centre(rate, i) + var_off(v, bias) + kInsSpan / 2;
-          if (j >= 0 && j < kInsSpan) {
-            const uint32_t b = 1u << j;
-            if (bits & 1u) atomicOr(&sh.macc[i], b);
-            if (w0 & kFConflict) atomicOr(&sh.mcf[i], b);
-            else atomicOr(&sh.mcov[i], b);
-            if (w0 & kFOverflow) atomicOr(&sh.mov[i], b);
+        } else {  // a particle's slot: bits over its candidate N window
+          int64_t nlo;
+          int cnt;
+          n_window((int64_t)n, rate, i, a.nvar, nlo, cnt);
+          const int j0 = (int)(nlo - (int64_t)n) + kInsSpan / 2;
+          const uint32_t acc16 = bits & 0xffffu, cov16 = (bits >> 16) & 0xffffu;
+          auto place = [&](uint32_t m) -> uint32_t {
+            if (j0 >= 32 || j0 <= -32) return 0u;
+            return j0 >= 0 ? (m << j0) : (m >> -j0);
+          };
+          const uint32_t cw = place(cov16), aw = place(acc16);
+          if (aw) atomicOr(&sh.macc[i], aw);
+          if (cw) {
+            if (w0 & kFConflict) atomicOr(&sh.mcf[i], cw);
+            else atomicOr(&sh.mcov[i], cw);
+            if (w0 & kFOverflow) atomicOr(&sh.mov[i], cw);
           }
         }
       }
@@ -1097,7 +1185,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             const int k = sh.mkind[i];
             const int dd = di[h];
             const int fs = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
-            sh.res_s[i] = fs + (k == 1 ? 0 : var_of(dd - var_centre(rate, i), bias));
+            sh.res_s[i] = resolved_slot(a, sh.ring[(base + i) % kRing], i, fs, (int64_t)n, rate, dd);
+            (void)k;
             sh.res_d[i] = dd;
           }
         }
@@ -1106,14 +1195,16 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           const int k = sh.mkind[i];
           const int fs = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
           sh.acc_i[lane] = i;
-          sh.acc_s[lane] = fs + (k == 1 ? 0 : var_of(acc_dd - var_centre(rate, i), bias));
+          sh.acc_s[lane] = resolved_slot(a, sh.ring[(base + i) % kRing], i, fs, (int64_t)n, rate, acc_dd);
+          (void)k;
           sh.acc_d[lane] = (int)((int64_t)n + acc_dd);  // store size before move i
         }
         if (err) {  // the overflowing move's slot
           const int i = len;
           const int k = sh.mkind[i];
           const int fs = i == 0 ? 0 : 1 + sh.Q[i] - sh.Q[1];
-          if (lane == 0) sh.err_slot = fs + (k == 1 ? 0 : var_of(d - var_centre(rate, i), bias));
+          if (lane == 0) sh.err_slot = resolved_slot(a, sh.ring[(base + i) % kRing], i, fs, (int64_t)n, rate, d);
+          (void)k;
         }
         if (lane == 0) {
           sh.len = len;
