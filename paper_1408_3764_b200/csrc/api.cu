@@ -192,6 +192,10 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     capn = (uint64_t)(vol * 1.5) + 1024;
     if (g.kind != GCMC_ALL_PAIRS) capn = std::min<uint64_t>(capn, (uint64_t)g.cap * g.ncells + 1);
   }
+  if (capn >= (1ull << 31)) {  // particle ids are int32 in the grids and the engine's words
+    delete c;
+    return set_error(GCMC_ARG, "store capacity must be < 2^31 particles");
+  }
   c->capn = capn;
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device), "props");
