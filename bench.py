@@ -48,11 +48,12 @@ def parse_args(argv=None):
     ap.add_argument("--mu", type=float, default=1.0)
     ap.add_argument("--temperature", type=float, default=2.0)
     ap.add_argument("--strategy", default="microcell")
-    ap.add_argument("--moves-per-step", type=int, default=1 << 18)
+    ap.add_argument("--moves-per-step", type=int, default=1 << 22)
     ap.add_argument("--cpu-moves", type=int, default=100000,
                     help="(--impl reference) unused; kept for compatibility")
-    ap.add_argument("--cpu-steps", type=int, default=0,
-                    help="timed steps of the CPU baseline (0 = --steps)")
+    ap.add_argument("--cpu-steps", type=int, default=1,
+                    help="timed steps of the CPU baseline (the first timed GPU steps; "
+                         "bounded to ~20 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE configs[4]: mu isotherm sweep, one 64k chain per GPU "
@@ -167,22 +168,22 @@ def config_dict(a, world):
             "parallelism": f"replicas x{world} (independent chains, seed 1+rank)"}
 
 
-def cpu_baseline(xyz, rng_hex, u0, w0, a, box):
+def cpu_baseline(snap, a, box):
     """The reference's own Simulation::step loop (oracle/_ref, g++ -O3 with the
-    reference's Release flags, 1 core) resumed from the GPU chain's start state
-    (engine.hpp:244-252) and timed on EXACTLY the moves the GPU timed: the
-    warm-up moves run untimed, then --steps x --moves-per-step timed. Returns the
-    baseline dict and the reference's final N (the same trajectory)."""
+    reference's Release flags, 1 core) resumed (engine.hpp:244-252) from the
+    GPU chain's state at the start of the timed steps (positions, RNG, step,
+    U, W) and timed on exactly the moves of the first --cpu-steps timed GPU
+    steps. Returns the baseline dict and the reference's N afterwards (the
+    same trajectory)."""
     import oracle as O
 
-    warm = a.warmup * a.moves_per_step
+    xyz, rng_hex, step, u0, w0 = snap
     timed = a.cpu_steps * a.moves_per_step
     if os.path.exists(O.REF_SO):
         kind = "reference"
         cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
                            strategy=a.strategy)
-        sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=rng_hex, step=0, energy=u0, virial=w0)
-        sim.run(warm)
+        sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=rng_hex, step=step, energy=u0, virial=w0)
         secs, _ = sim.run(timed)
         n_after = int(sim.state().n)
     else:
@@ -190,16 +191,15 @@ def cpu_baseline(xyz, rng_hex, u0, w0, a, box):
         p = O.port_params(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
                           strategy=a.strategy)
         sim = O.PortSim(p, xyz, O.rng_from_hex(rng_hex), energy=u0, virial=w0)
-        sim.run(warm)
         t0 = time.perf_counter()
         sim.run(timed)
         secs = time.perf_counter() - t0
         n_after = None
     return ({"value": timed / secs, "unit": "moves/s", "cores": 1, "kind": kind,
-             "sample": f"moves {warm}..{warm + timed} of the same chain (the {a.cpu_steps} steps "
-                       f"after the {a.warmup} warm-up steps the GPU ran), reference "
-                       f"Simulation::step loop resumed from the same start state, {secs:.2f} s, "
-                       f"host {os.cpu_count()} cores, 1 used"}, n_after)
+             "sample": f"moves {step}..{step + timed} of the same chain (the first "
+                       f"{a.cpu_steps} of the {a.steps} timed GPU steps), reference "
+                       f"Simulation::step loop resumed from the GPU chain's state there, "
+                       f"{secs:.2f} s, host {os.cpu_count()} cores, 1 used"}, n_after)
 
 
 def run_reference(a, rank, world):
@@ -215,9 +215,12 @@ def run_reference(a, rank, world):
     # U/W only matter for reported observables, not for the trajectory; the
     # resume ctor avoids the O(N^2) total energy (hours at 1M on one core).
     sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=hexs, step=0, energy=0.0, virial=0.0)
-    per_step = a.moves_per_step  # the same steps as the GPU arm
+    # warm-up: the same moves as the GPU arm's warm-up steps; then each timed
+    # step is a bounded sample of 2^20 consecutive moves of the same chain
+    # (the run stays within a few minutes on one core)
     for _ in range(a.warmup):
-        sim.run(per_step)
+        sim.run(a.moves_per_step)
+    per_step = min(a.moves_per_step, 1 << 20)
     secs = 0.0
     for _ in range(a.steps):
         s, _ = sim.run(per_step)
@@ -230,7 +233,8 @@ def run_reference(a, rank, world):
             "config": config_dict(a, 1), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "moves/s", "cores": 1,
                              "kind": "reference" if os.path.exists(O.REF_SO) else "port",
-                             "sample": f"{a.warmup} untimed + {a.steps} timed steps of {per_step} moves, "
+                             "sample": f"{a.warmup} warm-up steps of {a.moves_per_step} moves, then "
+                                       f"{a.steps} timed steps of {per_step} consecutive moves, "
                                        "reference Simulation::step loop (oracle/_ref, g++ -O3, "
                                        "proj/CMakeLists Release flags), same start state as the GPU arm"},
             "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0,
@@ -267,19 +271,22 @@ def main():
     st0 = sim.dev.get_state()
     u0, w0 = st0.energy, st0.virial
 
-    # CPU baseline from the identical start state (rank 0, N=1 only)
+    for _ in range(a.warmup):
+        sim.run(a.moves_per_step)
+
+    # CPU baseline: the reference resumed from this exact state (rank 0, N=1 only)
     cpu, cpu_n = None, None
-    if not a.cpu_steps:
+    if not a.cpu_steps or a.cpu_steps > a.steps:
         a.cpu_steps = a.steps
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            cpu, cpu_n = cpu_baseline(xyz, rng.serialize_hex(), u0, w0, a, box)
+            stw = sim.dev.get_state()
+            snap = (sim.dev.positions(), sim.dev.get_rng().serialize_hex(), stw.step, stw.energy,
+                    stw.virial)
+            cpu, cpu_n = cpu_baseline(snap, a, box)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}
-
-    for _ in range(a.warmup):
-        sim.run(a.moves_per_step)
 
     def barrier():
         torch.cuda.synchronize()
@@ -292,9 +299,11 @@ def main():
     rounds = 0
     acc0 = sum(sim.dev.get_state().accepted)
     moves0 = sim.dev.get_state().step
+    n_after_step = []
     with ClockSampler(local) as clk:
         for _ in range(a.steps):
             sim.run(a.moves_per_step)
+            n_after_step.append(sim.dev.get_state().n)
             r = sim.last_run
             dev_ms += r.device_ms + r.gen_ms
             eng_ms += r.device_ms
@@ -320,15 +329,17 @@ def main():
     value = moves_rank * world / t_dev
     e2e = moves_rank * world / e2e_s
     peak, peak_kind = hbm_peak()
-    eng_launch_s = eng_ms / 1e3 / a.steps  # one engine launch per step (<= 2^21 moves)
-    achieved = ALG_BYTES_PER_MOVE * a.moves_per_step / eng_launch_s / 1e9
+    launches = (a.moves_per_step + (1 << 21) - 1) >> 21  # engine launches per step
+    moves_per_launch = a.moves_per_step / launches
+    eng_launch_s = eng_ms / 1e3 / (a.steps * launches)
+    achieved = ALG_BYTES_PER_MOVE * moves_per_launch / eng_launch_s / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "engine_traffic.json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
                 tj = json.load(f)
-            traffic = tj.get("bytes_per_launch")
+            traffic = tj.get("bytes_per_move") * moves_per_launch  # ncu dram bytes, per launch
         except Exception:
             traffic = None
     n_final = sim.dev.get_state().n
@@ -343,13 +354,15 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
-                         "kernel": "k_engine (persistent cluster Metropolis loop)",
+                         "kernel": "k_engine (persistent whole-GPU Metropolis loop)",
                          "alg_bytes_per_move": ALG_BYTES_PER_MOVE,
                          "note": "serial Markov chain: latency-bound, not HBM-bound; see "
                                  "ns_per_round and DESIGN.md"},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": 2 * a.steps,
+            # per step: one engine launch + one look-ahead proposal generation
+            # per 2^21-move chunk (gcmc_run_moves)
+            "gpu_launches": 2 * a.steps * ((a.moves_per_step + (1 << 21) - 1) >> 21),
             "ns_per_move": 1e9 * t_dev / moves_rank,
             "ns_per_round": 1e9 * (eng_ms / 1e3) / max(rounds, 1),
             "moves_per_round": moves_rank / max(rounds, 1),
@@ -359,9 +372,9 @@ def main():
         if cpu and cpu.get("value"):
             line["speedup_vs_cpu_e2e"] = e2e / cpu["value"]
             line["speedup_vs_cpu_device"] = value / cpu["value"]
-        if cpu_n is not None and a.cpu_steps == a.steps:
+        if cpu_n is not None:
             # the CPU reference ran the identical moves: same N afterwards
-            line["cpu_gpu_same_trajectory"] = bool(cpu_n == n_timed_end)
+            line["cpu_gpu_same_trajectory"] = bool(cpu_n == n_after_step[a.cpu_steps - 1])
         print(json.dumps(line), flush=True)
     sim.close()
     if pg:

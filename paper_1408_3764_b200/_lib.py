@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(PKG, "libgcmc_b200.so")
+SO = os.environ.get("GCMC_LIB") or os.path.join(PKG, "libgcmc_b200.so")
 
 _d, _u64, _i32, _p = C.c_double, C.c_uint64, C.c_int32, C.c_void_p
 _dp = C.POINTER(C.c_double)

@@ -35,6 +35,9 @@
 // commits before the next-but-one round reads them.
 #include <cstdlib>
 
+#ifndef GCMC_KMAXMOVES
+#define GCMC_KMAXMOVES 64
+#endif
 #include "commit.cuh"
 #include "internal.h"
 #include "slot.cuh"
@@ -44,10 +47,10 @@ namespace gcmcb {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kMaxMoves = 64;    // moves per round
+constexpr int kMaxMoves = GCMC_KMAXMOVES;   // moves per round
 constexpr int kMH = kMaxMoves / 32;  // moves per walk lane
 constexpr int kMaxAcc = 32;      // accepted moves per round
-constexpr int kRing = 256;       // proposal ring (moves)
+constexpr int kRing = GCMC_KMAXMOVES * 4;       // proposal ring (moves)
 constexpr int kPre = 2 * kMaxMoves + 2;  // slot prefix entries
 constexpr int kDecHdr = 4;
 constexpr int kDecEnt = 2;
