@@ -503,11 +503,15 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     uint64_t* rw = a.res + (size_t)(r & 1) * kResWords * a.nslots + cta_slot0 + g;  // + j * nslots
     SlotExt* ex = a.ext + (size_t)(r & 1) * a.nslots + cta_slot0 + g;
     if (G.i >= 0) {
+      constexpr int kGW = T / 32;                 // warps per group
+      const int lw = g % (kGW < 4 ? kGW : 4);     // leader warp
+      const int lw2 = kGW > 1 ? (lw + 1) % kGW : lw;
       int ocb = 0;
       int setup_nent = 0, setup_nent0 = 0;
-      const int bar_pair = 1 + MG + g;  // warps 0 and 1 of the group
-      // ---- setup (warp 0 of the group)
-      if (gw == 0) {
+      const int bar_pair = 1 + MG + g;  // leader and second warp of the group
+      // ---- setup (the group's leader warp: warp g % 4 of group g, so the
+      // groups' serial chains run on different SM sub-partitions)
+      if (gw == lw) {
         const uint64_t mv = d.base + (uint64_t)G.i;
         const Proposal& pr = sh.ring[mv % kRing];
         const int kind = pr.kind;
@@ -621,7 +625,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         }
         group_sync(bar_pair, 64);  // G published to warp 1
         if (!all_pairs && !G.empty) win_finish<T>(a.m, ws, occ_s, setup_nent, setup_nent0, lane);
-      } else if (gw == 1) {
+      } else if (gw == lw2) {
         // read set and conflicts with the previous round's commits, in
         // parallel with warp 0's window finish
         group_sync(bar_pair, 64);
@@ -649,10 +653,10 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         else
           win_sums<T>(a.m, a.b, ws, gt, du, dw);
       }
-      group_reduce<T>(ws, du, dw, bar_id, gt);
+      group_reduce<T>(ws, du, dw, bar_id, gt, 32 * lw);
       pc.mark(4);  // sums + reduce
-      // ---- acceptance bits, conflicts, publish (warp 0)
-      if (gw == 0) {
+      // ---- acceptance bits, conflicts, publish (leader warp)
+      if (gw == lw) {
         const int kind = G.kind;
         const MoveData& md = G.md;
         RW rs;

@@ -203,11 +203,11 @@ __device__ __forceinline__ void win_sums(const Mirror& m, const Box& b, WinWs<T>
   if (lane < qn) lj_accum(b, ws.qr2[warp][lane], (double)ws.qs[warp][lane], du, dw);
 }
 
-// Group-wide deterministic reduction; result valid in thread gt == 0 after
-// the call (all T threads call).
+// Group-wide deterministic reduction; result valid in thread gt == leader_gt
+// after the call (all T threads call).
 template <int T>
 __device__ __forceinline__ void group_reduce(WinWs<T>& ws, double& du, double& dw, int bar_id,
-                                             int gt) {
+                                             int gt, int leader_gt = 0) {
   const int lane = threadIdx.x & 31, w = gt >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -220,7 +220,7 @@ __device__ __forceinline__ void group_reduce(WinWs<T>& ws, double& du, double& d
       ws.red[w][1] = dw;
     }
     group_sync(bar_id, T);
-    if (gt == 0) {
+    if (gt == leader_gt) {
       double a = 0.0, c = 0.0;
 #pragma unroll
       for (int i = 0; i < T / 32; ++i) {
