@@ -635,10 +635,10 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     }
     if (c.prof) CK(cudaMemsetAsync(c.prof, 0, 4096 * sizeof(unsigned long long), c.stream), "prof");
     const bool lat = std::getenv("GCMC_ENGINE_LATENCY") != nullptr;
-    if (lat && !c.stamp) CK(cudaMalloc(&c.stamp, 5 * 8192 * sizeof(unsigned long long)), "stamp");
+    if (lat && !c.stamp) CK(cudaMalloc(&c.stamp, 8 * 8192 * sizeof(unsigned long long)), "stamp");
     if (lat) {
-      std::vector<unsigned long long> init(5 * 8192, 0);
-      for (int k = 0; k < 8192; ++k) init[5 * k + 1] = ~0ull;
+      std::vector<unsigned long long> init(8 * 8192, 0);
+      for (int k = 0; k < 8192; ++k) init[8 * k + 1] = init[8 * k + 5] = ~0ull;
       CK(cudaMemcpyAsync(c.stamp, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c.stream), "stamp");
     }
     CK(cudaEventRecord(c.ev[1], c.stream), "event");
@@ -659,9 +659,9 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
       unsigned long long hp[64];
       cudaMemcpy(hp, c.prof, sizeof hp, cudaMemcpyDeviceToHost);
       const double R = (double)(hp[15] ? hp[15] : 1);
-      const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "close_publish", "walk_masks", "walk_iter"};
+      const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "next_shape", "walk_masks", "walk_iter", "close_to_publish"};
       std::fprintf(stderr, "[engine prof] rounds %llu sequencer:", hp[15]);
-      for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.0f", sn[k], hp[k] / R);
+      for (int k = 1; k < 9; ++k) std::fprintf(stderr, " %s=%.0f", sn[k], hp[k] / R);
       const char* en[] = {"idle", "poll_D", "assign", "setup_sync", "sums", "publish", "tail",
                           "s_prop", "s_neww", "s_load", "s_oldw", "s_finish"};
       std::fprintf(stderr, "\n[engine prof] evaluator(cta1,g0):");
@@ -671,22 +671,24 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
       std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",
                    hp[40], hp[41], hp[42], hp[43], hp[44], hp[45]);
       if (c.stamp) {
-        std::vector<unsigned long long> st(5 * 8192);
+        std::vector<unsigned long long> st(8 * 8192);
         cudaMemcpy(st.data(), c.stamp, st.size() * 8, cudaMemcpyDeviceToHost);
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
         int cnt = 0;
         for (int k = 2; k < 8192 && k < (int)hp[15]; ++k) {
-          const unsigned long long* e = &st[5 * k];
-          if (!e[0] || e[1] == ~0ull || !e[3] || !e[4]) continue;
+          const unsigned long long* e = &st[8 * k];
+          if (!e[0] || e[1] == ~0ull || !e[3] || !e[4] || !e[7]) continue;
           a0 += (double)(long long)(e[1] - e[0]);
           a1 += (double)(long long)(e[2] - e[0]);
           a2 += (double)(long long)(e[3] - e[0]);
           a3 += (double)(long long)(e[4] - e[3]);
+          a4 += (double)(long long)(e[5] - e[0]);
+          a5 += (double)e[6] / (double)e[7];
           ++cnt;
         }
         if (cnt)
-          std::fprintf(stderr, "[engine prof] latency ns (%d rounds): publish->first CTA sees D=%.0f publish->last CTA sees D=%.0f publish->last result=%.0f last result->sequencer has all=%.0f\n",
-                       cnt, a0 / cnt, a1 / cnt, a2 / cnt, a3 / cnt);
+          std::fprintf(stderr, "[engine prof] latency ns (%d rounds): publish->first CTA sees D=%.0f ->last CTA sees D=%.0f ->first result=%.0f ->mean result=%.0f ->last result=%.0f; last result->sequencer has all=%.0f\n",
+                       cnt, a0 / cnt, a1 / cnt, a4 / cnt, a5 / cnt, a2 / cnt, a3 / cnt);
       }
     }
     if (c.st_host->error) break;

@@ -87,9 +87,16 @@ struct Proposal {
   double pick;
   double acc;
   int32_t kind;
-  int32_t pad;
+  // State-independent data of the new position, filled by k_annotate (gen.cu)
+  // off the engine's critical path: the pruned 3x3x3 brick window as a 27-bit
+  // mask (kNoMask: not precomputed), the packed brick point and the
+  // reference-grid cell.
+  uint32_t wmask;
+  uint32_t bpt;
+  int32_t cell;
 };
-static_assert(sizeof(Proposal) == 48, "Proposal layout");
+static_assert(sizeof(Proposal) == 56, "Proposal layout");
+constexpr uint32_t kNoMask = 0xffffffffu;
 
 // ----------------------------------------------------------------- box.hpp
 // box.hpp:24-31. fmod is exact in CUDA as in glibc.

@@ -39,6 +39,7 @@
 #define GCMC_KMAXMOVES 64
 #endif
 #include "commit.cuh"
+#include <cstdio>
 #include "internal.h"
 #include "slot.cuh"
 
@@ -412,6 +413,8 @@ struct EvalShared {
     uint64_t pid, q, nv;
     MoveData md;
     double acc;
+    int pre, cell;   // new position precomputed (k_annotate): its brick point and grid cell
+    uint32_t bpt;
   } gs[kThreads / T];
 };
 
@@ -471,8 +474,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       pc.mark(1);  // D observed
       if (a.stamp && lane == 0) {
         const unsigned long long t = gtimer();
-        atomicMin(a.stamp + 5 * (r & 8191) + 1, t);  // first CTA sees D_r
-        atomicMax(a.stamp + 5 * (r & 8191) + 2, t);  // last CTA sees D_r
+        atomicMin(a.stamp + 8 * (r & 8191) + 1, t);  // first CTA sees D_r
+        atomicMax(a.stamp + 8 * (r & 8191) + 2, t);  // last CTA sees D_r
       }
       const Dec& d = sh.d;
       // replica: the previous round's commits (a--, b++)
@@ -541,57 +544,70 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           empty = !any_real;   // nothing to evaluate (rejection-only or no coverage)
           nv = any_real ? p + 1 : 0;  // any N that maps to p (only for the loads below)
         }
+        pc.mark(7);  // s_prop
         MoveData md;
         md.nx = pr.x;
         md.ny = pr.y;
         md.nz = pr.z;
         md.rslot_pid = md.bslot_pid = -1;
         md.ox = md.oy = md.oz = 0.0;
-        double4 o = make_double4(0, 0, 0, 0);
-        int rsl = -1, bsl = -1;
         const bool loads = kind != 1 && !empty;
-        if (loads) {
-          pid = (uint64_t)(nv - 1);  // the slot's particle p (nv = p + 1 above)
-          q = 0;
-          if (lane == 0) {  // the mover's position and back-pointers: one L2 hop, in flight
-            o = ld_cg(a.s.pos + pid);
-            rsl = -1;  // the commit loads the reference slot itself
-            bsl = bslot_in(o);
-          }
-        }
-        // the new-position window does not need the mover (unless max_displacement)
+        if (loads) pid = (uint64_t)(nv - 1);  // the slot's particle p (nv = p + 1 above)
+        q = 0;
+        // The mover's position and back-pointer: one L2 hop, issued by every
+        // lane (one broadcast transaction) and unconditionally (record 0 when
+        // unused), so that no register merge waits on it before the windows.
+        // (four 64-bit loads: a quad destination invites an early register
+        // move that waits on the load)
+        const double* op = reinterpret_cast<const double*>(a.s.pos + (loads ? pid : 0));
+        double4 o;
+        o.x = __ldcg(op);
+        o.y = __ldcg(op + 1);
+        o.z = __ldcg(op + 2);
+        o.w = __ldcg(op + 3);
+        // windows, one call site: [0] the new position before the mover load
+        // lands (it does not need the mover unless max_displacement), [1] the
+        // new position after it (max_displacement), [2] the old position
         const bool early = kind != 2 && !empty && !(kind == 0 && a.max_disp > 0.0) && !all_pairs;
+        const bool pre = early && pr.wmask != kNoMask;  // window precomputed (k_annotate)
+        if (lane == 0 && early)  // reference cell entered
+          ocb = __ldcg(a.g.occ + (pre ? pr.cell : cell_of(a.g, md.nx, md.ny, md.nz)));
         int nent = 0, nent0 = 0;
-        if (early) {
-          nent = win_add<T>(a.m, a.b, ws, 0, md.nx, md.ny, md.nz, lane);
-          nent0 = nent;
-        }
-        if (lane == 0 && !empty && kind != 2 && !all_pairs && early)  // reference cell entered
-          ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
-        if (loads) {
-          md.ox = __shfl_sync(0xffffffffu, o.x, 0);
-          md.oy = __shfl_sync(0xffffffffu, o.y, 0);
-          md.oz = __shfl_sync(0xffffffffu, o.z, 0);
-          md.rslot_pid = __shfl_sync(0xffffffffu, rsl, 0);
-          md.bslot_pid = __shfl_sync(0xffffffffu, bsl, 0);
-          if (kind == 0 && a.max_disp > 0.0) {  // engine.hpp:359-365
-            const double c = a.max_disp;
-            md.nx = wrap_axis(__dadd_rn(md.ox, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.x), 1.0), c)), a.b.l);
-            md.ny = wrap_axis(__dadd_rn(md.oy, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.y), 1.0), c)), a.b.l);
-            md.nz = wrap_axis(__dadd_rn(md.oz, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.z), 1.0), c)), a.b.l);
+#pragma unroll 1
+        for (int w = 0; w < 3; ++w) {
+          if (w == 1) {
+            pc.mark(8);  // s_neww
+            if (loads) {
+              md.ox = o.x;
+              md.oy = o.y;
+              md.oz = o.z;
+              md.rslot_pid = -1;  // the commit loads the reference slot itself
+              md.bslot_pid = bslot_in(o);
+              if (kind == 0 && a.max_disp > 0.0) {  // engine.hpp:359-365
+                const double c = a.max_disp;
+                md.nx = wrap_axis(__dadd_rn(md.ox, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.x), 1.0), c)), a.b.l);
+                md.ny = wrap_axis(__dadd_rn(md.oy, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.y), 1.0), c)), a.b.l);
+                md.nz = wrap_axis(__dadd_rn(md.oz, __dmul_rn(__dsub_rn(__dmul_rn(2.0, pr.z), 1.0), c)), a.b.l);
+                if (lane == 0 && !all_pairs) ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
+              }
+            }
+            pc.mark(9);  // s_load
+          }
+          const bool want = w == 0 ? early
+                          : (!all_pairs && !empty &&
+                             (w == 1 ? (kind == 0 && !early) : kind != 1));
+          if (want) {
+            if (w == 0 && pre) {
+              nent = window_bricks_mask(a.m, pr.wmask, pr.bpt, ws.brick, lane);
+            } else {
+              const double cx = w == 2 ? md.ox : md.nx, cy = w == 2 ? md.oy : md.ny,
+                           cz = w == 2 ? md.oz : md.nz;
+              nent = win_add<T>(a.m, a.b, ws, nent, cx, cy, cz, lane);
+            }
+            if (w < 2 || kind == 2) nent0 = nent;
           }
         }
-        if (!all_pairs && !empty) {
-          if (kind == 0 && !early) {  // max_displacement: new window now
-            nent = win_add<T>(a.m, a.b, ws, 0, md.nx, md.ny, md.nz, lane);
-            nent0 = nent;
-            if (lane == 0) ocb = __ldcg(a.g.occ + cell_of(a.g, md.nx, md.ny, md.nz));
-          }
-          if (kind != 1) {
-            nent = win_add<T>(a.m, a.b, ws, nent, md.ox, md.oy, md.oz, lane);
-            if (kind == 2) nent0 = nent;
-          }
-        }
+        pc.mark(10);  // s_oldw
         setup_nent = nent;
         setup_nent0 = nent0;
         if (lane == 0) {
@@ -604,6 +620,9 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           G.nv = (uint64_t)(nv < 0 ? 0 : nv);
           G.md = md;
           G.acc = pr.acc;
+          G.pre = pre;
+          G.bpt = pr.bpt;
+          G.cell = pr.cell;
           ws.excl = loads ? md.bslot_pid : -1;
           if (kind == 2) {
             ws.nwin = 1;
@@ -625,6 +644,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         }
         group_sync(bar_pair, 64);  // G published to warp 1
         if (!all_pairs && !G.empty) win_finish<T>(a.m, ws, occ_s, setup_nent, setup_nent0, lane);
+        pc.mark(11);  // s_finish
       } else if (gw == lw2) {
         // read set and conflicts with the previous round's commits, in
         // parallel with warp 0's window finish
@@ -633,7 +653,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         const MoveData& md = G.md;
         const bool loads = kind != 1 && !G.empty;
         RW rs;
-        rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
+        rs.pt[0] = kind != 2 ? (G.pre ? (uint64_t)G.bpt : mpoint(a.m, md.nx, md.ny, md.nz)) : kNoPoint;
         rs.pt[1] = loads ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
         rs.pt[2] = kNoPoint;
         rs.ia = loads ? (int64_t)G.pid : -1;
@@ -660,7 +680,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         const int kind = G.kind;
         const MoveData& md = G.md;
         RW rs;
-        rs.pt[0] = kind != 2 ? mpoint(a.m, md.nx, md.ny, md.nz) : kNoPoint;
+        rs.pt[0] = kind != 2 ? (G.pre ? (uint64_t)G.bpt : mpoint(a.m, md.nx, md.ny, md.nz)) : kNoPoint;
         rs.pt[1] = kind != 1 && !G.empty ? mpoint(a.m, md.ox, md.oy, md.oz) : kNoPoint;
         rs.pt[2] = kNoPoint;
         rs.ia = kind != 1 && !G.empty ? (int64_t)G.pid : -1;
@@ -673,36 +693,48 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         double rdu = du, rdw = dw;
         if (G.empty) {
           rdu = rdw = 0.0;
-        } else if (kind == 1) {
-          pe = exp(__dmul_rn(a.beta, __dsub_rn(a.mu, du)));  // engine.hpp:49
-          const int64_t nj = (int64_t)d.n + lane - kInsSpan / 2;
-          bool ok = false;
-          if (nj >= 0) {
-            const double p = metropolis(__dmul_rn(
-                __ddiv_rn(a.vol, __dmul_rn(a.lambda3, (double)(nj + 1))), pe));
-            ok = G.acc < p;
-          }
-          bits = __ballot_sync(0xffffffffu, ok);
-        } else if (kind == 0) {
-          pe = displacement_acceptance(du, a.beta);
-          bits = G.acc < pe ? G.cov : 0u;  // N-independent
-          for (int l = 0; l < 32; ++l)       // rejection-only bits (N <= 0) never accept
-            if (((G.cov >> l) & 1u) && G.nlo + l <= 0) bits &= ~(1u << l);
         } else {
-          rdu = -du;
-          rdw = -dw;
-          // deletion_acceptance with each candidate N mapping to this particle
-          const int64_t nl = G.nlo + lane;
-          bool ok = false;
-          double pl = 0.0;
-          if (((G.cov >> lane) & 1u) && nl > 0) {
-            pl = deletion_acceptance(rdu, (uint64_t)nl, a.vol, a.beta, a.mu, a.lambda3);
-            ok = G.acc < pl;
+          if (kind == 2) {
+            rdu = -du;
+            rdw = -dw;
           }
-          bits = __ballot_sync(0xffffffffu, ok);
-          // the trace reports p for the N the walk resolves; publish the one at
-          // the lowest covered N (recomputed by the trace writer otherwise)
-          pe = __shfl_sync(0xffffffffu, pl, __ffs(G.cov & 0x7fffffffu) ? __ffs(G.cov) - 1 : 0);
+          // the one exponential of each kind (engine.hpp:28-59, same operation order)
+          const double x = kind == 1 ? __dmul_rn(a.beta, __dsub_rn(a.mu, du))
+                         : (kind == 0 ? __dmul_rn(-a.beta, du)
+                                      : __dmul_rn(-a.beta, __dadd_rn(a.mu, rdu)));
+          const double ex = exp(x);
+          if (kind == 1) {
+            pe = ex;
+            const int64_t nj = (int64_t)d.n + lane - kInsSpan / 2;
+            bool ok = false;
+            if (nj >= 0) {
+              const double p = metropolis(__dmul_rn(
+                  __ddiv_rn(a.vol, __dmul_rn(a.lambda3, (double)(nj + 1))), ex));
+              ok = G.acc < p;
+            }
+            bits = __ballot_sync(0xffffffffu, ok);
+          } else if (kind == 0) {
+            pe = metropolis(ex);
+            bits = G.acc < pe ? G.cov : 0u;  // N-independent
+            // rejection-only bits (N <= 0) never accept: offsets l <= -nlo
+            if (G.nlo <= 0) {
+              const int64_t k = 1 - G.nlo;  // bits 0..k-1
+              bits &= k >= 32 ? 0u : ~((1u << k) - 1u);
+            }
+          } else {
+            // deletion_acceptance with each candidate N mapping to this particle
+            const int64_t nl = G.nlo + lane;
+            bool ok = false;
+            double pl = 0.0;
+            if (((G.cov >> lane) & 1u) && nl > 0) {
+              pl = metropolis(__dmul_rn(__ddiv_rn(__dmul_rn(a.lambda3, (double)nl), a.vol), ex));
+              ok = G.acc < pl;
+            }
+            bits = __ballot_sync(0xffffffffu, ok);
+            // the trace reports p for the N the walk resolves; publish the one at
+            // the lowest covered N (recomputed by the trace writer otherwise)
+            pe = __shfl_sync(0xffffffffu, pl, __ffs(G.cov & 0x7fffffffu) ? __ffs(G.cov) - 1 : 0);
+          }
         }
         // overflow of the commit (occupancies read this round; exact unless cf)
         bool ovf = false;
@@ -713,7 +745,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           ob = occ_s ? (int)occ_s[bb] : __ldcg(a.m.occ + bb);
           if (!same_b && ob >= a.m.cap) ovf = true;
           if (!all_pairs) {
-            cb = cell_of(a.g, md.nx, md.ny, md.nz);
+            cb = G.pre ? G.cell : cell_of(a.g, md.nx, md.ny, md.nz);
             const bool same_c = kind == 0 && cb == cell_of(a.g, md.ox, md.oy, md.oz);
             if (!same_c && ocb >= a.g.cap) ovf = true;
           }
@@ -733,7 +765,14 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
                 ((uint64_t)G.v << 39);
           st_relaxed(rw + (size_t)lane * a.nslots, tagw(r, p));
         }
-        if (a.stamp && lane == 0) atomicMax(a.stamp + 5 * (r & 8191) + 3, gtimer());  // last result
+        if (a.stamp && lane == 0) {
+          const unsigned long long t = gtimer();
+          unsigned long long* e = a.stamp + 8 * (r & 8191);
+          atomicMax(e + 3, t);  // last result
+          atomicMin(e + 5, t);  // first result
+          atomicAdd(e + 6, t - e[0]);  // mean result time (after the publish)
+          atomicAdd(e + 7, 1ull);
+        }
         pc.mark(5);  // bits + publish
         // off the critical path: payload, then its own tag after a release
         if (lane == 0) {
@@ -798,6 +837,9 @@ struct SeqShared {
   int res_d[kMaxMoves];  // N offset at each consumed move
   Round done;            // previous round, processed by the helpers
   double acc_du[kMaxAcc], acc_dw[kMaxAcc];
+  double st_e[kMaxAcc + 1], st_w[kMaxAcc + 1];  // statistics: states of the round
+  uint64_t st_n[kMaxAcc + 1];
+  double st_v[kMaxAcc + 1][4];
   unsigned long long stops[kNStop];
   unsigned long long lat[6];
   uint64_t dw[kDecWords];  // decision words being broadcast
@@ -923,62 +965,100 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
     }
     if (mine) fence_gpu();  // every commit is in L2 before the next decision is published
   } else if (warp == kPollWarps + 1) {  // statistics (engine.hpp:293-308, 413-426)
-    if (lane < D.nacc) {
+#ifdef GCMC_EXP_NOSTATS
+    return;
+#endif
+    // Warp-parallel form of the reference's per-step loop with its exact
+    // operation order: the energy/virial chain over the accepted moves and
+    // the running sums over the sampled steps stay sequential double adds
+    // (lane 0), everything else is per lane.
+    const int len = D.len, nacc = D.nacc;
+    ChainState& ks = sh.ks;
+    if (lane < nacc) {
       const SlotExt* ex = ext_of(D.acc_s[lane]);
       sh.acc_du[lane] = ex->du;
       sh.acc_dw[lane] = ex->dw;
     }
     __syncwarp();
-    if (lane == 0) {
-      ChainState& ks = sh.ks;
-      uint64_t step = ks.step, samples = ks.samples;
-      uint64_t att0 = 0, att1 = 0, att2 = 0;
-      double sum_n = ks.sum_n, sum_n2 = ks.sum_n2, sum_u = ks.sum_u, sum_p = ks.sum_p;
+    if (lane == 0) {  // state k = after the k-th accepted move of the round
       double energy = ks.energy, virial = ks.virial;
       uint64_t cur = D.n;
-      Observables ob = observables(a, cur, energy, virial);
-      double nd = (double)cur, nd2 = __dmul_rn(nd, nd);
-      // sampled(step) = step > equil && (step - equil) % interval == 0, tracked incrementally
-      uint64_t rem = step > a.equil ? (step - a.equil) % a.interval : 0;
-      int k = 0;
-      for (int i = 0; i < D.len; ++i) {
-        const int kind = D.kind[i];
-        att0 += kind == 0;
-        att1 += kind == 1;
-        att2 += kind == 2;
-        if (k < D.nacc && D.acc_i[k] == i) {
-          energy = __dadd_rn(energy, sh.acc_du[k]);
-          virial = __dadd_rn(virial, sh.acc_dw[k]);
-          ++ks.accepted[kind];
-          cur = kind == 1 ? cur + 1 : (kind == 2 ? cur - 1 : cur);
-          ob = observables(a, cur, energy, virial);
-          nd = (double)cur;
-          nd2 = __dmul_rn(nd, nd);
-          ++k;
+      sh.st_e[0] = energy;
+      sh.st_w[0] = virial;
+      sh.st_n[0] = cur;
+      for (int k = 0; k < nacc; ++k) {
+        energy = __dadd_rn(energy, sh.acc_du[k]);
+        virial = __dadd_rn(virial, sh.acc_dw[k]);
+        const int kind = D.acc_kind[k];
+        ++ks.accepted[kind];
+        cur = kind == 1 ? cur + 1 : (kind == 2 ? cur - 1 : cur);
+        sh.st_e[k + 1] = energy;
+        sh.st_w[k + 1] = virial;
+        sh.st_n[k + 1] = cur;
+      }
+      ks.energy = energy;
+      ks.virial = virial;
+    }
+    __syncwarp();
+    for (int k = lane; k <= nacc; k += 32) {  // sampled values of each state
+      const uint64_t cur = sh.st_n[k];
+      const Observables ob = observables(a, cur, sh.st_e[k], sh.st_w[k]);
+      const double nd = (double)cur;
+      sh.st_v[k][0] = nd;
+      sh.st_v[k][1] = __dmul_rn(nd, nd);
+      sh.st_v[k][2] = ob.rep_u;
+      sh.st_v[k][3] = ob.pres;
+    }
+    // attempted moves by kind; sampled steps (move i ends step step0 + i + 1)
+    const uint64_t step0 = ks.step;
+    unsigned smp[kMH];
+    unsigned att0 = 0, att1 = 0, att2 = 0;
+#pragma unroll
+    for (int h = 0; h < kMH; ++h) {
+      const int i = lane + 32 * h;
+      const bool in = i < len;
+      const int kind = in ? D.kind[i] : 3;
+      att0 += __popc(__ballot_sync(0xffffffffu, kind == 0));
+      att1 += __popc(__ballot_sync(0xffffffffu, kind == 1));
+      att2 += __popc(__ballot_sync(0xffffffffu, kind == 2));
+      const uint64_t st = step0 + (uint64_t)i + 1;
+      const bool sm = in && st > a.equil && (a.interval == 1 || (st - a.equil) % a.interval == 0);
+      smp[h] = __ballot_sync(0xffffffffu, sm);
+    }
+    __syncwarp();
+    if (lane == 0) {  // running sums in step order; state k holds for moves [acc_i[k-1], acc_i[k])
+      double sn = ks.sum_n, sn2 = ks.sum_n2, su = ks.sum_u, sp = ks.sum_p;
+      uint64_t samples = 0;
+      int lo = 0;
+      for (int k = 0; k <= nacc; ++k) {
+        const int hi = k < nacc ? D.acc_i[k] : len;
+        int c = 0;
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) {
+          const int a0 = lo - 32 * h, a1 = hi - 32 * h;  // bit range [a0, a1) of word h
+          const unsigned m_hi = a1 >= 32 ? 0xffffffffu : (a1 <= 0 ? 0u : (1u << a1) - 1u);
+          const unsigned m_lo = a0 >= 32 ? 0xffffffffu : (a0 <= 0 ? 0u : (1u << a0) - 1u);
+          c += __popc(smp[h] & m_hi & ~m_lo);
         }
-        ++step;
-        if (step > a.equil) {
-          rem = step == a.equil + 1 ? (a.interval == 1 ? 0 : 1) : (rem + 1 == a.interval ? 0 : rem + 1);
-          if (rem == 0) {
-            ++samples;
-            sum_n = __dadd_rn(sum_n, nd);
-            sum_n2 = __dadd_rn(sum_n2, nd2);
-            sum_u = __dadd_rn(sum_u, ob.rep_u);
-            sum_p = __dadd_rn(sum_p, ob.pres);
-          }
+        const double v0 = sh.st_v[k][0], v1 = sh.st_v[k][1], v2 = sh.st_v[k][2], v3 = sh.st_v[k][3];
+        for (int j = 0; j < c; ++j) {
+          sn = __dadd_rn(sn, v0);
+          sn2 = __dadd_rn(sn2, v1);
+          su = __dadd_rn(su, v2);
+          sp = __dadd_rn(sp, v3);
         }
+        samples += (uint64_t)c;
+        lo = hi;
       }
       ks.attempted[0] += att0;
       ks.attempted[1] += att1;
       ks.attempted[2] += att2;
-      ks.step = step;
-      ks.samples = samples;
-      ks.sum_n = sum_n;
-      ks.sum_n2 = sum_n2;
-      ks.sum_u = sum_u;
-      ks.sum_p = sum_p;
-      ks.energy = energy;
-      ks.virial = virial;
+      ks.step = step0 + (uint64_t)len;
+      ks.samples += samples;
+      ks.sum_n = sn;
+      ks.sum_n2 = sn2;
+      ks.sum_u = su;
+      ks.sum_p = sp;
     }
   } else if (a.trace) {  // trace records (MoveOutcome, engine.hpp:104-110)
     const int nt = (kThreads / 32 - kPollWarps - 2) * 32;
@@ -1100,7 +1180,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(1);  // poll (waiting for the evaluators)
-      if (a.stamp && tid == 0) a.stamp[5 * (r & 8191) + 4] = gtimer();  // sequencer has all
+      if (a.stamp && tid == 0) a.stamp[8 * (r & 8191) + 4] = gtimer();  // sequencer has all
       if (warp == 0) {  // ---- walk (table-driven: bit j of a mask <-> d = j - 16)
         const int fit = sh.fit;
         uint32_t accm[kMH], stopm[kMH], ovfm[kMH], cfmk[kMH];
@@ -1299,8 +1379,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
     }
     __syncthreads();
-    if (a.stamp && tid == 0) a.stamp[5 * ((r + 1) & 8191)] = gtimer();  // publish of D_{r+1}
+    if (a.stamp && tid == 0) a.stamp[8 * ((r + 1) & 8191)] = gtimer();  // publish of D_{r+1}
     broadcast_dec(a, sh, tid);
+    pc.mark(8);  // close until the publish
     // next round's shape, masks, ring (while the evaluators work)
     if (warp == 0) {
       const uint64_t want = nbase + kRing < a.nmoves ? nbase + kRing : a.nmoves;
@@ -1316,7 +1397,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       sh.macc[tid - 32] = sh.mcov[tid - 32] = sh.mcf[tid - 32] = sh.mov[tid - 32] = 0;
     }
     __syncthreads();
-    pc.mark(5);  // close + publish + next shape
+    pc.mark(5);  // next shape (after the publish)
     ph.mark(1);
     base = nbase;
     n = nn;
@@ -1440,6 +1521,9 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
     smem = eval_bytes;
   }
   if (smem < sizeof(SeqShared)) smem = sizeof(SeqShared);
+  if (a.prof)
+    std::fprintf(stderr, "[engine prof] smem=%zu eval=%zu seq=%zu occ_replica=%d nb=%u\n", smem,
+                 eval_bytes, sizeof(SeqShared), a.smem_occ, c.mirror.nb);
   void (*kern)(EngineArgs) = T == 128 ? k_engine<128> : (T == 256 ? k_engine<256> : k_engine<512>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return cuda_error(e, "engine smem");

@@ -18,6 +18,7 @@
 // offsets 0..5 into a segment), composes the lane maps with a warp scan, then
 // re-walks and emits.
 #include "internal.h"
+#include "mirror.cuh"
 
 namespace gcmcb {
 
@@ -153,7 +154,9 @@ __global__ void __launch_bounds__(kThreads) k_gen(GenArgs a) {
           const int len = len_at(p);
           if (mi < a.nmoves) {
             Proposal pr;
-            pr.pad = 0;
+            pr.wmask = kNoMask;
+            pr.bpt = 0;
+            pr.cell = 0;
             const double sel = D(p);
             if (sel < a.dp) {
               pr.kind = 0;
@@ -216,6 +219,36 @@ __global__ void __launch_bounds__(kThreads) k_gen(GenArgs a) {
   }
 }
 
+// The state-independent part of each proposal's evaluation, once per
+// proposal and off the engine's critical path: the pruned brick window of the
+// new position (window_keep, the same arithmetic as the engine's own
+// window_bricks_warp), its packed brick point and reference-grid cell.
+// Deletions and max_displacement displacements (new position relative to the
+// mover) get kNoMask and are computed in the engine.
+__global__ void __launch_bounds__(256) k_annotate(Proposal* p, uint64_t n, Mirror m, Box b,
+                                                  Grid g, int raw) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    Proposal& q = p[i];
+    uint32_t mask = kNoMask, bpt = 0;
+    int cell = 0;
+    if (q.kind != 2 && !(q.kind == 0 && raw) && m.dims >= 3) {
+      const double x = q.x, y = q.y, z = q.z;
+      const int bx = mcoord(m, x), by = mcoord(m, y), bz = mcoord(m, z);
+      mask = 0;
+      for (int l = 0; l < 27; ++l) {
+        uint32_t id;
+        if (window_keep(m, b, x, y, z, bx, by, bz, l, id)) mask |= 1u << l;
+      }
+      bpt = (uint32_t)bx | ((uint32_t)by << 8) | ((uint32_t)bz << 16);
+      if (g.kind != GCMC_ALL_PAIRS) cell = cell_of(g, x, y, z);
+    }
+    q.wmask = mask;
+    q.bpt = bpt;
+    q.cell = cell;
+  }
+}
+
 }  // namespace
 
 gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s) {
@@ -227,6 +260,8 @@ gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n
   GenArgs a{mt, out, n, c.params.displace_percent, c.box.l,
             c.params.max_displacement > 0.0 ? 1 : 0};
   k_gen<<<1, kThreads, 0, s>>>(a);
+  const unsigned blocks = (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  k_annotate<<<blocks, 256, 0, s>>>(out, n, c.mirror, c.box, c.grid, a.raw_disp);
   cudaError_t e = cudaGetLastError();
   if (e) return cuda_error(e, "gen_proposals");
   return GCMC_OK;

@@ -43,46 +43,72 @@ __device__ __forceinline__ bool mnear(const Mirror& m, uint64_t a, uint64_t b) {
          axis_near(pt_z(a), pt_z(b), m.dims, m.reach);
 }
 
-// Brick (ox, oy, oz) offsets of the 3x3x3 window that can hold a particle
-// within r_cut of p: bricks whose box lies farther than r_cut from p are
-// pruned (spherical window; ~20 of 27 bricks at side ~ r_cut). Returns the
-// brick count and writes ids to out[0..26]. Lanes 0..26 of a warp call it
-// cooperatively (one offset each); result compacted by ballot.
+// Tiny grids (dims < 3): every brick of the box is in the window.
+static __device__ __noinline__ int window_bricks_small(const Mirror& m, uint32_t* out, int lane) {
+  const int nb = m.dims * m.dims * m.dims;
+  if (lane < nb) out[lane] = (uint32_t)lane;
+  return nb;
+}
+
+// Window offset `lane` (0..26: ox = lane % 3 - 1, oy = lane / 3 % 3 - 1,
+// oz = lane / 9 - 1) of a point in brick (bx, by, bz), dims >= 3: its brick
+// id, and whether the brick's box lies within r_cut of the point (spherical
+// pruning; ~20 of 27 bricks at side ~ r_cut).
+__device__ __forceinline__ bool window_keep(const Mirror& m, const Box& b, double x, double y,
+                                            double z, int bx, int by, int bz, int lane,
+                                            uint32_t& id) {
+  const int d = m.dims;
+  const int ox = lane % 3 - 1, oy = (lane / 3) % 3 - 1, oz = lane / 9 - 1;
+  int cx = bx + ox, cy = by + oy, cz = bz + oz;
+  cx += cx < 0 ? d : 0;
+  cx -= cx >= d ? d : 0;
+  cy += cy < 0 ? d : 0;
+  cy -= cy >= d ? d : 0;
+  cz += cz < 0 ? d : 0;
+  cz -= cz >= d ? d : 0;
+  id = (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
+  // distance from p to the brick's box along each axis
+  auto ax = [&](double v, int bc, int o) {
+    const double f = __dsub_rn(v, __dmul_rn((double)bc, m.side));  // offset in own brick
+    const double t = o == 0 ? 0.0 : (o > 0 ? __dsub_rn(m.side, f) : f);
+    return t > 0.0 ? t : 0.0;
+  };
+  const double dx = ax(x, bx, ox), dy = ax(y, by, oy), dz = ax(z, bz, oz);
+  const double d2 = dx * dx + dy * dy + dz * dz;
+  return d2 <= b.rc2 * (1.0 + 1e-9) + 1e-12;
+}
+
+// The window of a point as brick ids in out[0..], lanes 0..26 of a warp
+// cooperatively (one offset each), compacted by ballot in offset order.
 __device__ __forceinline__ int window_bricks_warp(const Mirror& m, const Box& b, double x,
                                                   double y, double z, uint32_t* out, int lane) {
-  const int d = m.dims;
-  const int cnt = d < 3 ? d : 3;
+  if (m.dims < 3) return window_bricks_small(m, out, lane);
   const int bx = mcoord(m, x), by = mcoord(m, y), bz = mcoord(m, z);
-  bool keep = false;
   uint32_t id = 0;
-  if (lane < cnt * cnt * cnt) {
-    const int ix = lane % cnt, iy = (lane / cnt) % cnt, iz = lane / (cnt * cnt);
-    // offsets -1, 0, +1 (or 0..cnt-1 from -1 for tiny grids)
-    const int ox = ix - 1, oy = iy - 1, oz = iz - 1;
-    int cx = bx + ox, cy = by + oy, cz = bz + oz;
+  const bool keep = lane < 27 && window_keep(m, b, x, y, z, bx, by, bz, lane, id);
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  if (keep) out[__popc(mask & ((1u << lane) - 1u))] = id;
+  return __popc(mask);
+}
+
+// The same window from a precomputed offset mask (Proposal::wmask) and
+// packed brick point: integer work only.
+__device__ __forceinline__ int window_bricks_mask(const Mirror& m, uint32_t wmask, uint32_t bpt,
+                                                  uint32_t* out, int lane) {
+  const bool keep = lane < 27 && ((wmask >> lane) & 1u);
+  if (keep) {
+    const int d = m.dims;
+    int cx = pt_x(bpt) + lane % 3 - 1, cy = pt_y(bpt) + (lane / 3) % 3 - 1, cz = pt_z(bpt) + lane / 9 - 1;
     cx += cx < 0 ? d : 0;
     cx -= cx >= d ? d : 0;
     cy += cy < 0 ? d : 0;
     cy -= cy >= d ? d : 0;
     cz += cz < 0 ? d : 0;
     cz -= cz >= d ? d : 0;
-    id = (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
-    keep = true;
-    if (d >= 3) {
-      // distance from p to the brick's box along each axis
-      auto ax = [&](double v, int bc, int o) {
-        const double f = __dsub_rn(v, __dmul_rn((double)bc, m.side));  // offset in own brick
-        double t = o == 0 ? 0.0 : (o > 0 ? __dsub_rn(m.side, f) : f);
-        return t > 0.0 ? t : 0.0;
-      };
-      const double dx = ax(x, bx, ox), dy = ax(y, by, oy), dz = ax(z, bz, oz);
-      const double d2 = dx * dx + dy * dy + dz * dz;
-      keep = d2 <= b.rc2 * (1.0 + 1e-9) + 1e-12;
-    }
+    out[__popc(wmask & ((1u << lane) - 1u))] =
+        (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
   }
-  const unsigned mask = __ballot_sync(0xffffffffu, keep);
-  if (keep) out[__popc(mask & ((1u << lane) - 1u))] = id;
-  return __popc(mask);
+  return __popc(wmask);
 }
 
 }  // namespace gcmcb

@@ -12,8 +12,8 @@
 //   gather  every thread loads the x/y/z record planes of its candidates
 //           (one dependent L2 hop for the whole window);
 //   math    FP64 minimum-image r^2 with the reference's exact rounding
-//           (common.cuh); in-cutoff pairs are compacted per warp through a
-//           shared queue so the LJ divide runs on full warps;
+//           (common.cuh) and the LJ pair for those within r_cut (latency
+//           form: two candidates per thread, no compaction);
 //   reduce  warp tree + fixed-order cross-warp sum (deterministic).
 //
 // The mover's own record is excluded by record index (the reference skips
@@ -25,7 +25,6 @@ namespace gcmcb {
 
 constexpr int kMaxEnt = 54;     // 2 windows x 27 bricks
 constexpr int kCandMax = 1536;  // expanded candidates per group per pass
-constexpr int kQueue = 64;      // per-warp in-cutoff queue
 
 template <int T>
 struct WinWs {
@@ -38,8 +37,6 @@ struct WinWs {
   uint32_t brick[kMaxEnt];
   int pre[kMaxEnt + 1];
   uint16_t cand[kCandMax];     // entry << 7 | slot
-  double qr2[T / 32][kQueue];  // in-cutoff queue: r^2
-  float qs[T / 32][kQueue];    // and sign
   double red[T / 32][2];
 };
 
@@ -70,22 +67,19 @@ __device__ __forceinline__ void win_finish(const Mirror& m, WinWs<T>& ws, const 
     const uint32_t id = ws.brick[lane + 32];
     o1 = occ_s ? (int)occ_s[id] : __ldcg(m.occ + id);
   }
-  int s0 = o0, s1 = o1;
+  // one scan of both halves packed in 16 bits each (counts <= 27 * cap < 2^16)
+  int s = o0 | (o1 << 16);
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, s0, o);
-    const int c = __shfl_up_sync(0xffffffffu, s1, o);
-    if (lane >= o) {
-      s0 += a;
-      s1 += c;
-    }
+    const int t = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += t;
   }
-  const int tot0 = __shfl_sync(0xffffffffu, s0, 31);
-  s1 += tot0;
-  const int e0 = s0 - o0, e1 = s1 - o1;  // exclusive
+  const int last = __shfl_sync(0xffffffffu, s, 31);
+  const int tot0 = last & 0xffff;
+  const int e0 = (s & 0xffff) - o0, e1 = tot0 + (s >> 16) - o1;  // exclusive
   if (lane < nent) ws.pre[lane] = e0;
   if (lane + 32 < nent) ws.pre[lane + 32] = e1;
-  const int total = __shfl_sync(0xffffffffu, s1, 31);
+  const int total = tot0 + (last >> 16);
   if (lane == 0) {
     ws.nent0 = nent0;
     ws.nent = nent;
@@ -93,8 +87,10 @@ __device__ __forceinline__ void win_finish(const Mirror& m, WinWs<T>& ws, const 
     ws.total = total;
   }
   // expansion (first kCandMax candidates; the rest are found by search)
+#pragma unroll 1
   for (int k = 0; k < o0; ++k)
     if (e0 + k < kCandMax) ws.cand[e0 + k] = (uint16_t)((lane << 7) | k);
+#pragma unroll 1
   for (int k = 0; k < o1; ++k)
     if (e1 + k < kCandMax) ws.cand[e1 + k] = (uint16_t)(((lane + 32) << 7) | k);
 }
@@ -121,25 +117,26 @@ __device__ __forceinline__ void lj_accum(const Box& b, double r2, double sign, d
 
 // All T threads (after the group barrier that publishes ws): Σ_w sign_w Σ
 // pair(centre_w, record) over the candidates, excluding record ws.excl.
-// Returns per-thread partial sums (reduce with group_reduce).
+// Returns per-thread partial sums (reduce with group_reduce). Latency form:
+// a thread takes candidates gt and gt + T (both gathers in flight at once),
+// then runs the pair math on each; no compaction (one window is < 2T).
 template <int T>
 __device__ __forceinline__ void win_sums(const Mirror& m, const Box& b, WinWs<T>& ws, int gt,
                                          double& du, double& dw) {
-  constexpr int U = 4;
-  const int lane = threadIdx.x & 31, warp = gt >> 5;
   const int total = ws.total;
-  int qn = 0;  // warp-uniform queue fill
   du = 0.0;
   dw = 0.0;
-  for (int base = 0; base < total; base += T * U) {
-    double rx[U], ry[U], rz[U];
-    int win[U];
-    bool ok[U];
+#pragma unroll 1
+  for (int base = 0; base < total; base += 2 * T) {
+    double rx[2], ry[2], rz[2];
+    int win[2];
+    bool ok[2];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < 2; ++u) {
       const int f = base + u * T + gt;
       ok[u] = f < total;
       win[u] = 0;
+      rx[u] = ry[u] = rz[u] = 0.0;
       if (ok[u]) {
         int e, k;
         if (f < kCandMax) {
@@ -166,41 +163,17 @@ __device__ __forceinline__ void win_sums(const Mirror& m, const Box& b, WinWs<T>
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      double r2 = 0.0;
-      bool in = false;
-      if (ok[u]) {
-        const int w = win[u];
-        r2 = min_image_dist2(ws.cx[w], ws.cy[w], ws.cz[w], rx[u], ry[u], rz[u], b);
-        in = r2 <= b.rc2;
-      }
-      // compaction of in-cutoff pairs into the warp queue
-      const unsigned mask = __ballot_sync(0xffffffffu, in);
-      if (mask) {
-        const int pos = qn + __popc(mask & ((1u << lane) - 1u));
-        if (in) {
-          ws.qr2[warp][pos] = r2;
-          ws.qs[warp][pos] = win[u] ? (float)ws.sign1 : 1.0f;
-        }
-        qn += __popc(mask);
-        __syncwarp();
-        if (qn >= 32) {  // drain one full warp of pairs
-          lj_accum(b, ws.qr2[warp][lane], (double)ws.qs[warp][lane], du, dw);
-          qn -= 32;
-          const double t = ws.qr2[warp][32 + lane];
-          const float s = ws.qs[warp][32 + lane];
-          __syncwarp();
-          if (lane < qn) {
-            ws.qr2[warp][lane] = t;
-            ws.qs[warp][lane] = s;
-          }
-          __syncwarp();
-        }
+#pragma unroll 1
+    for (int u = 0; u < 2; ++u) {
+      const bool o = u ? ok[1] : ok[0];
+      if (o) {
+        const int w = u ? win[1] : win[0];
+        const double r2 = min_image_dist2(ws.cx[w], ws.cy[w], ws.cz[w], u ? rx[1] : rx[0],
+                                          u ? ry[1] : ry[0], u ? rz[1] : rz[0], b);
+        if (r2 <= b.rc2) lj_accum(b, r2, w ? (double)ws.sign1 : 1.0, du, dw);
       }
     }
   }
-  if (lane < qn) lj_accum(b, ws.qr2[warp][lane], (double)ws.qs[warp][lane], du, dw);
 }
 
 // Group-wide deterministic reduction; result valid in thread gt == leader_gt

@@ -32,5 +32,10 @@ for r in data:
     for s in stalls: a[2][s[6:]] += f(r, s)
 tot = sum(a[0] for a in agg.values())
 print(f"total samples {tot:.0f}")
-for k, a in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{a[0]:7.0f} {100*a[0]/tot:5.1f}% inst {a[1]:10.0f}  {k:28s} {a[2].most_common(2)}")
+# samples of warps that are not parked at a barrier or asleep (the serial chains)
+act = lambda a: a[0] - a[2]["barrier"] - a[2]["sleep"]
+tact = sum(act(a) for a in agg.values())
+print(f"active samples {tact:.0f}")
+for k, a in sorted(agg.items(), key=lambda kv: -act(kv[1]))[:top]:
+    c = a[2].copy(); c.pop("barrier", None); c.pop("sleep", None)
+    print(f"{act(a):7.0f} {100*act(a)/tact:5.1f}% inst {a[1]:10.0f}  {k:28s} {c.most_common(3)}")
