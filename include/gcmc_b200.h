@@ -68,6 +68,9 @@ typedef struct gcmc_params {
   int32_t engine_group;       /* threads per evaluation slot: 128/256/512 (0 = 256) */
   int32_t engine_variants;    /* N-variants per displace/delete proposal after the first (0 = 9) */
   int32_t engine_bias;        /* initial variant order: -1 N expected to fall, +1 rise (0 = -1) */
+  int32_t engine_mode;        /* 0 = maintained-energy engine where supported (brick strategies,
+                                 max_displacement = 0), 1 = per-window engine always */
+  int32_t engine_pad;
 } gcmc_params;
 
 /* SystemState + RunStatistics + step counter (engine.hpp:112-140, 436). */
@@ -131,6 +134,11 @@ gcmc_status gcmc_commit_insert(gcmc_dev* h, const double pos[3], uint64_t* pid);
 gcmc_status gcmc_commit_delete(gcmc_dev* h, uint64_t pid);
 
 gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w);
+
+/* Diagnostic (no reference counterpart): largest |e_i - fresh e_i| over the
+ * per-particle pair energies / virials the maintained-energy engine carries
+ * across moves, against a from-scratch evaluation (0, 0 when not in use). */
+gcmc_status gcmc_energy_drift(gcmc_dev* h, double* max_du, double* max_dw);
 
 /* std::mt19937_64 state in libstdc++ order: 312 words + position (_M_p),
  * plus RngStream's draw counter. */

@@ -30,7 +30,8 @@ class GcmcParams(C.Structure):
                 ("equilibration_steps", _u64), ("sampling_interval", _u64),
                 ("strategy", _i32), ("cell_capacity", _i32), ("microcell_capacity", _i32),
                 ("tail_corrections", _i32), ("max_particles", _u64), ("engine_ctas", _i32),
-                ("engine_group", _i32), ("engine_variants", _i32), ("engine_bias", _i32)]
+                ("engine_group", _i32), ("engine_variants", _i32), ("engine_bias", _i32),
+                ("engine_mode", _i32), ("engine_pad", _i32)]
 
 
 class GcmcState(C.Structure):
@@ -53,7 +54,7 @@ EXPORTS = [
     "gcmc_download_positions", "gcmc_build", "gcmc_grid_info", "gcmc_download_grid",
     "gcmc_rebuild_check", "gcmc_peak_occupancy", "gcmc_delta_displace", "gcmc_delta_insert",
     "gcmc_delta_delete", "gcmc_delta_batch", "gcmc_commit_displace", "gcmc_commit_insert",
-    "gcmc_commit_delete", "gcmc_total_energy", "gcmc_seed_rng", "gcmc_set_rng_state",
+    "gcmc_commit_delete", "gcmc_total_energy", "gcmc_energy_drift", "gcmc_seed_rng", "gcmc_set_rng_state",
     "gcmc_get_rng_state", "gcmc_set_state", "gcmc_get_state", "gcmc_run_moves",
     "gcmc_random_initial_configuration",
 ]
@@ -100,6 +101,7 @@ def load(path: str = SO):
         "gcmc_commit_insert": [_p, _dp, P(_u64)],
         "gcmc_commit_delete": [_p, _u64],
         "gcmc_total_energy": [_p, _dp, _dp],
+        "gcmc_energy_drift": [_p, _dp, _dp],
         "gcmc_seed_rng": [_p, _u64],
         "gcmc_set_rng_state": [_p, P(_u64), _u64, _u64],
         "gcmc_get_rng_state": [_p, P(_u64), P(_u64), P(_u64)],

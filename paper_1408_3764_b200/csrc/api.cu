@@ -260,6 +260,7 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   }
   CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
   CK(cudaMalloc(&c->rslot, capn * sizeof(int32_t)), "alloc rslot");
+  CK(cudaMalloc(&c->ep, capn * sizeof(double2)), "alloc energies");
   if (g.ncells) {
     CK(cudaMalloc(&g.occ, g.ncells * sizeof(int32_t)), "alloc occ");
     CK(cudaMalloc(&g.slots, g.ncells * g.cap * sizeof(int32_t)), "alloc slots");
@@ -303,6 +304,8 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   cudaFree(c->grid.occ);
   cudaFree(c->grid.slots);
   cudaFree(c->rslot);
+  cudaFree(c->ep);
+  cudaFree(c->eng2_buf);
   cudaFree(c->mirror.rid);
   cudaFree(c->eng_dec);
   cudaFree(c->eng_res);
@@ -495,6 +498,14 @@ gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w) {
   gcmc_status s = pull_state(c);
   if (s) return s;
   return total_energy(c, u, w);
+}
+
+gcmc_status gcmc_energy_drift(gcmc_dev* h, double* max_du, double* max_dw) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  return epart_drift(c, max_du, max_dw);
 }
 
 gcmc_status gcmc_seed_rng(gcmc_dev* h, uint64_t seed) {

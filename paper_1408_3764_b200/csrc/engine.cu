@@ -42,6 +42,7 @@
 #include <cstdio>
 #include "internal.h"
 #include "slot.cuh"
+#include "sync.cuh"
 
 namespace gcmcb {
 
@@ -64,7 +65,6 @@ constexpr int kSlotsPerPoller = 2;
 constexpr int kMaxSlots = kPollWarps * 32 * kSlotsPerPoller;
 constexpr int kInsSpan = 32;     // insertion accept mask covers d in [-16, 15]
 
-constexpr uint64_t kPay = 0xffffffffffffull;
 
 enum SlotFlag : uint32_t {
   kFKindMask = 3u,   // 0 displace, 1 insert, 2 delete
@@ -105,54 +105,6 @@ struct EngineArgs {
   unsigned epoll_ns;  // back-off between polls (evaluators)
   unsigned long long* prof;
   unsigned long long* stamp;  // profiling: [0] publish time, [1 + slot] (seen, done) pairs
-};
-
-// ----------------------------------------------------------------- words
-__device__ __forceinline__ uint64_t tagw(uint32_t r, uint64_t payload) {
-  return ((uint64_t)(r & 0xffffu) << 48) | (payload & kPay);
-}
-__device__ __forceinline__ bool tagged(uint64_t w, uint32_t r) {
-  return (uint32_t)(w >> 48) == (r & 0xffffu);
-}
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void nap() { __nanosleep(20); }
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-// Phase timers (GCMC_ENGINE_PROFILE=1): prof[role*16 + phase] accumulates ns.
-struct PhaseClock {
-  unsigned long long acc[12] = {0};
-  unsigned long long t = 0;
-  bool on = false;
-  __device__ __forceinline__ void start(bool enable) {
-    on = enable;
-    if (on) t = clock64();
-  }
-  __device__ __forceinline__ void mark(int k) {
-    if (!on) return;
-    const unsigned long long n = clock64();
-    acc[k] += n - t;
-    t = n;
-  }
-  __device__ __forceinline__ void flush(unsigned long long* p) {
-    if (!on) return;
-    for (int k = 0; k < 12; ++k) p[k] = acc[k];
-  }
 };
 
 // ----------------------------------------------------------------- variants
@@ -313,13 +265,6 @@ struct Dec {
   RW acc[kMaxAcc];
   int kind[kMaxAcc];
 };
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Ring refill by one warp: proposals [lo, hi) (8-byte async copies).
 __device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, uint64_t lo,
@@ -1460,6 +1405,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(EngineArgs a) {
 
 gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaStream_t s) {
   if (nmoves == 0) return GCMC_OK;
+  if (engine2_supported(c)) return engine2_run(c, nmoves, trace_d, s);
+  c.e_valid = false;  // this engine does not maintain the per-particle energies
   const gcmc_params& P = c.params;
   EngineArgs a{};
   a.g = c.grid;

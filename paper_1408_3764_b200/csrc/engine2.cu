@@ -1,0 +1,1430 @@
+// Maintained-energy engine: Simulation::step() x n (engine.hpp:293-308,
+// 350-426) as exact multi-move speculation in which every move costs ONE
+// evaluation slot, whatever N turns out to be.
+//
+// The per-window engine (engine.cu) pays a window evaluation for every
+// distinct particle a displacement / deletion could pick over its candidate
+// N: the old-position sum Σ_j u(x_pid, x_j) is what makes a move depend on N.
+// Here every particle carries its current pair energy and virial
+//   e[i] = Σ_{j != i, r_ij <= r_c} (u_ij, w_ij)
+// maintained on the device across accepted moves, so
+//   delete  pid:      ΔU = -e[pid]                                  (no window)
+//   displace pid->n:  ΔU = (S(n) - pair(n, x_pid)) - e[pid]         (window of n)
+//   insert  n:        ΔU = S(n)                                     (window of n)
+// where S(n) = Σ_all pair(n, x_j) does not depend on N. A slot evaluates S(n)
+// once with its whole group, then its leader warp resolves all 32 candidate N
+// (offsets d = -16..15 around the round's starting N, one lane each: pid =
+// index_from(pick, N + d), one load of x_pid and e[pid]) into accept bits.
+// ΔU differs from the reference's Kahan sums only by rounding (parity bound
+// 1e-10 relative, observed ~1e-15); the exclusion pair(n, x_pid) is a plain
+// subtraction unless it is large enough to cost precision, in which case the
+// warp re-sums the window without pid.
+//
+// A round: decision D_r (base, N, the previous round's accepted moves) ->
+// each evaluator group takes slot s = move base + s (s < fit) -> the
+// sequencer polls the slots' accept / stop / overflow masks, walks the moves
+// tracking N, verifies that no consumed move read anything an earlier
+// accepted move of the round changed (exact distances: a move reads the
+// positions within r_c of its new point and e / x of its particle), and
+// publishes D_{r+1}. Commits of round r run during round r+1:
+//   * structural (positions, reference grid, brick mirror, e of the mover):
+//     the sequencer's helper warp, then a release of flags[0] = r;
+//   * pair-energy updates of the neighbours (e_j -= u(o, x_j), e_j += u(n,
+//     x_j)): one reserved evaluator group per accepted move, after flags[0];
+//     the sequencer waits for all of them before publishing D_{r+2}.
+// An evaluation of round r+1 whose window overlaps a brick a round-r commit
+// changes waits for flags[0] (it then reads the committed state); one whose
+// particle might be touched by an in-flight commit or energy update (same
+// index, or within r_c of a changed position) stops the walk there, and the
+// move is re-evaluated in the next round.
+//
+// Supported: brick-window strategies (microcell, cell list) with whole-box
+// displacements (max_displacement = 0, the bench and paper configuration).
+// Otherwise engine.cu runs.
+#include <cstdio>
+#include <cstdlib>
+
+#include "commit.cuh"
+#include "internal.h"
+#include "slot.cuh"
+#include "sync.cuh"
+
+namespace gcmcb {
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kMaxMoves = 256;            // moves per round
+constexpr int kMH = kMaxMoves / 32;       // moves per walk lane
+constexpr int kMaxAcc = 32;               // accepted moves per round (= reserved e-update groups)
+constexpr int kRing = 512;                // proposal ring (>= 2 * kMaxMoves)
+constexpr int kHalf = 16;                 // N offsets d = -16..15 <-> bit d + 16
+constexpr int kDecHdr = 4;
+constexpr int kDecEnt = 3;
+constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 100
+constexpr int kDecStride = 128;
+constexpr int kResWords = 3;
+constexpr int kPollWarps = 12;
+constexpr int kMaxSlots = 768;            // buffer sizing: evaluator groups
+constexpr double kHugeTerm = 1e4;         // |pair(n, x_pid)| above this: re-sum without pid
+
+struct OffRec {  // one candidate N offset of a slot (accepted offsets; all when tracing)
+  double du, dw;  // ΔU, ΔW
+  double su, sw;  // e of the mover after the move
+  double pe;      // acceptance probability
+  double pad;
+};
+struct SlotExt {
+  OffRec off[32];
+  uint64_t tag;
+  uint64_t pad[3];
+};
+static_assert(sizeof(SlotExt) % 32 == 0, "SlotExt layout");
+
+struct ATab {  // accepted move k of a round, exact (sequencer -> evaluators)
+  double ox, oy, oz, nx, ny, nz;
+  int64_t ia, ib;
+  int32_t kind, pad;
+  uint64_t tag;  // round (stored last, release)
+};
+
+struct EngineArgs {
+  Grid g;
+  Mirror m;
+  Box b;
+  Store s;
+  double2* ep;
+  ChainState* st;
+  const Proposal* props;
+  gcmc_trace_rec* trace;
+  uint64_t nmoves;
+  double beta, mu, lambda3, vol, temp;
+  uint64_t equil, interval;
+  int tail, nslots, fitmax;
+  double tail_cu, tail_cp, tail_s3, tail_bu, tail_bp;
+  uint64_t* dec;    // [kDecStride]
+  uint64_t* res;    // [2][kResWords][nslots]
+  SlotExt* ext;     // [2][nslots]
+  ATab* atab;       // [2][kMaxAcc]
+  uint64_t* flags;  // [0] structural commits done through round; [8] energy updates done (count)
+  int smem_occ;
+  unsigned poll_ns, epoll_ns;
+  unsigned long long* prof;
+};
+
+__device__ __forceinline__ int fit_of(const EngineArgs& a, uint64_t base) {
+  if (base >= a.nmoves) return 0;
+  const uint64_t left = a.nmoves - base;
+  return left < (uint64_t)a.fitmax ? (int)left : a.fitmax;
+}
+
+__device__ __forceinline__ bool within_rc(const Box& b, double ax, double ay, double az, double bx,
+                                          double by, double bz) {
+  return min_image_dist2(ax, ay, az, bx, by, bz, b) <= b.rc2 * (1.0 + 1e-9);
+}
+
+// ----------------------------------------------------------------- decision
+struct AccE {
+  uint64_t pt0, pt1;  // brick points: new (displace / insert), old (displace / delete)
+  int64_t ia, ib;     // particle (insert: its new index), last index (delete)
+  int kind;
+};
+struct Dec {
+  uint64_t base, n;
+  int nacc, stop;
+  AccE acc[kMaxAcc];
+};
+
+__device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, uint64_t lo,
+                                         uint64_t hi, int lane) {
+  constexpr unsigned W = sizeof(Proposal) / 8;
+  const unsigned cnt = (unsigned)(hi - lo) * W;
+  for (unsigned k = lane; k < cnt; k += 32) {
+    const uint64_t mv = lo + k / W;
+    const unsigned w = k % W;
+    cp_async8(reinterpret_cast<uint64_t*>(&ring[mv % kRing]) + w,
+              reinterpret_cast<const uint64_t*>(a.props + mv) + w);
+  }
+  cp_async_commit();
+}
+
+// Warp: wait for D_r (self-validating tagged words) and decode it.
+__device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane) {
+  constexpr int PER = (kDecWords + 31) / 32;  // 4
+  uint64_t w[PER];
+  for (;;) {
+    w[0] = ld_relaxed(a.dec + lane);
+    w[1] = ld_relaxed(a.dec + 32 + lane);
+    const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2);
+    const bool h2ok = tagged(h2, r);
+    const int nacc = h2ok ? (int)(h2 & 0xff) : 0;
+    const int need = kDecHdr + kDecEnt * nacc;
+#pragma unroll
+    for (int j = 2; j < PER; ++j) {
+      const int idx = lane + 32 * j;
+      w[j] = idx < need ? ld_relaxed(a.dec + idx) : 0;
+    }
+    bool ok = h2ok;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int idx = lane + 32 * j;
+      if (idx < need && !tagged(w[j], r)) ok = false;
+    }
+    if (__all_sync(0xffffffffu, ok)) break;
+    __nanosleep(a.epoll_ns);
+  }
+  const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2) & kPay;
+  const int nacc = (int)(h2 & 0xff);
+  const int need = kDecHdr + kDecEnt * nacc;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int idx = lane + 32 * j;
+    if (idx >= need) continue;
+    const uint64_t p = w[j] & kPay;
+    if (idx == 0) d.base = p;
+    else if (idx == 1) d.n = p;
+    else if (idx == 2) {
+      d.nacc = nacc;
+      d.stop = (int)((p >> 9) & 1);
+    } else if (idx >= kDecHdr) {
+      const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
+      if (f == 0) {
+        d.acc[e].pt0 = p & kNoPoint;
+        d.acc[e].pt1 = (p >> 24) & kNoPoint;
+      } else if (f == 1) {
+        d.acc[e].kind = (int)(p >> 32) & 3;
+        d.acc[e].ia = (int64_t)(uint32_t)p;
+      } else {
+        const uint32_t ib = (uint32_t)p;
+        d.acc[e].ib = ib == 0xffffffffu ? -1 : (int64_t)ib;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// =================================================================== evaluator
+template <int T>
+struct EvalShared {
+  Proposal ring[kRing];
+  Dec d;
+  WinWs<T> ws[kThreads / T];
+  struct G {
+    int task;        // 0 none, 1 evaluate move i, 2 energy update of accepted entry k
+    int i, k, kind;
+    double nx, ny, nz;
+    double ox, oy, oz;
+    int64_t excl;    // energy update: particle id excluded (the mover)
+    int sgn0, sgn1;  // energy update: window signs
+  } gs[kThreads / T];
+};
+
+// Energy update of accepted move k of round r - 1 (group-wide): the
+// neighbours' e_j lose the pair with the old position and gain the pair with
+// the new one, on the committed state (after flags[0] >= r - 1).
+template <int T>
+__device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& ws, const uint8_t* occ_s,
+                              uint32_t r, int g, int gt, int gw, int lane, int bar_id) {
+  auto& G = sh.gs[g];
+  if (gw == 0) {
+    const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + G.k;
+    if (lane == 0) {
+      while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
+      while (ld_acquire(a.flags) < (uint64_t)(r - 1)) nap();
+    }
+    __syncwarp();
+    const int kind = (int)__ldcg(&t->kind);
+    const double ox = __ldcg(&t->ox), oy = __ldcg(&t->oy), oz = __ldcg(&t->oz);
+    const double nx = __ldcg(&t->nx), ny = __ldcg(&t->ny), nz = __ldcg(&t->nz);
+    const int64_t ia = __ldcg(&t->ia);
+    int nent = 0, nent0 = 0;
+    // window 0: new position (+), window 1: old position (-); a deletion has
+    // only the old one (as window 0, sign -)
+    if (kind != 2) nent = win_add<T>(a.m, a.b, ws, nent, nx, ny, nz, lane);
+    nent0 = nent;
+    if (kind != 1) nent = win_add<T>(a.m, a.b, ws, nent, ox, oy, oz, lane);
+    if (kind == 2) nent0 = nent;
+    win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
+    if (lane == 0) {
+      G.kind = kind;
+      G.nx = kind == 2 ? ox : nx;
+      G.ny = kind == 2 ? oy : ny;
+      G.nz = kind == 2 ? oz : nz;
+      G.ox = ox;
+      G.oy = oy;
+      G.oz = oz;
+      G.sgn0 = kind == 2 ? -1 : 1;
+      G.sgn1 = -1;
+      G.excl = kind == 2 ? -1 : ia;  // displaced particle / inserted index: not its own neighbour
+    }
+  }
+  group_sync(bar_id, T);
+  const int total = ws.total;
+  const double c0x = G.nx, c0y = G.ny, c0z = G.nz, c1x = G.ox, c1y = G.oy, c1z = G.oz;
+  const double s0 = (double)G.sgn0, s1 = (double)G.sgn1;
+  const int64_t excl = G.excl;
+  for (int f = gt; f < total; f += T) {
+    int e, k;
+    if (f < kCandMax) {
+      const int c = ws.cand[f];
+      e = c >> 7;
+      k = c & 127;
+    } else {
+      int lo = 0, hi = ws.nent - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ws.pre[mid] <= f) lo = mid; else hi = mid - 1;
+      }
+      e = lo;
+      k = f - ws.pre[lo];
+    }
+    const int idx = (int)ws.brick[e] * a.m.cap + k;
+    const int32_t rid = __ldcg(a.m.rid + idx);
+    if ((int64_t)rid == excl) continue;
+    const double rx = __ldcg(a.m.rx + idx), ry = __ldcg(a.m.ry + idx), rz = __ldcg(a.m.rz + idx);
+    const bool w1 = e >= ws.nent0;
+    const double r2 = w1 ? min_image_dist2(c1x, c1y, c1z, rx, ry, rz, a.b)
+                         : min_image_dist2(c0x, c0y, c0z, rx, ry, rz, a.b);
+    if (r2 <= a.b.rc2) {
+      double u, w;
+      lj_pair_clamped(r2, a.b, u, w);
+      const double sg = w1 ? s1 : s0;
+      atomicAdd(&a.ep[rid].x, __dmul_rn(sg, u));
+      atomicAdd(&a.ep[rid].y, __dmul_rn(sg, w));
+    }
+  }
+  __threadfence();
+  group_sync(bar_id, T);
+  if (gt == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + 8), 1ull);
+}
+
+template <int T>
+__device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
+  constexpr int MG = kThreads / T;
+  constexpr int kGW = T / 32;
+  auto& sh = *reinterpret_cast<EvalShared<T>*>(smem);
+  uint8_t* occ_s = a.smem_occ ? smem + ((sizeof(EvalShared<T>) + 15) & ~size_t(15)) : nullptr;
+  uint32_t* occ_w = reinterpret_cast<uint32_t*>(occ_s);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = tid / T, gt = tid % T, gw = gt >> 5;
+  const int bar_id = 1 + g;
+  const int slot = (blockIdx.x - 1) * MG + g;
+  const int eslot0 = a.nslots - kMaxAcc;  // groups reserved for energy updates
+  WinWs<T>& ws = sh.ws[g];
+  auto& G = sh.gs[g];
+  const bool grid = a.g.kind != GCMC_ALL_PAIRS;
+  const bool tracing = a.trace != nullptr;
+
+  if (occ_s)
+    for (uint32_t i = tid; i < a.m.nb; i += kThreads) occ_s[i] = (uint8_t)__ldcg(a.m.occ + i);
+  uint64_t ring_hi = a.nmoves < (uint64_t)kRing ? a.nmoves : (uint64_t)kRing;
+  if (tid < 32) {
+    ring_fill(a, sh.ring, 0, ring_hi, lane);
+    cp_async_wait();
+  }
+  __syncthreads();
+  PhaseClock pc;
+  pc.start(a.prof && blockIdx.x == 1 && tid == 0);
+  for (uint32_t r = 1;; ++r) {
+    pc.mark(0);
+    if (tid < 32) {
+      poll_dec(a, r, sh.d, lane);
+      const Dec& d = sh.d;
+      // replica: the previous round's commits (a--, b++)
+      if (occ_s && lane < d.nacc) {
+        const int k = d.acc[lane].kind;
+        if (k != 1) {
+          const uint32_t ba = mbrick(a.m, d.acc[lane].pt1);
+          atomicSub(occ_w + (ba >> 2), 1u << (8 * (ba & 3)));
+        }
+        if (k != 2) {
+          const uint32_t bb = mbrick(a.m, d.acc[lane].pt0);
+          atomicAdd(occ_w + (bb >> 2), 1u << (8 * (bb & 3)));
+        }
+      }
+      if (lane < MG) {
+        const int s = slot - g + lane;
+        const int fit = d.stop ? 0 : fit_of(a, d.base);
+        auto& Gl = sh.gs[lane];
+        Gl.task = 0;
+        if (s < fit) {
+          Gl.task = 1;
+          Gl.i = s;
+        } else if (s >= eslot0 && s - eslot0 < d.nacc) {
+          Gl.task = 2;
+          Gl.k = s - eslot0;
+        }
+      }
+      cp_async_wait();
+    }
+    __syncthreads();
+    pc.mark(1);
+    const Dec& d = sh.d;
+    if (G.task == 2) energy_update<T>(a, sh, ws, occ_s, r, g, gt, gw, lane, bar_id);
+    if (d.stop) break;
+    if (G.task == 1) {
+      const int lw = g % (kGW < 4 ? kGW : 4);  // leader warp (groups on different sub-partitions)
+      const uint64_t mv = d.base + (uint64_t)G.i;
+      const Proposal& pr = sh.ring[mv % kRing];
+      const int kind = pr.kind;
+      uint64_t* rw = a.res + (size_t)(r & 1) * kResWords * a.nslots + slot;
+      SlotExt* ex = a.ext + (size_t)(r & 1) * a.nslots + slot;
+      // per-lane candidate state (leader warp only)
+      const int dd = lane - kHalf;
+      const int64_t nd = (int64_t)d.n + dd;
+      const bool valid = kind == 1 ? nd >= 0 : nd >= 1;  // kinds 0/2 at N <= 0: counted rejection
+      uint64_t pid = 0;
+      double xox = 0.0, xoy = 0.0, xoz = 0.0, eu = 0.0, ew = 0.0;
+      int ocb = 0, ob = 0;
+      bool cf = false;
+      if (gw == lw) {
+        // candidate particles: one L2 hop for x_pid and e[pid], issued first
+        if (kind != 1 && valid) {
+          pid = index_from(pr.pick, (uint64_t)nd);
+          const double* op = reinterpret_cast<const double*>(a.s.pos + pid);
+          xox = __ldcg(op);
+          xoy = __ldcg(op + 1);
+          xoz = __ldcg(op + 2);
+          const double2 e2 = __ldcg(a.ep + pid);
+          eu = e2.x;
+          ew = e2.y;
+        }
+        int nent = 0;
+        if (kind != 2) {
+          if (pr.wmask != kNoMask) nent = window_bricks_mask(a.m, pr.wmask, pr.bpt, ws.brick, lane);
+          else nent = win_add<T>(a.m, a.b, ws, 0, pr.x, pr.y, pr.z, lane);
+          // a window brick changed by an in-flight commit of round r-1: read after it
+          const uint64_t pn = pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z);
+          bool near = false;
+          if (lane < d.nacc) near = mnear(a.m, pn, d.acc[lane].pt0) || mnear(a.m, pn, d.acc[lane].pt1);
+          if (__any_sync(0xffffffffu, near)) {
+            if (lane == 0)
+              while (ld_acquire(a.flags) < (uint64_t)(r - 1)) nap();
+            __syncwarp();
+          }
+          if (lane == 0) {
+            const uint32_t bb = mbrick(a.m, pn);
+            ob = occ_s ? (int)occ_s[bb] : __ldcg(a.m.occ + bb);
+            if (grid) ocb = __ldcg(a.g.occ + (pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z)));
+          }
+          win_finish<T>(a.m, ws, occ_s, nent, nent, lane);
+        }
+        if (lane == 0) {
+          G.kind = kind;
+          ws.excl = -1;
+          ws.nwin = 1;
+          ws.sign1 = 1;
+          ws.cx[0] = pr.x;
+          ws.cy[0] = pr.y;
+          ws.cz[0] = pr.z;
+          if (kind == 2) ws.total = 0;
+        }
+        // the particle's e / position vs the previous round's in-flight commits
+        if (kind != 1 && valid) {
+          const uint64_t po = mpoint(a.m, xox, xoy, xoz);
+          for (int k = 0; k < d.nacc; ++k) {
+            const AccE& A = d.acc[k];
+            if ((int64_t)pid == A.ia || (int64_t)pid == A.ib) {
+              cf = true;
+            } else if (mnear(a.m, po, A.pt0) || mnear(a.m, po, A.pt1)) {
+              const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + k;
+              while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
+              const int ak = (int)__ldcg(&t->kind);
+              if (ak != 2 && within_rc(a.b, xox, xoy, xoz, __ldcg(&t->nx), __ldcg(&t->ny), __ldcg(&t->nz))) cf = true;
+              if (ak != 1 && within_rc(a.b, xox, xoy, xoz, __ldcg(&t->ox), __ldcg(&t->oy), __ldcg(&t->oz))) cf = true;
+            }
+          }
+        }
+      }
+      group_sync(bar_id, T);
+      pc.mark(2);
+      // ---- S(n): the whole group
+      double su = 0.0, sw = 0.0;
+      if (kind != 2) win_sums<T>(a.m, a.b, ws, gt, su, sw);
+      group_reduce<T>(ws, su, sw, bar_id, gt, 32 * lw);
+      pc.mark(3);
+      if (gw == lw) {
+        su = __shfl_sync(0xffffffffu, su, 0);
+        sw = __shfl_sync(0xffffffffu, sw, 0);
+        double du = 0.0, dw = 0.0, mu_ = 0.0, mw = 0.0, p = 0.0;
+        bool slow = false;
+        if (valid) {
+          if (kind == 1) {
+            du = su;
+            dw = sw;
+            mu_ = su;
+            mw = sw;
+          } else if (kind == 0) {
+            const double r2 = min_image_dist2(pr.x, pr.y, pr.z, xox, xoy, xoz, a.b);
+            double tu = 0.0, tw = 0.0;
+            if (r2 <= a.b.rc2) lj_pair_clamped(r2, a.b, tu, tw);
+            slow = fabs(tu) > kHugeTerm || fabs(tw) > kHugeTerm;
+            mu_ = __dsub_rn(su, tu);
+            mw = __dsub_rn(sw, tw);
+          } else {
+            du = -eu;
+            dw = -ew;
+          }
+        }
+        // rare: the mover's own pair is large -> S(n) without pid, re-summed (warp, fixed order)
+        unsigned sl = __ballot_sync(0xffffffffu, slow);
+        while (sl) {
+          const int src = __ffs(sl) - 1;
+          sl &= sl - 1;
+          const int64_t xp = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)pid, src);
+          double au = 0.0, aw = 0.0;
+          for (int f = lane; f < ws.total; f += 32) {
+            int e, k;
+            if (f < kCandMax) {
+              const int c = ws.cand[f];
+              e = c >> 7;
+              k = c & 127;
+            } else {
+              int lo = 0, hi = ws.nent - 1;
+              while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (ws.pre[mid] <= f) lo = mid; else hi = mid - 1;
+              }
+              e = lo;
+              k = f - ws.pre[lo];
+            }
+            const int idx = (int)ws.brick[e] * a.m.cap + k;
+            if ((int64_t)__ldcg(a.m.rid + idx) == xp) continue;
+            const double r2 = min_image_dist2(pr.x, pr.y, pr.z, __ldcg(a.m.rx + idx),
+                                              __ldcg(a.m.ry + idx), __ldcg(a.m.rz + idx), a.b);
+            if (r2 <= a.b.rc2) lj_accum(a.b, r2, 1.0, au, aw);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            au = __dadd_rn(au, __shfl_xor_sync(0xffffffffu, au, o));
+            aw = __dadd_rn(aw, __shfl_xor_sync(0xffffffffu, aw, o));
+          }
+          if (lane == src) {
+            mu_ = au;
+            mw = aw;
+          }
+        }
+        if (valid) {
+          if (kind == 0) {
+            du = __dsub_rn(mu_, eu);
+            dw = __dsub_rn(mw, ew);
+            p = displacement_acceptance(du, a.beta);
+          } else if (kind == 1) {
+            p = insertion_acceptance(du, (uint64_t)nd, a.vol, a.beta, a.mu, a.lambda3);
+          } else {
+            p = deletion_acceptance(du, (uint64_t)nd, a.vol, a.beta, a.mu, a.lambda3);
+          }
+        }
+        const bool acc = valid && pr.acc < p;
+        // overflow of the commit (exact: occupancies after the previous round)
+        ob = __shfl_sync(0xffffffffu, ob, 0);
+        ocb = __shfl_sync(0xffffffffu, ocb, 0);
+        bool ovf = false;
+        if (valid && kind != 2) {
+          const uint32_t bb = mbrick(a.m, pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z));
+          const bool same_b = kind == 0 && mbrick(a.m, mpoint(a.m, xox, xoy, xoz)) == bb;
+          if (!same_b && ob >= a.m.cap) ovf = true;
+          if (grid) {
+            const int cb = pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z);
+            const bool same_c = kind == 0 && cell_of(a.g, xox, xoy, xoz) == cb;
+            if (!same_c && ocb >= a.g.cap) ovf = true;
+          }
+        }
+        const uint32_t accm = __ballot_sync(0xffffffffu, acc);
+        const uint32_t cfm = __ballot_sync(0xffffffffu, cf);
+        const uint32_t ovm = __ballot_sync(0xffffffffu, ovf);
+        if (lane < kResWords) {
+          const uint64_t pw = lane == 0 ? ((uint64_t)kind | ((uint64_t)accm << 8))
+                                        : (lane == 1 ? (uint64_t)cfm : (uint64_t)ovm);
+          st_relaxed(rw + (size_t)lane * a.nslots, tagw(r, pw));
+        }
+        pc.mark(4);
+        // payload for commits / statistics / trace (off the critical path)
+        if (acc || tracing) {
+          OffRec o;
+          o.du = du;
+          o.dw = dw;
+          o.su = mu_;
+          o.sw = mw;
+          o.pe = valid ? p : 0.0;
+          o.pad = 0.0;
+          ex->off[lane] = o;
+          __threadfence();
+        }
+        __syncwarp();
+        if (lane == 0) {
+          fence_gpu();
+          st_relaxed(&ex->tag, (uint64_t)r);
+        }
+      }
+    }
+    // ring refill (off the critical path)
+    if (tid < 32) {
+      const uint64_t want = d.base + kRing < a.nmoves ? d.base + kRing : a.nmoves;
+      if (want > ring_hi) {
+        ring_fill(a, sh.ring, ring_hi, want, lane);
+        ring_hi = want;
+      }
+    }
+    pc.mark(5);
+  }
+  if (a.prof && blockIdx.x == 1 && tid == 0) pc.flush(a.prof + 16);
+}
+
+// =================================================================== sequencer
+struct Round {  // a decided round, handed to the helper warps
+  uint64_t base, n;
+  uint32_t r;
+  int len, nacc, par;
+  int acc_i[kMaxAcc], acc_d[kMaxAcc], acc_kind[kMaxAcc];
+  int64_t acc_ia[kMaxAcc];
+  double acc_nx[kMaxAcc], acc_ny[kMaxAcc], acc_nz[kMaxAcc];
+  int res_d[kMaxMoves];
+  uint8_t kind[kMaxMoves];
+};
+
+enum Stop { kStopEnd, kStopRange, kStopPrev, kStopVerify, kStopFull, kStopOverflow, kNStop };
+
+struct SeqShared {
+  Proposal ring[kRing];
+  uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
+  uint8_t mkind[kMaxMoves];
+  int len, nacc, err, cmin, why;
+  int acc_i[kMaxAcc], acc_d[kMaxAcc];
+  int res_d[kMaxMoves];
+  // read / write sets of the consumed moves (verify)
+  double xo[kMaxMoves][3];
+  uint32_t pto[kMaxMoves], ptn[kMaxMoves];
+  int32_t co[kMaxMoves], cn[kMaxMoves];
+  int64_t ia[kMaxMoves], ib[kMaxMoves];
+  Round done;
+  double acc_du[kMaxAcc], acc_dw[kMaxAcc];
+  double st_e[kMaxAcc + 1], st_w[kMaxAcc + 1];
+  uint64_t st_n[kMaxAcc + 1];
+  double st_v[kMaxAcc + 1][4];
+  unsigned long long stops[kNStop];
+  uint64_t dw[kDecWords];
+  int dneed;
+  ChainState ks;
+};
+
+struct Observables {
+  double rep_u, pres;
+};
+
+// reported_energy() and pressure() (engine.hpp:277-291) with the tail terms
+// of tail_corrections() (potential.hpp:63-72), same operation order.
+__device__ __forceinline__ Observables observables(const EngineArgs& a, uint64_t n, double u,
+                                                   double w) {
+  const double rho = __ddiv_rn((double)n, a.vol);
+  double p = __dadd_rn(__dmul_rn(rho, a.temp), __ddiv_rn(w, __dmul_rn(3.0, a.vol)));
+  double ru = u;
+  if (a.tail) {
+    const double tu = __dmul_rn(
+        __dmul_rn(__dmul_rn(__dmul_rn(a.tail_cu, rho), a.b.eps), a.tail_s3), a.tail_bu);
+    const double tp = __dmul_rn(
+        __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(a.tail_cp, rho), rho), a.b.eps), a.tail_s3),
+        a.tail_bp);
+    p = __dadd_rn(p, tp);
+    ru = __dadd_rn(ru, __dmul_rn((double)n, tu));
+  }
+  return {ru, p};
+}
+
+// Does consumed move i read anything accepted move j (earlier in the round)
+// changed? Index overlap, the target brick / cell of i (overflow test), or a
+// changed position within r_c of a point i read (its new point's window, its
+// particle's e). Brick proximity filters, exact distances decide.
+__device__ __forceinline__ bool conflict(const EngineArgs& a, const SeqShared& sh, int i, int j) {
+  const int64_t la = sh.ia[i], lb = sh.ib[i], aa = sh.ia[j], ab = sh.ib[j];
+  if (la >= 0 && (la == aa || la == ab)) return true;
+  if (lb >= 0 && (lb == aa || lb == ab)) return true;
+  const bool grid = a.g.kind != GCMC_ALL_PAIRS;
+  const uint64_t ln = sh.ptn[i], an = sh.ptn[j], ao = sh.pto[j];
+  if (ln != kNoPoint) {
+    if (ao != kNoPoint && (mbrick(a.m, ln) == mbrick(a.m, ao) || (grid && sh.cn[i] == sh.co[j]))) return true;
+    if (an != kNoPoint && (ln == an || (grid && sh.cn[i] == sh.cn[j]))) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ bool conflict_xyz(const EngineArgs& a, const SeqShared& sh,
+                                             const Proposal& pi, const Proposal& pj, int i, int j) {
+  const uint64_t ln = sh.ptn[i], lo = sh.pto[i], an = sh.ptn[j], ao = sh.pto[j];
+  // i's points: new (window) and old (its particle); j's changed points: old, new
+  if (ln != kNoPoint) {
+    if (ao != kNoPoint && mnear(a.m, ln, ao) &&
+        within_rc(a.b, pi.x, pi.y, pi.z, sh.xo[j][0], sh.xo[j][1], sh.xo[j][2])) return true;
+    if (an != kNoPoint && mnear(a.m, ln, an) && within_rc(a.b, pi.x, pi.y, pi.z, pj.x, pj.y, pj.z))
+      return true;
+  }
+  if (lo != kNoPoint) {
+    if (ao != kNoPoint && mnear(a.m, lo, ao) &&
+        within_rc(a.b, sh.xo[i][0], sh.xo[i][1], sh.xo[i][2], sh.xo[j][0], sh.xo[j][1], sh.xo[j][2]))
+      return true;
+    if (an != kNoPoint && mnear(a.m, lo, an) &&
+        within_rc(a.b, sh.xo[i][0], sh.xo[i][1], sh.xo[i][2], pj.x, pj.y, pj.z)) return true;
+  }
+  return false;
+}
+
+// All changed points of accepted moves i and j more than 2 r_c apart.
+__device__ __forceinline__ bool far_apart(const EngineArgs& a, const SeqShared& sh,
+                                          const Proposal& pi, const Proposal& pj, int i, int j) {
+  double p[2][3], q[2][3];
+  int np = 0, nq = 0;
+  if (sh.ptn[i] != kNoPoint) { p[np][0] = pi.x; p[np][1] = pi.y; p[np][2] = pi.z; ++np; }
+  if (sh.pto[i] != kNoPoint) { p[np][0] = sh.xo[i][0]; p[np][1] = sh.xo[i][1]; p[np][2] = sh.xo[i][2]; ++np; }
+  if (sh.ptn[j] != kNoPoint) { q[nq][0] = pj.x; q[nq][1] = pj.y; q[nq][2] = pj.z; ++nq; }
+  if (sh.pto[j] != kNoPoint) { q[nq][0] = sh.xo[j][0]; q[nq][1] = sh.xo[j][1]; q[nq][2] = sh.xo[j][2]; ++nq; }
+  const double lim = __dmul_rn(4.0, a.b.rc2) * (1.0 + 1e-9);
+  for (int x = 0; x < np; ++x)
+    for (int y = 0; y < nq; ++y)
+      if (min_image_dist2(p[x][0], p[x][1], p[x][2], q[y][0], q[y][1], q[y][2], a.b) <= lim) return false;
+  return true;
+}
+
+__device__ __forceinline__ void compose_dec(uint32_t r, uint64_t base, uint64_t n, int nacc,
+                                            int stop, SeqShared& sh, int lane) {
+  for (int idx = lane; idx < kDecHdr + kDecEnt * nacc; idx += 32) {
+    uint64_t p = 0;
+    if (idx == 0) p = base;
+    else if (idx == 1) p = n;
+    else if (idx == 2) p = (uint64_t)nacc | ((uint64_t)stop << 9);
+    else if (idx >= kDecHdr) {
+      const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
+      const int i = sh.acc_i[e];
+      const int kind = sh.mkind[i];
+      if (f == 0) p = (uint64_t)(sh.ptn[i] & kNoPoint) | ((uint64_t)(sh.pto[i] & kNoPoint) << 24);
+      else if (f == 1) p = ((uint64_t)kind << 32) | (uint64_t)(uint32_t)sh.ia[i];
+      else p = sh.ib[i] < 0 ? 0xffffffffull : (uint64_t)(uint32_t)sh.ib[i];
+    }
+    sh.dw[idx] = tagw(r, p);
+  }
+  if (lane == 0) sh.dneed = kDecHdr + kDecEnt * nacc;
+}
+
+// Helper warps (kPollWarps .. 15): commits, statistics and trace of the round
+// in sh.done, while the poll warps wait for the next round.
+__device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) {
+  const Round& D = sh.done;
+  if (D.len == 0) return;
+  auto ext_of = [&](int s) -> const SlotExt* {
+    const SlotExt* ex = a.ext + (size_t)D.par * a.nslots + s;
+    while (ld_acquire(&ex->tag) != (uint64_t)D.r) nap();
+    return ex;
+  };
+  if (warp == kPollWarps) {  // structural commits (commit.cuh) + the movers' e
+    const bool mine = lane < D.nacc;
+    MoveData md{};
+    CommitIn c{};
+    Touch t{};
+    int kind = 0;
+    uint64_t pid = 0, nn = 0;
+    double esu = 0.0, esw = 0.0;
+    if (mine) {
+      kind = D.acc_kind[lane];
+      nn = (uint64_t)((int64_t)D.n + D.acc_d[lane]);
+      pid = kind == 1 ? 0 : (uint64_t)D.acc_ia[lane];
+      md.nx = D.acc_nx[lane];
+      md.ny = D.acc_ny[lane];
+      md.nz = D.acc_nz[lane];
+      md.rslot_pid = md.bslot_pid = -1;
+      load_move(a.s, kind, pid, md);
+      if (kind != 2) {
+        const OffRec& o = ext_of(D.acc_i[lane])->off[D.acc_d[lane] + kHalf];
+        esu = o.su;
+        esw = o.sw;
+      }
+      commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
+      t = touch_of(a.m, kind, pid, nn, c);
+    }
+    bool dep = false;
+    for (int j = 0; j < D.nacc - 1; ++j) {
+      Touch tj;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        tj.cell[x] = __shfl_sync(0xffffffffu, t.cell[x], j);
+        tj.brick[x] = __shfl_sync(0xffffffffu, t.brick[x], j);
+      }
+#pragma unroll
+      for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, t.part[x], j);
+      if (mine && j < lane && touches(t, tj)) dep = true;
+    }
+    auto set_e = [&]() {
+      if (kind == 0) a.ep[pid] = make_double2(esu, esw);
+      else if (kind == 1) a.ep[nn] = make_double2(esu, esw);
+      else if (pid != nn - 1) a.ep[pid] = __ldcg(a.ep + (nn - 1));
+    };
+    long long e1, e2, e3;
+    if (mine && !dep) {
+      commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+      set_e();
+    }
+    const unsigned deps = __ballot_sync(0xffffffffu, dep);
+    if (deps) {
+      __threadfence();
+      __syncwarp();
+      for (int j = 0; j < D.nacc; ++j) {
+        if (((deps >> j) & 1u) && lane == j) {
+          load_move(a.s, kind, pid, md);
+          commit_move(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, e1, e2, e3);
+          set_e();
+        }
+        __threadfence();
+        __syncwarp();
+      }
+    }
+    if (mine) __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(a.flags, (uint64_t)D.r);
+  } else if (warp == kPollWarps + 1) {  // statistics (engine.hpp:293-308, 413-426)
+    const int len = D.len, nacc = D.nacc;
+    ChainState& ks = sh.ks;
+    if (lane < nacc) {
+      const OffRec& o = ext_of(D.acc_i[lane])->off[D.acc_d[lane] + kHalf];
+      sh.acc_du[lane] = o.du;
+      sh.acc_dw[lane] = o.dw;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double energy = ks.energy, virial = ks.virial;
+      uint64_t cur = D.n;
+      sh.st_e[0] = energy;
+      sh.st_w[0] = virial;
+      sh.st_n[0] = cur;
+      for (int k = 0; k < nacc; ++k) {
+        energy = __dadd_rn(energy, sh.acc_du[k]);
+        virial = __dadd_rn(virial, sh.acc_dw[k]);
+        const int kind = D.acc_kind[k];
+        ++ks.accepted[kind];
+        cur = kind == 1 ? cur + 1 : (kind == 2 ? cur - 1 : cur);
+        sh.st_e[k + 1] = energy;
+        sh.st_w[k + 1] = virial;
+        sh.st_n[k + 1] = cur;
+      }
+      ks.energy = energy;
+      ks.virial = virial;
+    }
+    __syncwarp();
+    for (int k = lane; k <= nacc; k += 32) {
+      const uint64_t cur = sh.st_n[k];
+      const Observables ob = observables(a, cur, sh.st_e[k], sh.st_w[k]);
+      const double nd = (double)cur;
+      sh.st_v[k][0] = nd;
+      sh.st_v[k][1] = __dmul_rn(nd, nd);
+      sh.st_v[k][2] = ob.rep_u;
+      sh.st_v[k][3] = ob.pres;
+    }
+    const uint64_t step0 = ks.step;
+    unsigned smp[kMH];
+    unsigned att0 = 0, att1 = 0, att2 = 0;
+#pragma unroll
+    for (int h = 0; h < kMH; ++h) {
+      const int i = lane + 32 * h;
+      const bool in = i < len;
+      const int kind = in ? D.kind[i] : 3;
+      att0 += __popc(__ballot_sync(0xffffffffu, kind == 0));
+      att1 += __popc(__ballot_sync(0xffffffffu, kind == 1));
+      att2 += __popc(__ballot_sync(0xffffffffu, kind == 2));
+      const uint64_t st = step0 + (uint64_t)i + 1;
+      const bool sm = in && st > a.equil && (a.interval == 1 || (st - a.equil) % a.interval == 0);
+      smp[h] = __ballot_sync(0xffffffffu, sm);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double sn = ks.sum_n, sn2 = ks.sum_n2, su = ks.sum_u, sp = ks.sum_p;
+      uint64_t samples = 0;
+      int lo = 0;
+      for (int k = 0; k <= nacc; ++k) {
+        const int hi = k < nacc ? D.acc_i[k] : len;
+        int c = 0;
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) {
+          const int a0 = lo - 32 * h, a1 = hi - 32 * h;
+          const unsigned m_hi = a1 >= 32 ? 0xffffffffu : (a1 <= 0 ? 0u : (1u << a1) - 1u);
+          const unsigned m_lo = a0 >= 32 ? 0xffffffffu : (a0 <= 0 ? 0u : (1u << a0) - 1u);
+          c += __popc(smp[h] & m_hi & ~m_lo);
+        }
+        const double v0 = sh.st_v[k][0], v1 = sh.st_v[k][1], v2 = sh.st_v[k][2], v3 = sh.st_v[k][3];
+        for (int j = 0; j < c; ++j) {
+          sn = __dadd_rn(sn, v0);
+          sn2 = __dadd_rn(sn2, v1);
+          su = __dadd_rn(su, v2);
+          sp = __dadd_rn(sp, v3);
+        }
+        samples += (uint64_t)c;
+        lo = hi;
+      }
+      ks.attempted[0] += att0;
+      ks.attempted[1] += att1;
+      ks.attempted[2] += att2;
+      ks.step = step0 + (uint64_t)len;
+      ks.samples += samples;
+      ks.sum_n = sn;
+      ks.sum_n2 = sn2;
+      ks.sum_u = su;
+      ks.sum_p = sp;
+    }
+  } else if (a.trace) {  // trace records (MoveOutcome, engine.hpp:104-110)
+    const int nt = (kThreads / 32 - kPollWarps - 2) * 32;
+    for (int i = (warp - kPollWarps - 2) * 32 + lane; i < D.len; i += nt) {
+      const OffRec& o = ext_of(i)->off[D.res_d[i] + kHalf];
+      int accepted = 0, dn = 0;
+      for (int k = 0; k < D.nacc; ++k) {
+        if (D.acc_i[k] == i) accepted = 1;
+        if (D.acc_i[k] <= i) dn += D.acc_kind[k] == 1 ? 1 : (D.acc_kind[k] == 2 ? -1 : 0);
+      }
+      gcmc_trace_rec t;
+      t.kind = D.kind[i];
+      t.accepted = accepted;
+      t.delta_u = o.du;
+      t.delta_w = o.dw;
+      t.acceptance_prob = o.pe;
+      t.n_after = (uint64_t)((int64_t)D.n + dn);
+      a.trace[D.base + i] = t;
+    }
+  }
+}
+
+__device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
+  auto& sh = *reinterpret_cast<SeqShared*>(smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool grid = a.g.kind != GCMC_ALL_PAIRS;
+  constexpr int kPollThreads = kPollWarps * 32;
+  if (tid == 0) {
+    sh.ks = *a.st;
+    sh.done.len = 0;
+    sh.err = 0;
+    for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
+  }
+  uint64_t ring_hi = a.nmoves < (uint64_t)kRing ? a.nmoves : (uint64_t)kRing;
+  if (warp == 0) {
+    ring_fill(a, sh.ring, 0, ring_hi, lane);
+    cp_async_wait();
+  }
+  __syncthreads();
+  uint64_t base = 0, n = sh.ks.n;
+  uint64_t rounds = 0, etarget = 0;  // energy updates expected through the previous round
+  int fit = fit_of(a, 0);
+  uint32_t r = 1;
+  if (warp == 0) {
+    sh.nacc = 0;
+    compose_dec(r, base, n, 0, 0, sh, lane);
+  }
+  __syncthreads();
+  if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
+  PhaseClock pc;
+  pc.start(a.prof && tid == 0);
+  for (;;) {
+    const int par = (int)(r & 1);
+    if (warp < kPollWarps) {
+      // -------------------- poll: slot words -> per-move masks
+      for (int sl = tid; sl < fit; sl += kPollThreads) {
+        const uint64_t* rw = a.res + (size_t)par * kResWords * a.nslots + sl;
+        uint64_t w[kResWords];
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int j = 0; j < kResWords; ++j) {
+            w[j] = ld_relaxed(rw + (size_t)j * a.nslots);
+            ok &= tagged(w[j], r);
+          }
+          if (ok) break;
+          __nanosleep(a.poll_ns);
+        }
+        sh.mkind[sl] = (uint8_t)(w[0] & 3);
+        sh.macc[sl] = (uint32_t)((w[0] & kPay) >> 8);
+        sh.mcf[sl] = (uint32_t)w[1];
+        sh.movf[sl] = (uint32_t)w[2];
+      }
+      group_sync(1, kPollThreads);
+      pc.mark(1);
+      if (warp == 0) {  // ---- walk: bit j of a mask <-> N offset d = j - 16
+        uint32_t accm[kMH], stopm[kMH], ovfm[kMH];
+        unsigned kins[kMH], kdel[kMH];
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) {
+          const int i = lane + 32 * h;
+          const bool in = i < fit;
+          const int kd = in ? sh.mkind[i] : 0;
+          accm[h] = in ? sh.macc[i] : 0u;
+          stopm[h] = in ? sh.mcf[i] : 0xffffffffu;
+          ovfm[h] = in ? sh.movf[i] : 0u;
+          kins[h] = __ballot_sync(0xffffffffu, in && kd == 1);
+          kdel[h] = __ballot_sync(0xffffffffu, in && kd == 2);
+        }
+        int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
+        int di[kMH];
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) di[h] = 0;
+        int acc_e = -1, acc_dd = 0;
+        int h0 = 0;
+        for (;;) {
+          const int j = d + kHalf;
+          const bool inr = j >= 0 && j < 32;
+          int e = -1, eh = 0;
+          bool est = false, eov = false, ecf = false;
+#pragma unroll
+          for (int h = 0; h < kMH; ++h) {
+            if (h < h0 || e >= 0) continue;
+            const int i = lane + 32 * h;
+            const bool act = i >= start && i < fit;
+            const bool st = act && (!inr || ((stopm[h] >> j) & 1u));
+            const bool ac = act && inr && ((accm[h] >> j) & 1u);
+            const unsigned bmask = __ballot_sync(0xffffffffu, st || ac);
+            if (bmask) {
+              const int el = __ffs(bmask) - 1;
+              e = 32 * h + el;
+              eh = h;
+              const unsigned bit = 1u << el;
+              est = (__ballot_sync(0xffffffffu, st) & bit) != 0;
+              eov = (__ballot_sync(0xffffffffu, ac && ((ovfm[h] >> j) & 1u)) & bit) != 0;
+              ecf = inr;
+            } else {
+              h0 = h + 1;
+            }
+          }
+          if (e < 0) {
+            len = fit;
+            why = kStopEnd;
+            break;
+          }
+          if (est) {
+            len = e;
+            why = ecf ? kStopPrev : kStopRange;
+            break;
+          }
+          if (eov) {
+            len = e;
+            err = 1;
+            why = kStopOverflow;
+            break;
+          }
+          if (lane == nacc) {
+            acc_e = e;
+            acc_dd = d;
+          }
+          ++nacc;
+          const unsigned bit = 1u << (e & 31);
+          int delta = 0;
+#pragma unroll
+          for (int h = 0; h < kMH; ++h)
+            if (h == eh) delta = (kins[h] & bit) ? 1 : ((kdel[h] & bit) ? -1 : 0);
+#pragma unroll
+          for (int h = 0; h < kMH; ++h)
+            if (lane + 32 * h > e) di[h] += delta;
+          d += delta;
+          start = e + 1;
+          h0 = start >> 5;
+          if (nacc == kMaxAcc) {
+            len = e + 1;
+            why = kStopFull;
+            break;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < kMH; ++h) {
+          const int i = lane + 32 * h;
+          if (i < fit) sh.res_d[i] = di[h];
+        }
+        if (lane < nacc) {
+          sh.acc_i[lane] = acc_e;
+          sh.acc_d[lane] = acc_dd;
+        }
+        if (err && lane == 0) sh.res_d[len] = d;
+        if (lane == 0) {
+          sh.len = len;
+          sh.nacc = nacc;
+          sh.cmin = len;
+          sh.err = err;
+          sh.why = why;
+        }
+      }
+      group_sync(1, kPollThreads);
+      pc.mark(2);
+      {  // ---- read / write sets of the consumed moves (one L2 hop for x_pid)
+        const int len = sh.len + sh.err;  // the overflowing move's data is reported too
+        for (int i = tid; i < len; i += kPollThreads) {
+          const Proposal& pr = sh.ring[(base + i) % kRing];
+          const int kind = sh.mkind[i];
+          const int64_t nd = (int64_t)n + sh.res_d[i];
+          sh.ptn[i] = (uint32_t)(kind != 2 ? (pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z)) : kNoPoint);
+          sh.cn[i] = (kind != 2 && grid) ? (pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z)) : -1;
+          sh.pto[i] = (uint32_t)kNoPoint;
+          sh.co[i] = -1;
+          sh.ia[i] = -1;
+          sh.ib[i] = -1;
+          if (kind == 1) {
+            sh.ia[i] = nd;
+          } else if (nd >= 1) {
+            const uint64_t pid = index_from(pr.pick, (uint64_t)nd);
+            const double4 o = ld_cg(a.s.pos + pid);
+            sh.xo[i][0] = o.x;
+            sh.xo[i][1] = o.y;
+            sh.xo[i][2] = o.z;
+            sh.pto[i] = (uint32_t)mpoint(a.m, o.x, o.y, o.z);
+            sh.co[i] = grid ? cell_of(a.g, o.x, o.y, o.z) : -1;
+            sh.ia[i] = (int64_t)pid;
+            sh.ib[i] = kind == 2 ? nd - 1 : -1;
+          }
+        }
+      }
+      group_sync(1, kPollThreads);
+      {  // ---- verify: every consumed move against the accepted moves before it
+        const int len = sh.len, nacc = sh.nacc;
+        for (int q = tid; q < len * nacc; q += kPollThreads) {
+          const int i = q / nacc, k = q % nacc;
+          const int j = sh.acc_i[k];
+          if (i <= j) continue;
+          if (conflict(a, sh, i, j) ||
+              conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j))
+            atomicMin(&sh.cmin, i);
+        }
+        // two accepted moves of a round update disjoint sets of neighbour
+        // energies (no changed points within 2 r_c), so every e_j sees its
+        // updates in chain order whatever the round boundaries: bitwise
+        // reproducible trajectories
+        for (int q = tid; q < nacc * nacc; q += kPollThreads) {
+          const int k1 = q / nacc, k2 = q % nacc;
+          if (k2 >= k1) continue;
+          const int i = sh.acc_i[k1], j = sh.acc_i[k2];
+          if (far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) continue;
+          atomicMin(&sh.cmin, i);
+        }
+      }
+      group_sync(1, kPollThreads);
+      pc.mark(3);
+      if (tid == 0 && sh.cmin < sh.len) {
+        const int c = sh.cmin;
+        sh.len = c;
+        int k = 0;
+        while (k < sh.nacc && sh.acc_i[k] < c) ++k;
+        sh.nacc = k;
+        sh.err = 0;
+        sh.why = kStopVerify;
+      }
+    } else {
+      helpers(a, sh, warp, lane);  // previous round, concurrently with the poll
+    }
+    __syncthreads();
+    pc.mark(4);
+    // -------------------- close the round
+    const int len = sh.len, nacc = sh.nacc;
+    int dn = 0;
+    for (int k = 0; k < nacc; ++k) {
+      const int kd = sh.mkind[sh.acc_i[k]];
+      dn += kd == 1 ? 1 : (kd == 2 ? -1 : 0);
+    }
+    const uint64_t nbase = base + (uint64_t)len;
+    const uint64_t nn = (uint64_t)((int64_t)n + dn);
+    const bool stop = nbase >= a.nmoves || sh.err;
+    if (warp == 0) {
+      compose_dec(r + 1, nbase, nn, nacc, stop, sh, lane);
+    } else if (warp == 1) {  // exact accepted moves for the evaluators' e tests / updates
+      if (lane < nacc) {
+        const int i = sh.acc_i[lane];
+        const Proposal& pr = sh.ring[(base + i) % kRing];
+        ATab* t = a.atab + (size_t)par * kMaxAcc + lane;
+        const int kind = sh.mkind[i];
+        t->ox = kind != 1 ? sh.xo[i][0] : 0.0;
+        t->oy = kind != 1 ? sh.xo[i][1] : 0.0;
+        t->oz = kind != 1 ? sh.xo[i][2] : 0.0;
+        t->nx = pr.x;
+        t->ny = pr.y;
+        t->nz = pr.z;
+        t->ia = sh.ia[i];
+        t->ib = sh.ib[i];
+        t->kind = kind;
+        st_release(&t->tag, (uint64_t)r);
+      }
+    } else if (warp >= 2 && warp < 2 + kMaxMoves / 32) {  // hand the round to the helpers
+      Round& D = sh.done;
+      const int i = tid - 64;
+      if (i < len) {
+        D.res_d[i] = sh.res_d[i];
+        D.kind[i] = sh.mkind[i];
+      }
+      if (i < nacc) {
+        const int m = sh.acc_i[i];
+        const Proposal& pr = sh.ring[(base + m) % kRing];
+        D.acc_i[i] = m;
+        D.acc_d[i] = sh.acc_d[i];
+        D.acc_kind[i] = sh.mkind[m];
+        D.acc_ia[i] = sh.ia[m];
+        D.acc_nx[i] = pr.x;
+        D.acc_ny[i] = pr.y;
+        D.acc_nz[i] = pr.z;
+      }
+      if (i == 0) {
+        D.base = base;
+        D.n = n;
+        D.r = r;
+        D.len = len;
+        D.nacc = nacc;
+        D.par = par;
+        ++sh.stops[sh.why];
+      }
+    }
+    // the previous round's energy updates must land before D_{r+1}
+    if (tid == 32 * 15)
+      while (ld_acquire(a.flags + 8) < etarget) __nanosleep(a.poll_ns);
+    __syncthreads();
+    if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
+    etarget += (uint64_t)nacc;
+    pc.mark(5);
+    // next round's ring (while the evaluators work)
+    if (warp == 0) {
+      const uint64_t want = nbase + kRing < a.nmoves ? nbase + kRing : a.nmoves;
+      if (want > ring_hi) {
+        ring_fill(a, sh.ring, ring_hi, want, lane);
+        ring_hi = want;
+      }
+      cp_async_wait();
+    }
+    fit = fit_of(a, nbase);
+    __syncthreads();
+    base = nbase;
+    n = nn;
+    ++rounds;
+    ++r;
+    if (stop) break;
+  }
+  // the last round's commits / statistics / trace
+  if (warp >= kPollWarps) helpers(a, sh, warp, lane);
+  __syncthreads();
+  if (a.prof && tid == 0) {
+    pc.flush(a.prof);
+    a.prof[15] = rounds;
+    for (int k = 0; k < kNStop; ++k) a.prof[40 + k] = sh.stops[k];
+  }
+  if (tid == 0) {
+    ChainState& ks = sh.ks;
+    a.st->n = n;
+    a.st->step = ks.step;
+    a.st->energy = ks.energy;
+    a.st->virial = ks.virial;
+    for (int k = 0; k < 3; ++k) {
+      a.st->attempted[k] = ks.attempted[k];
+      a.st->accepted[k] = ks.accepted[k];
+    }
+    a.st->samples = ks.samples;
+    a.st->sum_u = ks.sum_u;
+    a.st->sum_p = ks.sum_p;
+    a.st->sum_n = ks.sum_n;
+    a.st->sum_n2 = ks.sum_n2;
+    a.st->moves_done = base;
+    a.st->rounds = rounds;
+    if (sh.err) {  // overflow at move `base` (relative index len of the last round)
+      const int i = sh.len;
+      const int kind = sh.mkind[i];
+      const uint32_t bb = mbrick(a.m, sh.ptn[i]);
+      const int ob = __ldcg(a.m.occ + bb);
+      bool ref = false;
+      int cb = -1, ocb = 0;
+      if (grid) {
+        cb = sh.cn[i];
+        ocb = __ldcg(a.g.occ + cb);
+        const bool same_c = kind == 0 && sh.co[i] == cb;
+        ref = !same_c && ocb >= a.g.cap;
+      }
+      a.st->error = GCMC_CELL_OVERFLOW;
+      a.st->err_a = ref ? cb : (int64_t)bb;
+      a.st->err_b = ref ? ocb : ob;
+      a.st->err_c = ref ? 0 : 1;
+    }
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(kThreads, 1) k_engine2(EngineArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (blockIdx.x == 0)
+    sequencer(a, smem);
+  else
+    evaluator<T>(a, smem);
+}
+
+// e[i] from scratch: one thread per particle over its 3x3x3 brick window
+// (plain sequential sums, deterministic).
+__global__ void __launch_bounds__(256) k_epart(Mirror m, Box b, const double4* __restrict__ pos,
+                                              uint64_t n, double2* out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 x = ld_cg(pos + i);
+  const int self = bslot_in(x);
+  double su = 0.0, sw = 0.0;
+  auto brick = [&](uint32_t id) {
+    const int occ = __ldcg(m.occ + id);
+    for (int k = 0; k < occ; ++k) {
+      const int idx = (int)id * m.cap + k;
+      if (idx == self) continue;
+      const double r2 = min_image_dist2(x.x, x.y, x.z, __ldcg(m.rx + idx), __ldcg(m.ry + idx),
+                                        __ldcg(m.rz + idx), b);
+      if (r2 <= b.rc2) lj_accum(b, r2, 1.0, su, sw);
+    }
+  };
+  if (m.dims < 3) {
+    for (uint32_t id = 0; id < m.nb; ++id) brick(id);
+  } else {
+    const int d = m.dims;
+    const int bx = mcoord(m, x.x), by = mcoord(m, x.y), bz = mcoord(m, x.z);
+    for (int oz = -1; oz <= 1; ++oz)
+      for (int oy = -1; oy <= 1; ++oy)
+        for (int ox = -1; ox <= 1; ++ox) {
+          const int cx = (bx + ox + d) % d, cy = (by + oy + d) % d, cz = (bz + oz + d) % d;
+          brick((uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz));
+        }
+  }
+  out[i] = make_double2(su, sw);
+}
+
+// max |a - b| over both components (non-negative doubles order as their bits)
+__global__ void k_ediff(const double2* a, const double2* b, uint64_t n, unsigned long long* out) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 x = a[i], y = b[i];
+  atomicMax(out, (unsigned long long)__double_as_longlong(fabs(x.x - y.x)));
+  atomicMax(out + 1, (unsigned long long)__double_as_longlong(fabs(x.y - y.y)));
+}
+
+}  // namespace
+
+bool engine2_supported(const Chain& c) {
+  if (c.params.engine_mode == 1) return false;
+  if (std::getenv("GCMC_ENGINE_V1")) return false;
+  if (c.grid.kind == GCMC_ALL_PAIRS || c.params.max_displacement > 0.0) return false;
+  const int mg = kThreads / c.engine_group;
+  return (c.engine_ctas - 1) * mg > kMaxAcc && (c.engine_ctas - 1) * mg <= kMaxSlots;
+}
+
+gcmc_status epart_build(Chain& c, double2* out) {
+  const uint64_t n = c.st_host->n;
+  if (n) {
+    k_epart<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.mirror, c.box, c.pos, n, out);
+    cudaError_t e = cudaGetLastError();
+    if (e) return cuda_error(e, "epart");
+  }
+  return GCMC_OK;
+}
+
+gcmc_status epart_drift(Chain& c, double* du, double* dw) {
+  *du = *dw = 0.0;
+  const uint64_t n = c.st_host->n;
+  if (!c.e_valid || n == 0) return GCMC_OK;
+  double2* fresh = nullptr;
+  unsigned long long* out = nullptr;
+  cudaError_t e = cudaMalloc(&fresh, n * sizeof(double2));
+  if (!e) e = cudaMalloc(&out, 2 * sizeof(unsigned long long));
+  if (e) return cuda_error(e, "epart drift");
+  gcmc_status s = epart_build(c, fresh);
+  if (!s) {
+    cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), c.stream);
+    k_ediff<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(fresh, c.ep, n, out);
+    unsigned long long h[2];
+    e = cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, c.stream);
+    if (!e) e = cudaStreamSynchronize(c.stream);
+    if (e) s = cuda_error(e, "epart drift");
+    *du = __builtin_bit_cast(double, h[0]);
+    *dw = __builtin_bit_cast(double, h[1]);
+  }
+  cudaFree(fresh);
+  cudaFree(out);
+  return s;
+}
+
+gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaStream_t s) {
+  if (nmoves == 0) return GCMC_OK;
+  const gcmc_params& P = c.params;
+  cudaError_t e;
+  if (!c.e_valid) {
+    gcmc_status st = epart_build(c, c.ep);
+    if (st) return st;
+    c.e_valid = true;
+  }
+  const int T = c.engine_group;
+  const int MG = kThreads / T;
+  const int G = c.engine_ctas;
+  EngineArgs a{};
+  a.g = c.grid;
+  a.m = c.mirror;
+  a.b = c.box;
+  a.s = Store{c.pos, c.rslot};
+  a.ep = c.ep;
+  a.st = c.st;
+  a.props = c.props;
+  a.trace = trace_d;
+  a.nmoves = nmoves;
+  a.beta = 1.0 / P.temperature;  // config.hpp:66
+  a.mu = P.chemical_potential;
+  a.lambda3 = P.lambda * P.lambda * P.lambda;
+  a.vol = P.box_length * P.box_length * P.box_length;  // box.hpp:19
+  a.temp = P.temperature;
+  a.equil = P.equilibration_steps;
+  a.interval = P.sampling_interval;
+  a.tail = P.tail_corrections;
+  a.prof = c.prof;
+  {
+    const double sg = P.sigma, rc = P.r_cut;
+    const double sr3 = (sg / rc) * (sg / rc) * (sg / rc);
+    const double sr9 = sr3 * sr3 * sr3;
+    const double pi = 3.141592653589793238462643383279502884;
+    a.tail_cu = (8.0 / 3.0) * pi;
+    a.tail_cp = (16.0 / 3.0) * pi;
+    a.tail_s3 = sg * sg * sg;
+    a.tail_bu = sr9 / 3.0 - sr3;
+    a.tail_bp = 2.0 / 3.0 * sr9 - sr3;
+  }
+  a.nslots = (G - 1) * MG;
+  a.fitmax = a.nslots - kMaxAcc < kMaxMoves ? a.nslots - kMaxAcc : kMaxMoves;
+  {
+    const char* f = std::getenv("GCMC_FITMAX");
+    if (f && std::atoi(f) > 0 && std::atoi(f) < a.fitmax) a.fitmax = std::atoi(f);
+  }
+  if (!c.eng2_buf) {
+    const size_t bytes = kDecStride * 8 + 2 * (size_t)kMaxSlots * kResWords * 8 +
+                         2 * (size_t)kMaxSlots * sizeof(SlotExt) + 2 * kMaxAcc * sizeof(ATab) + 16 * 8;
+    if ((e = cudaMalloc(&c.eng2_buf, bytes))) return cuda_error(e, "alloc engine2");
+    c.eng2_bytes = bytes;
+  }
+  char* p = static_cast<char*>(c.eng2_buf);
+  a.dec = reinterpret_cast<uint64_t*>(p);
+  p += kDecStride * 8;
+  a.res = reinterpret_cast<uint64_t*>(p);
+  p += 2 * (size_t)kMaxSlots * kResWords * 8;
+  a.ext = reinterpret_cast<SlotExt*>(p);
+  p += 2 * (size_t)kMaxSlots * sizeof(SlotExt);
+  a.atab = reinterpret_cast<ATab*>(p);
+  p += 2 * kMaxAcc * sizeof(ATab);
+  a.flags = reinterpret_cast<uint64_t*>(p);
+  {
+    const char* e1 = std::getenv("GCMC_POLL_NS");
+    a.poll_ns = e1 ? (unsigned)std::atoi(e1) : 64u;
+    const char* e2 = std::getenv("GCMC_EPOLL_NS");
+    a.epoll_ns = e2 ? (unsigned)std::atoi(e2) : 64u;
+  }
+  size_t eval_bytes = T == 128 ? sizeof(EvalShared<128>) : (T == 256 ? sizeof(EvalShared<256>) : sizeof(EvalShared<512>));
+  eval_bytes = (eval_bytes + 15) & ~size_t(15);
+  size_t smem = eval_bytes + ((c.mirror.nb + 15) & ~15u);
+  a.smem_occ = 1;
+  int max_optin = 0;
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
+  if (smem > (size_t)max_optin) {
+    a.smem_occ = 0;
+    smem = eval_bytes;
+  }
+  if (smem < sizeof(SeqShared)) smem = sizeof(SeqShared);
+  if (a.prof)
+    std::fprintf(stderr, "[engine2 prof] smem=%zu eval=%zu seq=%zu occ_replica=%d slots=%d fit=%d\n", smem,
+                 eval_bytes, sizeof(SeqShared), a.smem_occ, a.nslots, a.fitmax);
+  void (*kern)(EngineArgs) = T == 128 ? k_engine2<128> : (T == 256 ? k_engine2<256> : k_engine2<512>);
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+    return cuda_error(e, "engine2 smem");
+  if ((e = cudaMemsetAsync(c.eng2_buf, 0, c.eng2_bytes, s))) return cuda_error(e, "engine2");
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kThreads), args, smem, s);
+  if (e) return cuda_error(e, "engine2 launch");
+  return GCMC_OK;
+}
+
+}  // namespace gcmcb

@@ -234,6 +234,7 @@ std::string overflow_message(const Chain& c, int64_t cell, int64_t occ) {
 
 gcmc_status mirror_build(Chain& c) {
   const uint64_t n = c.st_host->n;
+  c.e_valid = false;
   cudaStream_t s = c.stream;
   int* flag = c.iscratch;
   cudaError_t e;
@@ -366,6 +367,7 @@ gcmc_status grid_check(Chain& c, std::string* issue) {
 
 gcmc_status commit_one(Chain& c, int kind, uint64_t pid, const double* p, uint64_t* new_pid) {
   const uint64_t n = c.st_host->n;
+  c.e_valid = false;  // rebuilt before the next maintained-energy engine run
   CommitArgs a{kind, pid, n, p ? p[0] : 0.0, p ? p[1] : 0.0, p ? p[2] : 0.0};
   long long* out = reinterpret_cast<long long*>(c.dscratch);
   k_commit_one<<<1, 1, 0, c.stream>>>(c.grid, c.mirror, Store{c.pos, c.rslot}, c.st, a,

@@ -55,6 +55,11 @@ struct Chain {
   uint64_t* eng_res = nullptr;
   void* eng_ext = nullptr;
   bool built = false;
+  // maintained per-particle pair energy / virial (engine2.cu)
+  double2* ep = nullptr;         // [capn]
+  bool e_valid = false;
+  void* eng2_buf = nullptr;
+  size_t eng2_bytes = 0;
   unsigned long long* prof = nullptr;
   unsigned long long* stamp = nullptr;  // per-round global timestamps (GCMC_ENGINE_LATENCY=1)
 };
@@ -84,6 +89,12 @@ gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n
 gcmc_status engine_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
 size_t engine_buffer_bytes(int nslots, size_t* dec, size_t* res, size_t* ext);
 int engine_max_slots();
+
+// engine2.cu: maintained-energy engine (one slot per move)
+bool engine2_supported(const Chain& c);
+gcmc_status engine2_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
+gcmc_status epart_build(Chain& c, double2* out);
+gcmc_status epart_drift(Chain& c, double* du, double* dw);
 
 // Error text in the reference's wording.
 std::string overflow_message(const Chain& c, int64_t cell, int64_t occ);

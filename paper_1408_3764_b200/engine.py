@@ -181,7 +181,7 @@ def random_initial_configuration(n: int, box_length: float, min_sep: float, seed
 
 
 def _params(cfg: RunConfig, engine_ctas=0, engine_group=0, engine_variants=0, engine_bias=0,
-            max_particles=0) -> L.GcmcParams:
+            max_particles=0, engine_mode=0) -> L.GcmcParams:
     return L.GcmcParams(
         box_length=cfg.box_length, epsilon=cfg.epsilon, sigma=cfg.sigma, r_cut=cfg.r_cut,
         temperature=cfg.temperature, chemical_potential=cfg.chemical_potential,
@@ -191,7 +191,7 @@ def _params(cfg: RunConfig, engine_ctas=0, engine_group=0, engine_variants=0, en
         cell_capacity=cfg.cell_capacity, microcell_capacity=cfg.microcell_capacity,
         tail_corrections=int(cfg.tail_corrections), max_particles=max_particles,
         engine_ctas=engine_ctas, engine_group=engine_group, engine_variants=engine_variants,
-        engine_bias=engine_bias)
+        engine_bias=engine_bias, engine_mode=engine_mode)
 
 
 class _Device:
@@ -259,6 +259,13 @@ class _Device:
     def total_energy(self):
         u, w = C.c_double(), C.c_double()
         L.check(self.lib.gcmc_total_energy(self.h, C.byref(u), C.byref(w)))
+        return u.value, w.value
+
+    def energy_drift(self):
+        """Largest |maintained - fresh| per-particle pair energy / virial
+        (gcmc_energy_drift; 0, 0 when the per-window engine ran last)."""
+        u, w = C.c_double(), C.c_double()
+        L.check(self.lib.gcmc_energy_drift(self.h, C.byref(u), C.byref(w)))
         return u.value, w.value
 
     def rebuild_check(self) -> Optional[str]:

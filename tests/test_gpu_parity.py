@@ -342,6 +342,32 @@ def test_first_1e5_moves_identical(strategy, mu):
     assert abs(st.sum_u - rs.sum_u) <= 1e-9 * max(1.0, abs(rs.sum_u))
 
 
+def test_maintained_energies_do_not_drift():
+    """The maintained-energy engine's per-particle e_i stay equal (to rounding)
+    to a from-scratch evaluation after many accepted moves."""
+    sim, tr, o, tp = run_pair("microcell", 32768, 200000, 1.0)
+    assert_trace_parity(tr, tp)
+    du, dw = sim.dev.energy_drift()
+    assert du <= 1e-11 and dw <= 1e-10, (du, dw)
+    assert int(tr["accepted"].sum()) > 1000
+
+
+def test_per_window_engine_still_identical():
+    """engine_mode=1 forces the per-window engine (engine.cu) on a strategy the
+    maintained-energy engine also supports: same decisions."""
+    box, xyz, rng = config(2048)
+    from paper_1408_3764_b200.config import RunConfig
+
+    cfg = RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box, strategy="microcell")
+    a = E().Simulation(cfg, xyz, rng)
+    b = E().Simulation(cfg, xyz, rng, engine_mode=1)
+    ta, tb = a.run(50000, trace=True), b.run(50000, trace=True)
+    assert np.array_equal(ta["accepted"], tb["accepted"])
+    assert np.array_equal(ta["n_after"], tb["n_after"])
+    assert rel(ta["delta_u"], tb["delta_u"]).max() <= TOL
+    assert b.dev.energy_drift() == (0.0, 0.0)
+
+
 def test_all_pairs_trajectory_identical():
     sim, tr, o, tp = run_pair("all_pairs", 1024, 5000, -2.0)
     assert_trace_parity(tr, tp)
