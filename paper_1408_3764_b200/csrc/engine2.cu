@@ -66,7 +66,8 @@ constexpr int kDecStride = 128;
 constexpr int kResWords = 3;
 constexpr int kPollWarps = 12;
 constexpr int kMaxSlots = 768;            // buffer sizing: evaluator groups
-constexpr double kHugeTerm = 1e4;         // |pair(n, x_pid)| above this: re-sum without pid
+constexpr double kHugeTerm = 1e4;
+constexpr int kBitWords = 4096;          // verify bitmap: up to 131072 bricks         // |pair(n, x_pid)| above this: re-sum without pid
 
 struct OffRec {  // one candidate N offset of a slot (accepted offsets; all when tracing)
   double du, dw;  // ΔU, ΔW
@@ -245,6 +246,7 @@ __device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& 
     if (kind != 1) nent = win_add<T>(a.m, a.b, ws, nent, ox, oy, oz, lane);
     if (kind == 2) nent0 = nent;
     win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
+    (void)ia;
     if (lane == 0) {
       G.kind = kind;
       G.nx = kind == 2 ? ox : nx;
@@ -255,14 +257,22 @@ __device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& 
       G.oz = oz;
       G.sgn0 = kind == 2 ? -1 : 1;
       G.sgn1 = -1;
-      G.excl = kind == 2 ? -1 : ia;  // displaced particle / inserted index: not its own neighbour
     }
   }
   group_sync(bar_id, T);
   const int total = ws.total;
   const double c0x = G.nx, c0y = G.ny, c0z = G.nz, c1x = G.ox, c1y = G.oy, c1z = G.oz;
   const double s0 = (double)G.sgn0, s1 = (double)G.sgn1;
-  const int64_t excl = G.excl;
+  // the mover's own record (displace / insert) is the one at exactly its new
+  // position, whatever id a later relabel of the round gave it
+  const bool excl = G.kind != 2;
+  // a displacement's two windows may share neighbours: the old window's
+  // updates land before the new window's (fixed order -> reproducible bits)
+  for (int pass = 0; pass < 2; ++pass) {
+  if (pass == 1) {
+    __threadfence();
+    group_sync(bar_id, T);
+  }
   for (int f = gt; f < total; f += T) {
     int e, k;
     if (f < kCandMax) {
@@ -278,11 +288,12 @@ __device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& 
       e = lo;
       k = f - ws.pre[lo];
     }
+    const bool w1 = e >= ws.nent0;
+    if ((pass == 0) != (w1 || G.kind == 2)) continue;
     const int idx = (int)ws.brick[e] * a.m.cap + k;
     const int32_t rid = __ldcg(a.m.rid + idx);
-    if ((int64_t)rid == excl) continue;
     const double rx = __ldcg(a.m.rx + idx), ry = __ldcg(a.m.ry + idx), rz = __ldcg(a.m.rz + idx);
-    const bool w1 = e >= ws.nent0;
+    if (excl && rx == c0x && ry == c0y && rz == c0z) continue;
     const double r2 = w1 ? min_image_dist2(c1x, c1y, c1z, rx, ry, rz, a.b)
                          : min_image_dist2(c0x, c0y, c0z, rx, ry, rz, a.b);
     if (r2 <= a.b.rc2) {
@@ -292,6 +303,7 @@ __device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& 
       atomicAdd(&a.ep[rid].x, __dmul_rn(sg, u));
       atomicAdd(&a.ep[rid].y, __dmul_rn(sg, w));
     }
+  }
   }
   __threadfence();
   group_sync(bar_id, T);
@@ -603,6 +615,7 @@ struct SeqShared {
   uint64_t st_n[kMaxAcc + 1];
   double st_v[kMaxAcc + 1][4];
   unsigned long long stops[kNStop];
+  uint32_t nbits[kBitWords];  // verify: bricks near a changed point of the round
   uint64_t dw[kDecWords];
   int dneed;
   ChainState ks;
@@ -636,9 +649,10 @@ __device__ __forceinline__ Observables observables(const EngineArgs& a, uint64_t
 // changed position within r_c of a point i read (its new point's window, its
 // particle's e). Brick proximity filters, exact distances decide.
 __device__ __forceinline__ bool conflict(const EngineArgs& a, const SeqShared& sh, int i, int j) {
-  const int64_t la = sh.ia[i], lb = sh.ib[i], aa = sh.ia[j], ab = sh.ib[j];
+  // i reads its particle's position and e (displace / delete); j wrote its
+  // particle (insert: the new index; delete: pid and the last index)
+  const int64_t la = sh.mkind[i] != 1 ? sh.ia[i] : -1, aa = sh.ia[j], ab = sh.ib[j];
   if (la >= 0 && (la == aa || la == ab)) return true;
-  if (lb >= 0 && (lb == aa || lb == ab)) return true;
   const bool grid = a.g.kind != GCMC_ALL_PAIRS;
   const uint64_t ln = sh.ptn[i], an = sh.ptn[j], ao = sh.pto[j];
   if (ln != kNoPoint) {
@@ -666,6 +680,19 @@ __device__ __forceinline__ bool conflict_xyz(const EngineArgs& a, const SeqShare
         within_rc(a.b, sh.xo[i][0], sh.xo[i][1], sh.xo[i][2], pj.x, pj.y, pj.z)) return true;
   }
   return false;
+}
+
+// Brick at window offset o (0..26) of a packed brick point (dims >= 3).
+__device__ __forceinline__ uint32_t nbr_brick(const Mirror& m, uint32_t pt, int o) {
+  const int d = m.dims;
+  int cx = pt_x(pt) + o % 3 - 1, cy = pt_y(pt) + (o / 3) % 3 - 1, cz = pt_z(pt) + o / 9 - 1;
+  cx += cx < 0 ? d : 0;
+  cx -= cx >= d ? d : 0;
+  cy += cy < 0 ? d : 0;
+  cy -= cy >= d ? d : 0;
+  cz += cz < 0 ? d : 0;
+  cz -= cz >= d ? d : 0;
+  return (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
 }
 
 // All changed points of accepted moves i and j more than 2 r_c apart.
@@ -892,6 +919,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool grid = a.g.kind != GCMC_ALL_PAIRS;
   constexpr int kPollThreads = kPollWarps * 32;
+  for (int q = tid; q < kBitWords; q += kThreads) sh.nbits[q] = 0u;
   if (tid == 0) {
     sh.ks = *a.st;
     sh.done.len = 0;
@@ -1071,15 +1099,51 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         }
       }
       group_sync(1, kPollThreads);
-      {  // ---- verify: every consumed move against the accepted moves before it
+      pc.mark(6);  // read / write sets
+      // ---- verify: every consumed move against the accepted moves before it.
+      // A brick bitmap (bricks within reach 1 of a changed point) filters the
+      // spatial tests; index / target-cell tests are a few compares per pair.
+      const bool bm = a.m.nb <= (uint32_t)kBitWords * 32u && a.m.dims >= 3;
+      {
+        const int nacc = sh.nacc;
+        if (bm)
+          for (int q = tid; q < nacc * 54; q += kPollThreads) {
+            const int k = q / 54, rem = q % 54;
+            const int i = sh.acc_i[k];
+            const uint32_t pt = rem >= 27 ? sh.pto[i] : sh.ptn[i];
+            if (pt == (uint32_t)kNoPoint) continue;
+            const uint32_t id = nbr_brick(a.m, pt, rem % 27);
+            atomicOr(&sh.nbits[id >> 5], 1u << (id & 31));
+          }
+      }
+      group_sync(1, kPollThreads);
+      {
         const int len = sh.len, nacc = sh.nacc;
-        for (int q = tid; q < len * nacc; q += kPollThreads) {
-          const int i = q / nacc, k = q % nacc;
-          const int j = sh.acc_i[k];
-          if (i <= j) continue;
-          if (conflict(a, sh, i, j) ||
-              conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j))
-            atomicMin(&sh.cmin, i);
+        const int first = nacc ? sh.acc_i[0] : len;
+        for (int i = first + 1 + tid; i < len; i += kPollThreads) {
+          bool c = false;
+          int kk = 0;
+          for (; kk < nacc && sh.acc_i[kk] < i; ++kk)
+            if (conflict(a, sh, i, sh.acc_i[kk])) c = true;
+          if (!c) {
+            bool hit = !bm;
+            if (bm) {
+              if (sh.ptn[i] != (uint32_t)kNoPoint) {
+                const uint32_t id = mbrick(a.m, sh.ptn[i]);
+                hit |= (sh.nbits[id >> 5] >> (id & 31)) & 1u;
+              }
+              if (sh.pto[i] != (uint32_t)kNoPoint) {
+                const uint32_t id = mbrick(a.m, sh.pto[i]);
+                hit |= (sh.nbits[id >> 5] >> (id & 31)) & 1u;
+              }
+            }
+            if (hit) {
+              const Proposal& pi = sh.ring[(base + i) % kRing];
+              for (int k = 0; k < kk && !c; ++k)
+                c = conflict_xyz(a, sh, pi, sh.ring[(base + sh.acc_i[k]) % kRing], i, sh.acc_i[k]);
+            }
+          }
+          if (c) atomicMin(&sh.cmin, i);
         }
         // two accepted moves of a round update disjoint sets of neighbour
         // energies (no changed points within 2 r_c), so every e_j sees its
@@ -1091,6 +1155,17 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           const int i = sh.acc_i[k1], j = sh.acc_i[k2];
           if (far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) continue;
           atomicMin(&sh.cmin, i);
+        }
+      }
+      group_sync(1, kPollThreads);
+      if (bm) {  // clear the bitmap words this round set
+        const int nacc = sh.nacc;
+        for (int q = tid; q < nacc * 54; q += kPollThreads) {
+          const int k = q / 54, rem = q % 54;
+          const int i = sh.acc_i[k];
+          const uint32_t pt = rem >= 27 ? sh.pto[i] : sh.ptn[i];
+          if (pt == (uint32_t)kNoPoint) continue;
+          sh.nbits[nbr_brick(a.m, pt, rem % 27) >> 5] = 0u;
         }
       }
       group_sync(1, kPollThreads);
