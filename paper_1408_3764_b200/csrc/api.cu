@@ -681,6 +681,17 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
                    hp[33] / R);
       std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",
                    hp[40], hp[41], hp[42], hp[43], hp[44], hp[45]);
+      {
+        unsigned long long xp[80];
+        cudaMemcpy(xp, c.prof, sizeof xp, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "[engine prof] raw seq:");
+        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[k] / R);
+        std::fprintf(stderr, "\n[engine prof] raw eval:");
+        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[16 + k] / R);
+        const double ne = (double)(xp[68] ? xp[68] : 1);
+        std::fprintf(stderr, "\n[engine prof] e-update (per update, %llu): atab=%.0f sflag=%.0f setup=%.0f traverse=%.0f\n",
+                     xp[68], xp[64] / ne, xp[65] / ne, xp[66] / ne, xp[67] / ne);
+      }
       if (c.stamp) {
         std::vector<unsigned long long> st(8 * 8192);
         cudaMemcpy(st.data(), c.stamp, st.size() * 8, cudaMemcpyDeviceToHost);

@@ -224,14 +224,18 @@ struct EvalShared {
 // neighbours' e_j lose the pair with the old position and gain the pair with
 // the new one, on the committed state (after flags[0] >= r - 1).
 template <int T>
-__device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& ws, const uint8_t* occ_s,
+__device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& ws, const uint8_t* occ_s,
                               uint32_t r, int g, int gt, int gw, int lane, int bar_id) {
   auto& G = sh.gs[g];
+  PhaseClock ec;
+  ec.start(a.prof && G.k == 0 && gt == 0);
   if (gw == 0) {
     const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + G.k;
     if (lane == 0) {
       while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
+      ec.mark(0);
       while (ld_acquire(a.flags) < (uint64_t)(r - 1)) nap();
+      ec.mark(1);
     }
     __syncwarp();
     const int kind = (int)__ldcg(&t->kind);
@@ -260,6 +264,7 @@ __device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& 
     }
   }
   group_sync(bar_id, T);
+  ec.mark(2);
   const int total = ws.total;
   const double c0x = G.nx, c0y = G.ny, c0z = G.nz, c1x = G.ox, c1y = G.oy, c1z = G.oz;
   const double s0 = (double)G.sgn0, s1 = (double)G.sgn1;
@@ -308,6 +313,46 @@ __device__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& 
   __threadfence();
   group_sync(bar_id, T);
   if (gt == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + 8), 1ull);
+  ec.mark(3);
+  if (ec.on)
+    for (int q = 0; q < 4; ++q) atomicAdd(a.prof + 64 + q, ec.acc[q]);
+  if (ec.on) atomicAdd(a.prof + 68, 1ull);
+}
+
+// S(n) without particle xp, re-summed by one warp over the window's
+// candidates in a fixed order (used when pair(n, x_pid) is too large to
+// subtract without losing precision).
+template <int T>
+__device__ __noinline__ void resum_excl(const EngineArgs& a, const WinWs<T>& ws, double px, double py,
+                                        double pz, int64_t xp, int lane, double& au, double& aw) {
+  au = 0.0;
+  aw = 0.0;
+  for (int f = lane; f < ws.total; f += 32) {
+    int e, k;
+    if (f < kCandMax) {
+      const int c = ws.cand[f];
+      e = c >> 7;
+      k = c & 127;
+    } else {
+      int lo = 0, hi = ws.nent - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ws.pre[mid] <= f) lo = mid; else hi = mid - 1;
+      }
+      e = lo;
+      k = f - ws.pre[lo];
+    }
+    const int idx = (int)ws.brick[e] * a.m.cap + k;
+    if ((int64_t)__ldcg(a.m.rid + idx) == xp) continue;
+    const double r2 = min_image_dist2(px, py, pz, __ldcg(a.m.rx + idx), __ldcg(a.m.ry + idx),
+                                      __ldcg(a.m.rz + idx), a.b);
+    if (r2 <= a.b.rc2) lj_accum(a.b, r2, 1.0, au, aw);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    au = __dadd_rn(au, __shfl_xor_sync(0xffffffffu, au, o));
+    aw = __dadd_rn(aw, __shfl_xor_sync(0xffffffffu, aw, o));
+  }
 }
 
 template <int T>
@@ -402,6 +447,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           ew = e2.y;
         }
         int nent = 0;
+        pc.mark(6);
         if (kind != 2) {
           if (pr.wmask != kNoMask) nent = window_bricks_mask(a.m, pr.wmask, pr.bpt, ws.brick, lane);
           else nent = win_add<T>(a.m, a.b, ws, 0, pr.x, pr.y, pr.z, lane);
@@ -414,6 +460,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
               while (ld_acquire(a.flags) < (uint64_t)(r - 1)) nap();
             __syncwarp();
           }
+          pc.mark(7);
           if (lane == 0) {
             const uint32_t bb = mbrick(a.m, pn);
             ob = occ_s ? (int)occ_s[bb] : __ldcg(a.m.occ + bb);
@@ -431,6 +478,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           ws.cz[0] = pr.z;
           if (kind == 2) ws.total = 0;
         }
+        pc.mark(8);
         // the particle's e / position vs the previous round's in-flight commits
         if (kind != 1 && valid) {
           const uint64_t po = mpoint(a.m, xox, xoy, xoz);
@@ -448,6 +496,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           }
         }
       }
+      pc.mark(9);
       group_sync(bar_id, T);
       pc.mark(2);
       // ---- S(n): the whole group
@@ -484,48 +533,27 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const int src = __ffs(sl) - 1;
           sl &= sl - 1;
           const int64_t xp = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)pid, src);
-          double au = 0.0, aw = 0.0;
-          for (int f = lane; f < ws.total; f += 32) {
-            int e, k;
-            if (f < kCandMax) {
-              const int c = ws.cand[f];
-              e = c >> 7;
-              k = c & 127;
-            } else {
-              int lo = 0, hi = ws.nent - 1;
-              while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (ws.pre[mid] <= f) lo = mid; else hi = mid - 1;
-              }
-              e = lo;
-              k = f - ws.pre[lo];
-            }
-            const int idx = (int)ws.brick[e] * a.m.cap + k;
-            if ((int64_t)__ldcg(a.m.rid + idx) == xp) continue;
-            const double r2 = min_image_dist2(pr.x, pr.y, pr.z, __ldcg(a.m.rx + idx),
-                                              __ldcg(a.m.ry + idx), __ldcg(a.m.rz + idx), a.b);
-            if (r2 <= a.b.rc2) lj_accum(a.b, r2, 1.0, au, aw);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            au = __dadd_rn(au, __shfl_xor_sync(0xffffffffu, au, o));
-            aw = __dadd_rn(aw, __shfl_xor_sync(0xffffffffu, aw, o));
-          }
+          double au, aw;
+          resum_excl<T>(a, ws, pr.x, pr.y, pr.z, xp, lane, au, aw);
           if (lane == src) {
             mu_ = au;
             mw = aw;
           }
         }
-        if (valid) {
-          if (kind == 0) {
-            du = __dsub_rn(mu_, eu);
-            dw = __dsub_rn(mw, ew);
-            p = displacement_acceptance(du, a.beta);
-          } else if (kind == 1) {
-            p = insertion_acceptance(du, (uint64_t)nd, a.vol, a.beta, a.mu, a.lambda3);
-          } else {
-            p = deletion_acceptance(du, (uint64_t)nd, a.vol, a.beta, a.mu, a.lambda3);
-          }
+        if (kind == 0) {
+          du = __dsub_rn(mu_, eu);
+          dw = __dsub_rn(mw, ew);
+        }
+        {  // engine.hpp:28-59 with one exponential (same operation order)
+          const double x = kind == 0 ? __dmul_rn(-a.beta, du)
+                         : (kind == 1 ? __dmul_rn(a.beta, __dsub_rn(a.mu, du))
+                                      : __dmul_rn(-a.beta, __dadd_rn(a.mu, du)));
+          const double ex = exp(x);
+          const double nn = (double)nd;
+          if (valid)
+            p = metropolis(kind == 0 ? ex
+                           : (kind == 1 ? __dmul_rn(__ddiv_rn(a.vol, __dmul_rn(a.lambda3, __dadd_rn(nn, 1.0))), ex)
+                                        : __dmul_rn(__ddiv_rn(__dmul_rn(a.lambda3, nn), a.vol), ex)));
         }
         const bool acc = valid && pr.acc < p;
         // overflow of the commit (exact: occupancies after the previous round)
@@ -601,7 +629,7 @@ struct SeqShared {
   Proposal ring[kRing];
   uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
   uint8_t mkind[kMaxMoves];
-  int len, nacc, err, cmin, why;
+  int len, nacc, err, cmin, why, dend;
   int acc_i[kMaxAcc], acc_d[kMaxAcc];
   int res_d[kMaxMoves];
   // read / write sets of the consumed moves (verify)
@@ -616,6 +644,7 @@ struct SeqShared {
   double st_v[kMaxAcc + 1][4];
   unsigned long long stops[kNStop];
   uint32_t nbits[kBitWords];  // verify: bricks near a changed point of the round
+  unsigned smp[kMH];          // statistics: sampled steps of the round
   uint64_t dw[kDecWords];
   int dneed;
   ChainState ks;
@@ -627,7 +656,7 @@ struct Observables {
 
 // reported_energy() and pressure() (engine.hpp:277-291) with the tail terms
 // of tail_corrections() (potential.hpp:63-72), same operation order.
-__device__ __forceinline__ Observables observables(const EngineArgs& a, uint64_t n, double u,
+__device__ __noinline__ Observables observables(const EngineArgs& a, uint64_t n, double u,
                                                    double w) {
   const double rho = __ddiv_rn((double)n, a.vol);
   double p = __dadd_rn(__dmul_rn(rho, a.temp), __ddiv_rn(w, __dmul_rn(3.0, a.vol)));
@@ -662,7 +691,7 @@ __device__ __forceinline__ bool conflict(const EngineArgs& a, const SeqShared& s
   return false;
 }
 
-__device__ __forceinline__ bool conflict_xyz(const EngineArgs& a, const SeqShared& sh,
+__device__ __noinline__ bool conflict_xyz(const EngineArgs& a, const SeqShared& sh,
                                              const Proposal& pi, const Proposal& pj, int i, int j) {
   const uint64_t ln = sh.ptn[i], lo = sh.pto[i], an = sh.ptn[j], ao = sh.pto[j];
   // i's points: new (window) and old (its particle); j's changed points: old, new
@@ -696,7 +725,7 @@ __device__ __forceinline__ uint32_t nbr_brick(const Mirror& m, uint32_t pt, int 
 }
 
 // All changed points of accepted moves i and j more than 2 r_c apart.
-__device__ __forceinline__ bool far_apart(const EngineArgs& a, const SeqShared& sh,
+__device__ __noinline__ bool far_apart(const EngineArgs& a, const SeqShared& sh,
                                           const Proposal& pi, const Proposal& pj, int i, int j) {
   double p[2][3], q[2][3];
   int np = 0, nq = 0;
@@ -733,7 +762,7 @@ __device__ __forceinline__ void compose_dec(uint32_t r, uint64_t base, uint64_t 
 
 // Helper warps (kPollWarps .. 15): commits, statistics and trace of the round
 // in sh.done, while the poll warps wait for the next round.
-__device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) {
+__device__ __noinline__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) {
   const Round& D = sh.done;
   if (D.len == 0) return;
   auto ext_of = [&](int s) -> const SlotExt* {
@@ -765,8 +794,19 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
       }
       commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
       t = touch_of(a.m, kind, pid, nn, c);
+      if (kind == 2 && pid != nn - 1) {  // the relabelled particle's e (loaded before any store)
+        const double2 el = __ldcg(a.ep + (nn - 1));
+        esu = el.x;
+        esw = el.y;
+      }
     }
+    // Commits load everything first, so a later insertion that reuses the
+    // index an earlier deletion vacated (relabel) stores nothing the deletion
+    // loads: that pair needs no ordering. Any other overlap of cells, bricks
+    // or particles is applied in move order.
     bool dep = false;
+    unsigned exm = 0;  // earlier deletions this insertion was exempted against
+#pragma unroll 1
     for (int j = 0; j < D.nacc - 1; ++j) {
       Touch tj;
 #pragma unroll
@@ -776,12 +816,22 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
       }
 #pragma unroll
       for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, t.part[x], j);
-      if (mine && j < lane && touches(t, tj)) dep = true;
+      const int kj = __shfl_sync(0xffffffffu, kind, j);
+      if (mine && j < lane) {
+        Touch tm = t;
+        if (kind == 1 && kj == 2 && tm.part[0] == tj.part[1]) {
+          tm.part[0] = -1;
+          exm |= 1u << j;
+        }
+        if (touches(tm, tj)) dep = true;
+      }
     }
+    // ... unless that deletion is itself applied in order (it then loads late)
+    if (__ballot_sync(0xffffffffu, dep) & exm) dep = true;
     auto set_e = [&]() {
       if (kind == 0) a.ep[pid] = make_double2(esu, esw);
       else if (kind == 1) a.ep[nn] = make_double2(esu, esw);
-      else if (pid != nn - 1) a.ep[pid] = __ldcg(a.ep + (nn - 1));
+      else if (pid != nn - 1) a.ep[pid] = make_double2(esu, esw);
     };
     long long e1, e2, e3;
     if (mine && !dep) {
@@ -790,15 +840,19 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
     }
     const unsigned deps = __ballot_sync(0xffffffffu, dep);
     if (deps) {
-      __threadfence();
-      __syncwarp();
+      __syncwarp();  // same warp: stores before the barrier are visible to loads after it
+#pragma unroll 1
       for (int j = 0; j < D.nacc; ++j) {
         if (((deps >> j) & 1u) && lane == j) {
           load_move(a.s, kind, pid, md);
+          if (kind == 2 && pid != nn - 1) {
+            const double2 el = __ldcg(a.ep + (nn - 1));
+            esu = el.x;
+            esw = el.y;
+          }
           commit_move(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, e1, e2, e3);
           set_e();
         }
-        __threadfence();
         __syncwarp();
       }
     }
@@ -844,9 +898,9 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
       sh.st_v[k][3] = ob.pres;
     }
     const uint64_t step0 = ks.step;
-    unsigned smp[kMH];
+    unsigned* smp = sh.smp;
     unsigned att0 = 0, att1 = 0, att2 = 0;
-#pragma unroll
+#pragma unroll 1
     for (int h = 0; h < kMH; ++h) {
       const int i = lane + 32 * h;
       const bool in = i < len;
@@ -856,8 +910,10 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
       att2 += __popc(__ballot_sync(0xffffffffu, kind == 2));
       const uint64_t st = step0 + (uint64_t)i + 1;
       const bool sm = in && st > a.equil && (a.interval == 1 || (st - a.equil) % a.interval == 0);
-      smp[h] = __ballot_sync(0xffffffffu, sm);
+      const unsigned b = __ballot_sync(0xffffffffu, sm);
+      if (lane == 0) smp[h] = b;
     }
+    __syncwarp();
     __syncwarp();
     if (lane == 0) {
       double sn = ks.sum_n, sn2 = ks.sum_n2, su = ks.sum_u, sp = ks.sum_p;
@@ -866,7 +922,7 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
       for (int k = 0; k <= nacc; ++k) {
         const int hi = k < nacc ? D.acc_i[k] : len;
         int c = 0;
-#pragma unroll
+#pragma unroll 1
         for (int h = 0; h < kMH; ++h) {
           const int a0 = lo - 32 * h, a1 = hi - 32 * h;
           const unsigned m_hi = a1 >= 32 ? 0xffffffffu : (a1 <= 0 ? 0u : (1u << a1) - 1u);
@@ -898,6 +954,7 @@ __device__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) 
     for (int i = (warp - kPollWarps - 2) * 32 + lane; i < D.len; i += nt) {
       const OffRec& o = ext_of(i)->off[D.res_d[i] + kHalf];
       int accepted = 0, dn = 0;
+#pragma unroll 1
       for (int k = 0; k < D.nacc; ++k) {
         if (D.acc_i[k] == i) accepted = 1;
         if (D.acc_i[k] <= i) dn += D.acc_kind[k] == 1 ? 1 : (D.acc_kind[k] == 2 ? -1 : 0);
@@ -969,114 +1026,84 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       group_sync(1, kPollThreads);
       pc.mark(1);
       if (warp == 0) {  // ---- walk: bit j of a mask <-> N offset d = j - 16
-        uint32_t accm[kMH], stopm[kMH], ovfm[kMH];
-        unsigned kins[kMH], kdel[kMH];
-#pragma unroll
-        for (int h = 0; h < kMH; ++h) {
+        // Compact (I-cache friendly) scan: one ballot per 32 moves plus one
+        // per event (accept / stop); N changes only at accepted insertions /
+        // deletions, which are rare.
+        int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
+        const int nh = (fit + 31) >> 5;
+#pragma unroll 1
+        for (int h = 0; h < nh; ++h) {
           const int i = lane + 32 * h;
           const bool in = i < fit;
+          const uint32_t am = in ? sh.macc[i] : 0u, sm = in ? sh.mcf[i] : 0u, om = in ? sh.movf[i] : 0u;
           const int kd = in ? sh.mkind[i] : 0;
-          accm[h] = in ? sh.macc[i] : 0u;
-          stopm[h] = in ? sh.mcf[i] : 0xffffffffu;
-          ovfm[h] = in ? sh.movf[i] : 0u;
-          kins[h] = __ballot_sync(0xffffffffu, in && kd == 1);
-          kdel[h] = __ballot_sync(0xffffffffu, in && kd == 2);
-        }
-        int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
-        int di[kMH];
-#pragma unroll
-        for (int h = 0; h < kMH; ++h) di[h] = 0;
-        int acc_e = -1, acc_dd = 0;
-        int h0 = 0;
-        for (;;) {
-          const int j = d + kHalf;
-          const bool inr = j >= 0 && j < 32;
-          int e = -1, eh = 0;
-          bool est = false, eov = false, ecf = false;
-#pragma unroll
-          for (int h = 0; h < kMH; ++h) {
-            if (h < h0 || e >= 0) continue;
-            const int i = lane + 32 * h;
-            const bool act = i >= start && i < fit;
-            const bool st = act && (!inr || ((stopm[h] >> j) & 1u));
-            const bool ac = act && inr && ((accm[h] >> j) & 1u);
-            const unsigned bmask = __ballot_sync(0xffffffffu, st || ac);
-            if (bmask) {
-              const int el = __ffs(bmask) - 1;
-              e = 32 * h + el;
-              eh = h;
-              const unsigned bit = 1u << el;
-              est = (__ballot_sync(0xffffffffu, st) & bit) != 0;
-              eov = (__ballot_sync(0xffffffffu, ac && ((ovfm[h] >> j) & 1u)) & bit) != 0;
-              ecf = inr;
-            } else {
-              h0 = h + 1;
+          bool done = false;
+#pragma unroll 1
+          for (;;) {
+            const int j = d + kHalf;
+            const bool inr = j >= 0 && j < 32;
+            const bool act = in && i >= start;
+            const bool st = act && (!inr || ((sm >> (j & 31)) & 1u));
+            const bool ac = act && inr && ((am >> (j & 31)) & 1u);
+            const unsigned ev = __ballot_sync(0xffffffffu, st || ac);
+            if (!ev) break;
+            const int el = __ffs(ev) - 1;
+            const int e = 32 * h + el;
+            const unsigned info = __shfl_sync(0xffffffffu, (st ? 1u : 0u) | (((om >> (j & 31)) & 1u) << 1) | ((unsigned)kd << 2), el);
+            if (info & 1u) {
+              len = e;
+              why = inr ? kStopPrev : kStopRange;
+              done = true;
+              break;
+            }
+            if (info & 2u) {
+              len = e;
+              err = 1;
+              why = kStopOverflow;
+              done = true;
+              break;
+            }
+            if (lane == 0) {
+              sh.acc_i[nacc] = e;
+              sh.acc_d[nacc] = d;
+            }
+            ++nacc;
+            const int k = (int)(info >> 2);
+            d += k == 1 ? 1 : (k == 2 ? -1 : 0);
+            start = e + 1;
+            if (nacc == kMaxAcc) {
+              len = e + 1;
+              why = kStopFull;
+              done = true;
+              break;
             }
           }
-          if (e < 0) {
-            len = fit;
-            why = kStopEnd;
-            break;
-          }
-          if (est) {
-            len = e;
-            why = ecf ? kStopPrev : kStopRange;
-            break;
-          }
-          if (eov) {
-            len = e;
-            err = 1;
-            why = kStopOverflow;
-            break;
-          }
-          if (lane == nacc) {
-            acc_e = e;
-            acc_dd = d;
-          }
-          ++nacc;
-          const unsigned bit = 1u << (e & 31);
-          int delta = 0;
-#pragma unroll
-          for (int h = 0; h < kMH; ++h)
-            if (h == eh) delta = (kins[h] & bit) ? 1 : ((kdel[h] & bit) ? -1 : 0);
-#pragma unroll
-          for (int h = 0; h < kMH; ++h)
-            if (lane + 32 * h > e) di[h] += delta;
-          d += delta;
-          start = e + 1;
-          h0 = start >> 5;
-          if (nacc == kMaxAcc) {
-            len = e + 1;
-            why = kStopFull;
-            break;
-          }
+          if (done) break;
         }
-#pragma unroll
-        for (int h = 0; h < kMH; ++h) {
-          const int i = lane + 32 * h;
-          if (i < fit) sh.res_d[i] = di[h];
-        }
-        if (lane < nacc) {
-          sh.acc_i[lane] = acc_e;
-          sh.acc_d[lane] = acc_dd;
-        }
-        if (err && lane == 0) sh.res_d[len] = d;
         if (lane == 0) {
           sh.len = len;
           sh.nacc = nacc;
           sh.cmin = len;
           sh.err = err;
           sh.why = why;
+          sh.dend = d;
         }
       }
       group_sync(1, kPollThreads);
       pc.mark(2);
       {  // ---- read / write sets of the consumed moves (one L2 hop for x_pid)
         const int len = sh.len + sh.err;  // the overflowing move's data is reported too
+        const int nacc = sh.nacc;
         for (int i = tid; i < len; i += kPollThreads) {
           const Proposal& pr = sh.ring[(base + i) % kRing];
           const int kind = sh.mkind[i];
-          const int64_t nd = (int64_t)n + sh.res_d[i];
+          int di = 0;  // N offset before move i
+          for (int k = 0; k < nacc && sh.acc_i[k] < i; ++k) {
+            const int ak = sh.mkind[sh.acc_i[k]];
+            di += ak == 1 ? 1 : (ak == 2 ? -1 : 0);
+          }
+          sh.res_d[i] = di;
+          const int64_t nd = (int64_t)n + di;
           sh.ptn[i] = (uint32_t)(kind != 2 ? (pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z)) : kNoPoint);
           sh.cn[i] = (kind != 2 && grid) ? (pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z)) : -1;
           sh.pto[i] = (uint32_t)kNoPoint;
