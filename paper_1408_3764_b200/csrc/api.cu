@@ -689,7 +689,7 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
         std::fprintf(stderr, "\n[engine prof] raw eval:");
         for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[16 + k] / R);
         const double ne = (double)(xp[68] ? xp[68] : 1);
-        std::fprintf(stderr, "\n[engine prof] e-update (per update, %llu): atab=%.0f sflag=%.0f setup=%.0f traverse=%.0f\n",
+        std::fprintf(stderr, "\n[engine prof] commit task (per move, %llu): atab=%.0f commit=%.0f setup+waits=%.0f traverse=%.0f\n",
                      xp[68], xp[64] / ne, xp[65] / ne, xp[66] / ne, xp[67] / ne);
       }
       if (c.stamp) {

@@ -82,12 +82,18 @@ struct SlotExt {
 };
 static_assert(sizeof(SlotExt) % 32 == 0, "SlotExt layout");
 
-struct ATab {  // accepted move k of a round, exact (sequencer -> evaluators)
+struct ATab {  // accepted move k of a round, exact (sequencer -> commit groups / evaluators)
   double ox, oy, oz, nx, ny, nz;
   int64_t ia, ib;
-  int32_t kind, pad;
-  uint64_t tag;  // round (stored last, release)
+  uint64_t nn;     // store size before the move
+  int32_t kind, slot, d;
+  uint32_t deps;   // earlier accepted moves of the round this commit is ordered after
+  uint64_t tag;    // round (stored last, release)
 };
+// flags[]: [kECount] energy updates done (cumulative); [kSFlag + k] round whose
+// accepted move k has been committed (structural + the mover's e).
+constexpr int kECount = 8;
+constexpr int kSFlag = 16;
 
 struct EngineArgs {
   Grid g;
@@ -107,7 +113,7 @@ struct EngineArgs {
   uint64_t* res;    // [2][kResWords][nslots]
   SlotExt* ext;     // [2][nslots]
   ATab* atab;       // [2][kMaxAcc]
-  uint64_t* flags;  // [0] structural commits done through round; [8] energy updates done (count)
+  uint64_t* flags;  // see kECount / kSFlag
   int smem_occ;
   unsigned poll_ns, epoll_ns;
   unsigned long long* prof;
@@ -220,28 +226,73 @@ struct EvalShared {
   } gs[kThreads / T];
 };
 
-// Energy update of accepted move k of round r - 1 (group-wide): the
-// neighbours' e_j lose the pair with the old position and gain the pair with
-// the new one, on the committed state (after flags[0] >= r - 1).
+// The structural commit of one accepted move (one thread): store,
+// reference grid and brick mirror (commit.cuh) and the mover's e. Loads
+// first, then stores; ordered after the round's commits it overlaps (ATab
+// deps) by per-move flags.
+__device__ __noinline__ void structural_commit(const EngineArgs& a, const ATab* t, uint32_t rr, int k) {
+  const int kind = (int)__ldcg(&t->kind);
+  const uint64_t nn = __ldcg(&t->nn);
+  const uint64_t pid = kind == 1 ? 0 : (uint64_t)__ldcg(&t->ia);
+  uint32_t deps = __ldcg(&t->deps);
+  while (deps) {
+    const int j = __ffs(deps) - 1;
+    deps &= deps - 1;
+    while (ld_acquire(a.flags + kSFlag + j) != (uint64_t)rr) nap();
+  }
+  MoveData md{};
+  md.nx = __ldcg(&t->nx);
+  md.ny = __ldcg(&t->ny);
+  md.nz = __ldcg(&t->nz);
+  md.rslot_pid = md.bslot_pid = -1;
+  load_move(a.s, kind, pid, md);
+  double esu = 0.0, esw = 0.0;
+  if (kind != 2) {
+    const SlotExt* ex = a.ext + (size_t)(rr & 1) * a.nslots + __ldcg(&t->slot);
+    while (ld_acquire(&ex->tag) != (uint64_t)rr) nap();
+    const OffRec* o = &ex->off[__ldcg(&t->d) + kHalf];
+    esu = __ldcg(&o->su);
+    esw = __ldcg(&o->sw);
+  }
+  CommitIn c;
+  commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
+  if (kind == 2 && pid != nn - 1) {  // the relabelled particle's e
+    const double2 el = __ldcg(a.ep + (nn - 1));
+    esu = el.x;
+    esw = el.y;
+  }
+  long long e1, e2, e3;
+  commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+  if (kind == 0) __stcg(a.ep + pid, make_double2(esu, esw));
+  else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
+  else if (pid != nn - 1) __stcg(a.ep + pid, make_double2(esu, esw));
+  __threadfence();
+  st_release(a.flags + kSFlag + k, (uint64_t)rr);
+}
+
+// Commit task for accepted move k of round r - 1 (a reserved group): the
+// structural commit, then the energy update — the neighbours' e_j lose the
+// pair with the old position and gain the pair with the new one — once every
+// commit of the round whose bricks its windows read has landed.
 template <int T>
 __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& ws, const uint8_t* occ_s,
                               uint32_t r, int g, int gt, int gw, int lane, int bar_id) {
   auto& G = sh.gs[g];
+  const uint32_t rr = r - 1;
   PhaseClock ec;
   ec.start(a.prof && G.k == 0 && gt == 0);
   if (gw == 0) {
-    const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + G.k;
+    const ATab* t = a.atab + (size_t)(rr & 1) * kMaxAcc + G.k;
     if (lane == 0) {
-      while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
+      while (ld_acquire(&t->tag) != (uint64_t)rr) nap();
       ec.mark(0);
-      while (ld_acquire(a.flags) < (uint64_t)(r - 1)) nap();
+      structural_commit(a, t, rr, G.k);
       ec.mark(1);
     }
     __syncwarp();
     const int kind = (int)__ldcg(&t->kind);
     const double ox = __ldcg(&t->ox), oy = __ldcg(&t->oy), oz = __ldcg(&t->oz);
     const double nx = __ldcg(&t->nx), ny = __ldcg(&t->ny), nz = __ldcg(&t->nz);
-    const int64_t ia = __ldcg(&t->ia);
     int nent = 0, nent0 = 0;
     // window 0: new position (+), window 1: old position (-); a deletion has
     // only the old one (as window 0, sign -)
@@ -250,7 +301,16 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
     if (kind != 1) nent = win_add<T>(a.m, a.b, ws, nent, ox, oy, oz, lane);
     if (kind == 2) nent0 = nent;
     win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
-    (void)ia;
+    // the round's other commits whose bricks these windows read
+    const Dec& d = sh.d;
+    const AccE& me = d.acc[G.k];
+    bool wait = false;
+    if (lane < d.nacc && lane != G.k)
+      wait = mnear(a.m, me.pt0, d.acc[lane].pt0) || mnear(a.m, me.pt0, d.acc[lane].pt1) ||
+             mnear(a.m, me.pt1, d.acc[lane].pt0) || mnear(a.m, me.pt1, d.acc[lane].pt1);
+    if (wait)
+      while (ld_acquire(a.flags + kSFlag + lane) != (uint64_t)rr) nap();
+    __syncwarp();
     if (lane == 0) {
       G.kind = kind;
       G.nx = kind == 2 ? ox : nx;
@@ -312,7 +372,7 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
   }
   __threadfence();
   group_sync(bar_id, T);
-  if (gt == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + 8), 1ull);
+  if (gt == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + kECount), 1ull);
   ec.mark(3);
   if (ec.on)
     for (int q = 0; q < 4; ++q) atomicAdd(a.prof + 64 + q, ec.acc[q]);
@@ -455,11 +515,9 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const uint64_t pn = pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z);
           bool near = false;
           if (lane < d.nacc) near = mnear(a.m, pn, d.acc[lane].pt0) || mnear(a.m, pn, d.acc[lane].pt1);
-          if (__any_sync(0xffffffffu, near)) {
-            if (lane == 0)
-              while (ld_acquire(a.flags) < (uint64_t)(r - 1)) nap();
-            __syncwarp();
-          }
+          if (near)
+            while (ld_acquire(a.flags + kSFlag + lane) != (uint64_t)(r - 1)) nap();
+          __syncwarp();
           pc.mark(7);
           if (lane == 0) {
             const uint32_t bb = mbrick(a.m, pn);
@@ -645,6 +703,10 @@ struct SeqShared {
   unsigned long long stops[kNStop];
   uint32_t nbits[kBitWords];  // verify: bricks near a changed point of the round
   unsigned smp[kMH];          // statistics: sampled steps of the round
+  int8_t acck[kMaxMoves];     // accepted index of a consumed move (-1: rejected)
+  double xq[kMaxAcc][3];      // position of the particle a deletion relabels
+  int32_t tcl[kMaxAcc], tbl[kMaxAcc], tbar[kMaxAcc];
+  uint32_t deps[kMaxAcc];
   uint64_t dw[kDecWords];
   int dneed;
   ChainState ks;
@@ -711,6 +773,28 @@ __device__ __noinline__ bool conflict_xyz(const EngineArgs& a, const SeqShared& 
   return false;
 }
 
+// Do the commits of accepted moves k and j (j earlier) touch a common
+// reference cell, brick or particle index (commit.cuh Touch)?
+__device__ __noinline__ bool commits_overlap(const EngineArgs& a, const SeqShared& sh, int k, int j) {
+  if (sh.tbar[k] || sh.tbar[j]) return true;
+  const int ik = sh.acc_i[k], ij = sh.acc_i[j];
+  const int kk = sh.mkind[ik], kj = sh.mkind[ij];
+  const int ck[3] = {kk != 1 ? sh.co[ik] : -1, kk != 2 ? sh.cn[ik] : -1, sh.tcl[k]};
+  const int cj[3] = {kj != 1 ? sh.co[ij] : -1, kj != 2 ? sh.cn[ij] : -1, sh.tcl[j]};
+  const int bk[3] = {kk != 1 ? (int)mbrick(a.m, sh.pto[ik]) : -1, kk != 2 ? (int)mbrick(a.m, sh.ptn[ik]) : -1, sh.tbl[k]};
+  const int bj[3] = {kj != 1 ? (int)mbrick(a.m, sh.pto[ij]) : -1, kj != 2 ? (int)mbrick(a.m, sh.ptn[ij]) : -1, sh.tbl[j]};
+  for (int x = 0; x < 3; ++x)
+    for (int y = 0; y < 3; ++y) {
+      if (ck[x] >= 0 && ck[x] == cj[y]) return true;
+      if (bk[x] >= 0 && bk[x] == bj[y]) return true;
+    }
+  const int64_t pk[2] = {sh.ia[ik], sh.ib[ik]}, pj[2] = {sh.ia[ij], sh.ib[ij]};
+  for (int x = 0; x < 2; ++x)
+    for (int y = 0; y < 2; ++y)
+      if (pk[x] >= 0 && pk[x] == pj[y]) return true;
+  return false;
+}
+
 // Brick at window offset o (0..26) of a packed brick point (dims >= 3).
 __device__ __forceinline__ uint32_t nbr_brick(const Mirror& m, uint32_t pt, int o) {
   const int d = m.dims;
@@ -770,95 +854,7 @@ __device__ __noinline__ void helpers(const EngineArgs& a, SeqShared& sh, int war
     while (ld_acquire(&ex->tag) != (uint64_t)D.r) nap();
     return ex;
   };
-  if (warp == kPollWarps) {  // structural commits (commit.cuh) + the movers' e
-    const bool mine = lane < D.nacc;
-    MoveData md{};
-    CommitIn c{};
-    Touch t{};
-    int kind = 0;
-    uint64_t pid = 0, nn = 0;
-    double esu = 0.0, esw = 0.0;
-    if (mine) {
-      kind = D.acc_kind[lane];
-      nn = (uint64_t)((int64_t)D.n + D.acc_d[lane]);
-      pid = kind == 1 ? 0 : (uint64_t)D.acc_ia[lane];
-      md.nx = D.acc_nx[lane];
-      md.ny = D.acc_ny[lane];
-      md.nz = D.acc_nz[lane];
-      md.rslot_pid = md.bslot_pid = -1;
-      load_move(a.s, kind, pid, md);
-      if (kind != 2) {
-        const OffRec& o = ext_of(D.acc_i[lane])->off[D.acc_d[lane] + kHalf];
-        esu = o.su;
-        esw = o.sw;
-      }
-      commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
-      t = touch_of(a.m, kind, pid, nn, c);
-      if (kind == 2 && pid != nn - 1) {  // the relabelled particle's e (loaded before any store)
-        const double2 el = __ldcg(a.ep + (nn - 1));
-        esu = el.x;
-        esw = el.y;
-      }
-    }
-    // Commits load everything first, so a later insertion that reuses the
-    // index an earlier deletion vacated (relabel) stores nothing the deletion
-    // loads: that pair needs no ordering. Any other overlap of cells, bricks
-    // or particles is applied in move order.
-    bool dep = false;
-    unsigned exm = 0;  // earlier deletions this insertion was exempted against
-#pragma unroll 1
-    for (int j = 0; j < D.nacc - 1; ++j) {
-      Touch tj;
-#pragma unroll
-      for (int x = 0; x < 3; ++x) {
-        tj.cell[x] = __shfl_sync(0xffffffffu, t.cell[x], j);
-        tj.brick[x] = __shfl_sync(0xffffffffu, t.brick[x], j);
-      }
-#pragma unroll
-      for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, t.part[x], j);
-      const int kj = __shfl_sync(0xffffffffu, kind, j);
-      if (mine && j < lane) {
-        Touch tm = t;
-        if (kind == 1 && kj == 2 && tm.part[0] == tj.part[1]) {
-          tm.part[0] = -1;
-          exm |= 1u << j;
-        }
-        if (touches(tm, tj)) dep = true;
-      }
-    }
-    // ... unless that deletion is itself applied in order (it then loads late)
-    if (__ballot_sync(0xffffffffu, dep) & exm) dep = true;
-    auto set_e = [&]() {
-      if (kind == 0) a.ep[pid] = make_double2(esu, esw);
-      else if (kind == 1) a.ep[nn] = make_double2(esu, esw);
-      else if (pid != nn - 1) a.ep[pid] = make_double2(esu, esw);
-    };
-    long long e1, e2, e3;
-    if (mine && !dep) {
-      commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
-      set_e();
-    }
-    const unsigned deps = __ballot_sync(0xffffffffu, dep);
-    if (deps) {
-      __syncwarp();  // same warp: stores before the barrier are visible to loads after it
-#pragma unroll 1
-      for (int j = 0; j < D.nacc; ++j) {
-        if (((deps >> j) & 1u) && lane == j) {
-          load_move(a.s, kind, pid, md);
-          if (kind == 2 && pid != nn - 1) {
-            const double2 el = __ldcg(a.ep + (nn - 1));
-            esu = el.x;
-            esw = el.y;
-          }
-          commit_move(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, e1, e2, e3);
-          set_e();
-        }
-        __syncwarp();
-      }
-    }
-    if (mine) __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(a.flags, (uint64_t)D.r);
+  if (warp == kPollWarps) {  // (commits run in the reserved evaluator groups)
   } else if (warp == kPollWarps + 1) {  // statistics (engine.hpp:293-308, 413-426)
     const int len = D.len, nacc = D.nacc;
     ChainState& ks = sh.ks;
@@ -1019,6 +1015,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           __nanosleep(a.poll_ns);
         }
         sh.mkind[sl] = (uint8_t)(w[0] & 3);
+        sh.acck[sl] = -1;
         sh.macc[sl] = (uint32_t)((w[0] & kPay) >> 8);
         sh.mcf[sl] = (uint32_t)w[1];
         sh.movf[sl] = (uint32_t)w[2];
@@ -1065,6 +1062,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             }
             if (lane == 0) {
               sh.acc_i[nacc] = e;
+              sh.acck[e] = (int8_t)nacc;
               sh.acc_d[nacc] = d;
             }
             ++nacc;
@@ -1122,6 +1120,13 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             sh.co[i] = grid ? cell_of(a.g, o.x, o.y, o.z) : -1;
             sh.ia[i] = (int64_t)pid;
             sh.ib[i] = kind == 2 ? nd - 1 : -1;
+            const int k = sh.acck[i];
+            if (kind == 2 && k >= 0 && pid != (uint64_t)(nd - 1)) {  // the particle the deletion relabels
+              const double4 q = ld_cg(a.s.pos + (nd - 1));
+              sh.xq[k][0] = q.x;
+              sh.xq[k][1] = q.y;
+              sh.xq[k][2] = q.z;
+            }
           }
         }
       }
@@ -1133,6 +1138,36 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       const bool bm = a.m.nb <= (uint32_t)kBitWords * 32u && a.m.dims >= 3;
       {
         const int nacc = sh.nacc;
+        // commit ordering data of accepted move k: the cell / brick of the
+        // particle a deletion relabels (its position forwarded from an earlier
+        // accepted move of the round that wrote that index)
+        if (tid < nacc) {
+          const int k = tid, i = sh.acc_i[k];
+          sh.tcl[k] = -1;
+          sh.tbl[k] = -1;
+          sh.tbar[k] = 0;
+          sh.deps[k] = 0u;
+          if (sh.mkind[i] == 2 && sh.ia[i] != sh.ib[i]) {
+            const int64_t q = sh.ib[i];
+            double x = sh.xq[k][0], y = sh.xq[k][1], z = sh.xq[k][2];
+            for (int j = k - 1; j >= 0; --j) {
+              const int ij = sh.acc_i[j];
+              if (sh.ia[ij] != q && sh.ib[ij] != q) continue;
+              const int kj = sh.mkind[ij];
+              if (kj == 2 || sh.ib[ij] == q) {
+                sh.tbar[k] = 1;  // index reused by a deletion's relabel: order after everything
+              } else {
+                const Proposal& pj = sh.ring[(base + ij) % kRing];
+                x = pj.x;
+                y = pj.y;
+                z = pj.z;
+              }
+              break;
+            }
+            sh.tcl[k] = grid ? cell_of(a.g, x, y, z) : -1;
+            sh.tbl[k] = (int)mbrick(a.m, mpoint(a.m, x, y, z));
+          }
+        }
         if (bm)
           for (int q = tid; q < nacc * 54; q += kPollThreads) {
             const int k = q / 54, rem = q % 54;
@@ -1171,6 +1206,13 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             }
           }
           if (c) atomicMin(&sh.cmin, i);
+        }
+        // commit order: accepted k after accepted j < k when they share a
+        // reference cell, a brick or a particle index
+        for (int q = tid; q < nacc * nacc; q += kPollThreads) {
+          const int k = q / nacc, j = q % nacc;
+          if (j >= k) continue;
+          if (commits_overlap(a, sh, k, j)) atomicOr(&sh.deps[k], 1u << j);
         }
         // two accepted moves of a round update disjoint sets of neighbour
         // energies (no changed points within 2 r_c), so every e_j sees its
@@ -1237,7 +1279,11 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         t->nz = pr.z;
         t->ia = sh.ia[i];
         t->ib = sh.ib[i];
+        t->nn = (uint64_t)((int64_t)n + sh.acc_d[lane]);
         t->kind = kind;
+        t->slot = i;
+        t->d = sh.acc_d[lane];
+        t->deps = sh.deps[lane] & ((1u << lane) - 1u);
         st_release(&t->tag, (uint64_t)r);
       }
     } else if (warp >= 2 && warp < 2 + kMaxMoves / 32) {  // hand the round to the helpers
@@ -1270,7 +1316,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     }
     // the previous round's energy updates must land before D_{r+1}
     if (tid == 32 * 15)
-      while (ld_acquire(a.flags + 8) < etarget) __nanosleep(a.poll_ns);
+      while (ld_acquire(a.flags + kECount) < etarget) __nanosleep(a.poll_ns);
     __syncthreads();
     if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
     etarget += (uint64_t)nacc;
