@@ -116,6 +116,7 @@ struct EngineArgs {
   uint64_t* flags;  // see kECount / kSFlag
   int smem_occ;
   unsigned poll_ns, epoll_ns;
+  int walk_reps;  // diagnostics: walk repeated (GCMC_WALK_REPS)
   unsigned long long* prof;
 };
 
@@ -301,14 +302,9 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
     if (kind != 1) nent = win_add<T>(a.m, a.b, ws, nent, ox, oy, oz, lane);
     if (kind == 2) nent0 = nent;
     win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
-    // the round's other commits whose bricks these windows read
-    const Dec& d = sh.d;
-    const AccE& me = d.acc[G.k];
-    bool wait = false;
-    if (lane < d.nacc && lane != G.k)
-      wait = mnear(a.m, me.pt0, d.acc[lane].pt0) || mnear(a.m, me.pt0, d.acc[lane].pt1) ||
-             mnear(a.m, me.pt1, d.acc[lane].pt0) || mnear(a.m, me.pt1, d.acc[lane].pt1);
-    if (wait)
+    // every commit of the round has landed (a relabel changes record ids in
+    // bricks these windows may read)
+    if (lane < sh.d.nacc)
       while (ld_acquire(a.flags + kSFlag + lane) != (uint64_t)rr) nap();
     __syncwarp();
     if (lane == 0) {
@@ -675,7 +671,7 @@ struct Round {  // a decided round, handed to the helper warps
   uint32_t r;
   int len, nacc, par;
   int acc_i[kMaxAcc], acc_d[kMaxAcc], acc_kind[kMaxAcc];
-  int64_t acc_ia[kMaxAcc];
+  int64_t acc_ia[kMaxAcc], acc_ib[kMaxAcc];
   double acc_nx[kMaxAcc], acc_ny[kMaxAcc], acc_nz[kMaxAcc];
   int res_d[kMaxMoves];
   uint8_t kind[kMaxMoves];
@@ -976,6 +972,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   if (tid == 0) {
     sh.ks = *a.st;
     sh.done.len = 0;
+    sh.done.nacc = 0;
     sh.err = 0;
     for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
   }
@@ -1026,6 +1023,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         // Compact (I-cache friendly) scan: one ballot per 32 moves plus one
         // per event (accept / stop); N changes only at accepted insertions /
         // deletions, which are rare.
+#pragma unroll 1
+        for (int rep = 0; rep < a.walk_reps; ++rep) {
+        if (rep == 1) pc.mark(7);
         int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
         const int nh = (fit + 31) >> 5;
 #pragma unroll 1
@@ -1085,6 +1085,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           sh.err = err;
           sh.why = why;
           sh.dend = d;
+        }
         }
       }
       group_sync(1, kPollThreads);
@@ -1149,6 +1150,10 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           sh.deps[k] = 0u;
           if (sh.mkind[i] == 2 && sh.ia[i] != sh.ib[i]) {
             const int64_t q = sh.ib[i];
+            // q written by the previous round's commits (possibly still in
+            // flight when xq was loaded): order this commit after everything
+            for (int j = 0; j < sh.done.nacc; ++j)
+              if (sh.done.acc_ia[j] == q || sh.done.acc_ib[j] == q) sh.tbar[k] = 1;
             double x = sh.xq[k][0], y = sh.xq[k][1], z = sh.xq[k][2];
             for (int j = k - 1; j >= 0; --j) {
               const int ij = sh.acc_i[j];
@@ -1300,6 +1305,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         D.acc_d[i] = sh.acc_d[i];
         D.acc_kind[i] = sh.mkind[m];
         D.acc_ia[i] = sh.ia[m];
+        D.acc_ib[i] = sh.ib[m];
         D.acc_nx[i] = pr.x;
         D.acc_ny[i] = pr.y;
         D.acc_nz[i] = pr.z;
@@ -1550,6 +1556,8 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
     a.poll_ns = e1 ? (unsigned)std::atoi(e1) : 64u;
     const char* e2 = std::getenv("GCMC_EPOLL_NS");
     a.epoll_ns = e2 ? (unsigned)std::atoi(e2) : 64u;
+    const char* e3 = std::getenv("GCMC_WALK_REPS");
+    a.walk_reps = e3 && std::atoi(e3) > 1 ? std::atoi(e3) : 1;
   }
   size_t eval_bytes = T == 128 ? sizeof(EvalShared<128>) : (T == 256 ? sizeof(EvalShared<256>) : sizeof(EvalShared<512>));
   eval_bytes = (eval_bytes + 15) & ~size_t(15);
