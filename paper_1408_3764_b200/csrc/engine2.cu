@@ -90,8 +90,8 @@ struct ATab {  // accepted move k of a round, exact (sequencer -> commit groups 
   uint32_t deps;   // earlier accepted moves of the round this commit is ordered after
   uint64_t tag;    // round (stored last, release)
 };
-// flags[]: [kECount] energy updates done (cumulative); [kSFlag + k] round whose
-// accepted move k has been committed (structural + the mover's e).
+// flags[]: [kECount] energy updates done (cumulative); [kSFlag] last round whose
+// accepted moves are committed (structural + the movers' e).
 constexpr int kECount = 8;
 constexpr int kSFlag = 16;
 
@@ -227,48 +227,101 @@ struct EvalShared {
   } gs[kThreads / T];
 };
 
-// The structural commit of one accepted move (one thread): store,
-// reference grid and brick mirror (commit.cuh) and the mover's e. Loads
-// first, then stores; ordered after the round's commits it overlaps (ATab
-// deps) by per-move flags.
-__device__ __noinline__ void structural_commit(const EngineArgs& a, const ATab* t, uint32_t rr, int k) {
-  const int kind = (int)__ldcg(&t->kind);
-  const uint64_t nn = __ldcg(&t->nn);
-  const uint64_t pid = kind == 1 ? 0 : (uint64_t)__ldcg(&t->ia);
-  uint32_t deps = __ldcg(&t->deps);
-  while (deps) {
-    const int j = __ffs(deps) - 1;
-    deps &= deps - 1;
-    while (ld_acquire(a.flags + kSFlag + j) != (uint64_t)rr) nap();
-  }
+// The structural commits of the accepted moves of round rr (one warp, lane
+// k = accepted move k): store, reference grid and brick mirror (commit.cuh)
+// and the movers' e. Every lane loads first; a commit whose cells, bricks or
+// particles overlap an earlier one of the round is re-loaded and applied
+// after it in move order (a later insertion reusing the index an earlier
+// deletion vacated needs no order: the deletion's loads precede every store,
+// unless it is itself ordered). Then flags[kSFlag] = rr.
+__device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_t rr, int lane) {
+  const bool mine = lane < nacc;
+  const ATab* t = a.atab + (size_t)(rr & 1) * kMaxAcc + lane;
   MoveData md{};
-  md.nx = __ldcg(&t->nx);
-  md.ny = __ldcg(&t->ny);
-  md.nz = __ldcg(&t->nz);
-  md.rslot_pid = md.bslot_pid = -1;
-  load_move(a.s, kind, pid, md);
+  CommitIn c{};
+  Touch tc{};
+  int kind = 0;
+  uint64_t pid = 0, nn = 0;
   double esu = 0.0, esw = 0.0;
-  if (kind != 2) {
-    const SlotExt* ex = a.ext + (size_t)(rr & 1) * a.nslots + __ldcg(&t->slot);
-    while (ld_acquire(&ex->tag) != (uint64_t)rr) nap();
-    const OffRec* o = &ex->off[__ldcg(&t->d) + kHalf];
-    esu = __ldcg(&o->su);
-    esw = __ldcg(&o->sw);
+  if (mine) {
+    while (ld_acquire(&t->tag) != (uint64_t)rr) nap();
+    kind = (int)__ldcg(&t->kind);
+    nn = __ldcg(&t->nn);
+    pid = kind == 1 ? 0 : (uint64_t)__ldcg(&t->ia);
+    md.nx = __ldcg(&t->nx);
+    md.ny = __ldcg(&t->ny);
+    md.nz = __ldcg(&t->nz);
+    md.rslot_pid = md.bslot_pid = -1;
+    load_move(a.s, kind, pid, md);
+    if (kind != 2) {
+      const SlotExt* ex = a.ext + (size_t)(rr & 1) * a.nslots + __ldcg(&t->slot);
+      while (ld_acquire(&ex->tag) != (uint64_t)rr) nap();
+      const OffRec* o = &ex->off[__ldcg(&t->d) + kHalf];
+      esu = __ldcg(&o->su);
+      esw = __ldcg(&o->sw);
+    }
+    commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
+    tc = touch_of(a.m, kind, pid, nn, c);
+    if (kind == 2 && pid != nn - 1) {
+      const double2 el = __ldcg(a.ep + (nn - 1));
+      esu = el.x;
+      esw = el.y;
+    }
   }
-  CommitIn c;
-  commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
-  if (kind == 2 && pid != nn - 1) {  // the relabelled particle's e
-    const double2 el = __ldcg(a.ep + (nn - 1));
-    esu = el.x;
-    esw = el.y;
+  bool dep = false;
+  unsigned exm = 0;
+#pragma unroll 1
+  for (int j = 0; j < nacc - 1; ++j) {
+    Touch tj;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      tj.cell[x] = __shfl_sync(0xffffffffu, tc.cell[x], j);
+      tj.brick[x] = __shfl_sync(0xffffffffu, tc.brick[x], j);
+    }
+#pragma unroll
+    for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tc.part[x], j);
+    const int kj = __shfl_sync(0xffffffffu, kind, j);
+    if (mine && j < lane) {
+      Touch tm = tc;
+      if (kind == 1 && kj == 2 && tm.part[0] == tj.part[1]) {
+        tm.part[0] = -1;
+        exm |= 1u << j;
+      }
+      if (touches(tm, tj)) dep = true;
+    }
   }
+  if (__ballot_sync(0xffffffffu, dep) & exm) dep = true;
+  auto set_e = [&]() {
+    if (kind == 0) __stcg(a.ep + pid, make_double2(esu, esw));
+    else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
+    else if (pid != nn - 1) __stcg(a.ep + pid, make_double2(esu, esw));
+  };
   long long e1, e2, e3;
-  commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
-  if (kind == 0) __stcg(a.ep + pid, make_double2(esu, esw));
-  else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
-  else if (pid != nn - 1) __stcg(a.ep + pid, make_double2(esu, esw));
-  __threadfence();
-  st_release(a.flags + kSFlag + k, (uint64_t)rr);
+  if (mine && !dep) {
+    commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+    set_e();
+  }
+  const unsigned deps = __ballot_sync(0xffffffffu, dep);
+  if (deps) {
+    __syncwarp();  // same warp: stores before the barrier are visible to loads after it
+#pragma unroll 1
+    for (int j = 0; j < nacc; ++j) {
+      if (((deps >> j) & 1u) && lane == j) {
+        load_move(a.s, kind, pid, md);
+        if (kind == 2 && pid != nn - 1) {
+          const double2 el = __ldcg(a.ep + (nn - 1));
+          esu = el.x;
+          esw = el.y;
+        }
+        commit_move(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, e1, e2, e3);
+        set_e();
+      }
+      __syncwarp();
+    }
+  }
+  if (mine) __threadfence();
+  __syncwarp();
+  if (lane == 0) st_release(a.flags + kSFlag, (uint64_t)rr);
 }
 
 // Commit task for accepted move k of round r - 1 (a reserved group): the
@@ -287,8 +340,6 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
     if (lane == 0) {
       while (ld_acquire(&t->tag) != (uint64_t)rr) nap();
       ec.mark(0);
-      structural_commit(a, t, rr, G.k);
-      ec.mark(1);
     }
     __syncwarp();
     const int kind = (int)__ldcg(&t->kind);
@@ -304,8 +355,10 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
     win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
     // every commit of the round has landed (a relabel changes record ids in
     // bricks these windows may read)
-    if (lane < sh.d.nacc)
-      while (ld_acquire(a.flags + kSFlag + lane) != (uint64_t)rr) nap();
+    if (lane == 0) {
+      while (ld_acquire(a.flags + kSFlag) != (uint64_t)rr) nap();
+      ec.mark(1);
+    }
     __syncwarp();
     if (lane == 0) {
       G.kind = kind;
@@ -466,6 +519,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         } else if (s >= eslot0 && s - eslot0 < d.nacc) {
           Gl.task = 2;
           Gl.k = s - eslot0;
+        } else if (s == eslot0 - 1 && d.nacc > 0) {
+          Gl.task = 3;  // structural commits of the previous round
         }
       }
       cp_async_wait();
@@ -473,6 +528,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     __syncthreads();
     pc.mark(1);
     const Dec& d = sh.d;
+    if (G.task == 3 && gt < 32) commit_round(a, d.nacc, r - 1, lane);
     if (G.task == 2) energy_update<T>(a, sh, ws, occ_s, r, g, gt, gw, lane, bar_id);
     if (d.stop) break;
     if (G.task == 1) {
@@ -511,8 +567,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const uint64_t pn = pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z);
           bool near = false;
           if (lane < d.nacc) near = mnear(a.m, pn, d.acc[lane].pt0) || mnear(a.m, pn, d.acc[lane].pt1);
-          if (near)
-            while (ld_acquire(a.flags + kSFlag + lane) != (uint64_t)(r - 1)) nap();
+          if (__any_sync(0xffffffffu, near) && lane == 0)
+            while (ld_acquire(a.flags + kSFlag) < (uint64_t)(r - 1)) nap();
           __syncwarp();
           pc.mark(7);
           if (lane == 0) {
@@ -683,7 +739,9 @@ struct SeqShared {
   Proposal ring[kRing];
   uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
   uint8_t mkind[kMaxMoves];
-  int len, nacc, err, cmin, why, dend;
+  int len, nacc, err, cmin, why, dend, arrived;
+  int wscr_i[kMaxAcc], wscr_d[kMaxAcc];  // walk dry runs (discarded)
+  int8_t wscr_k[kMaxMoves];
   int acc_i[kMaxAcc], acc_d[kMaxAcc];
   int res_d[kMaxMoves];
   // read / write sets of the consumed moves (verify)
@@ -700,9 +758,6 @@ struct SeqShared {
   uint32_t nbits[kBitWords];  // verify: bricks near a changed point of the round
   unsigned smp[kMH];          // statistics: sampled steps of the round
   int8_t acck[kMaxMoves];     // accepted index of a consumed move (-1: rejected)
-  double xq[kMaxAcc][3];      // position of the particle a deletion relabels
-  int32_t tcl[kMaxAcc], tbl[kMaxAcc], tbar[kMaxAcc];
-  uint32_t deps[kMaxAcc];
   uint64_t dw[kDecWords];
   int dneed;
   ChainState ks;
@@ -729,6 +784,74 @@ __device__ __noinline__ Observables observables(const EngineArgs& a, uint64_t n,
     ru = __dadd_rn(ru, __dmul_rn((double)n, tu));
   }
   return {ru, p};
+}
+
+struct WalkOut {
+  int len, nacc, err, why;
+};
+
+// The walk (one warp): moves in order, tracking the N offset d (bit d + 16
+// of a move's masks); stops at the first move whose mask says stop (conflict
+// with an in-flight commit, or d outside the evaluated range) or whose accepted
+// commit would overflow. One ballot per 32 moves plus one per event; N
+// changes only at accepted insertions / deletions.
+__device__ __noinline__ WalkOut walk_warp(const uint32_t* macc, const uint32_t* mcf, const uint32_t* movf,
+                                          const uint8_t* mkind, int fit, int* acc_i, int* acc_d,
+                                          int8_t* acck, int lane) {
+  int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
+  const int nh = (fit + 31) >> 5;
+#pragma unroll 1
+  for (int h = 0; h < nh; ++h) {
+    const int i = lane + 32 * h;
+    const bool in = i < fit;
+    const uint32_t am = in ? macc[i] : 0u, sm = in ? mcf[i] : 0u, om = in ? movf[i] : 0u;
+    const int kd = in ? mkind[i] : 0;
+    bool done = false;
+#pragma unroll 1
+    for (;;) {
+      const int j = d + kHalf;
+      const bool inr = j >= 0 && j < 32;
+      const bool act = in && i >= start;
+      const bool st = act && (!inr || ((sm >> (j & 31)) & 1u));
+      const bool ac = act && inr && ((am >> (j & 31)) & 1u);
+      const unsigned ev = __ballot_sync(0xffffffffu, st || ac);
+      if (!ev) break;
+      const int el = __ffs(ev) - 1;
+      const int e = 32 * h + el;
+      const unsigned info = __shfl_sync(0xffffffffu, (st ? 1u : 0u) | (((om >> (j & 31)) & 1u) << 1) | ((unsigned)kd << 2), el);
+      if (info & 1u) {
+        len = e;
+        why = inr ? kStopPrev : kStopRange;
+        done = true;
+        break;
+      }
+      if (info & 2u) {
+        len = e;
+        err = 1;
+        why = kStopOverflow;
+        done = true;
+        break;
+      }
+      if (lane == 0) {
+        acc_i[nacc] = e;
+        acc_d[nacc] = d;
+        acck[e] = (int8_t)nacc;
+      }
+      ++nacc;
+      const int k = (int)(info >> 2);
+      d += k == 1 ? 1 : (k == 2 ? -1 : 0);
+      start = e + 1;
+      if (nacc == kMaxAcc) {
+        len = e + 1;
+        why = kStopFull;
+        done = true;
+        break;
+      }
+    }
+    if (done) break;
+  }
+  __syncwarp();
+  return {len, nacc, err, why};
 }
 
 // Does consumed move i read anything accepted move j (earlier in the round)
@@ -766,28 +889,6 @@ __device__ __noinline__ bool conflict_xyz(const EngineArgs& a, const SeqShared& 
     if (an != kNoPoint && mnear(a.m, lo, an) &&
         within_rc(a.b, sh.xo[i][0], sh.xo[i][1], sh.xo[i][2], pj.x, pj.y, pj.z)) return true;
   }
-  return false;
-}
-
-// Do the commits of accepted moves k and j (j earlier) touch a common
-// reference cell, brick or particle index (commit.cuh Touch)?
-__device__ __noinline__ bool commits_overlap(const EngineArgs& a, const SeqShared& sh, int k, int j) {
-  if (sh.tbar[k] || sh.tbar[j]) return true;
-  const int ik = sh.acc_i[k], ij = sh.acc_i[j];
-  const int kk = sh.mkind[ik], kj = sh.mkind[ij];
-  const int ck[3] = {kk != 1 ? sh.co[ik] : -1, kk != 2 ? sh.cn[ik] : -1, sh.tcl[k]};
-  const int cj[3] = {kj != 1 ? sh.co[ij] : -1, kj != 2 ? sh.cn[ij] : -1, sh.tcl[j]};
-  const int bk[3] = {kk != 1 ? (int)mbrick(a.m, sh.pto[ik]) : -1, kk != 2 ? (int)mbrick(a.m, sh.ptn[ik]) : -1, sh.tbl[k]};
-  const int bj[3] = {kj != 1 ? (int)mbrick(a.m, sh.pto[ij]) : -1, kj != 2 ? (int)mbrick(a.m, sh.ptn[ij]) : -1, sh.tbl[j]};
-  for (int x = 0; x < 3; ++x)
-    for (int y = 0; y < 3; ++y) {
-      if (ck[x] >= 0 && ck[x] == cj[y]) return true;
-      if (bk[x] >= 0 && bk[x] == bj[y]) return true;
-    }
-  const int64_t pk[2] = {sh.ia[ik], sh.ib[ik]}, pj[2] = {sh.ia[ij], sh.ib[ij]};
-  for (int x = 0; x < 2; ++x)
-    for (int y = 0; y < 2; ++y)
-      if (pk[x] >= 0 && pk[x] == pj[y]) return true;
   return false;
 }
 
@@ -973,6 +1074,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     sh.ks = *a.st;
     sh.done.len = 0;
     sh.done.nacc = 0;
+    sh.arrived = 0;
     sh.err = 0;
     for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
   }
@@ -997,8 +1099,15 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   for (;;) {
     const int par = (int)(r & 1);
     if (warp < kPollWarps) {
-      // -------------------- poll: slot words -> per-move masks
-      for (int sl = tid; sl < fit; sl += kPollThreads) {
+      // -------------------- poll: slot words -> per-move masks. Warp 0 does
+      // not poll: it repeats the walk on the masks as they arrive (results
+      // discarded) so that the walk's code is in the instruction cache when
+      // the last slot lands.
+      if (warp == 0) {
+        while (*(volatile int*)&sh.arrived < fit)
+          walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+      }
+      for (int sl = tid - 32; sl >= 0 && sl < fit; sl += kPollThreads - 32) {
         const uint64_t* rw = a.res + (size_t)par * kResWords * a.nslots + sl;
         uint64_t w[kResWords];
         for (;;) {
@@ -1016,76 +1125,18 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         sh.macc[sl] = (uint32_t)((w[0] & kPay) >> 8);
         sh.mcf[sl] = (uint32_t)w[1];
         sh.movf[sl] = (uint32_t)w[2];
+        atomicAdd(&sh.arrived, 1);
       }
       group_sync(1, kPollThreads);
       pc.mark(1);
-      if (warp == 0) {  // ---- walk: bit j of a mask <-> N offset d = j - 16
-        // Compact (I-cache friendly) scan: one ballot per 32 moves plus one
-        // per event (accept / stop); N changes only at accepted insertions /
-        // deletions, which are rare.
-#pragma unroll 1
-        for (int rep = 0; rep < a.walk_reps; ++rep) {
-        if (rep == 1) pc.mark(7);
-        int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
-        const int nh = (fit + 31) >> 5;
-#pragma unroll 1
-        for (int h = 0; h < nh; ++h) {
-          const int i = lane + 32 * h;
-          const bool in = i < fit;
-          const uint32_t am = in ? sh.macc[i] : 0u, sm = in ? sh.mcf[i] : 0u, om = in ? sh.movf[i] : 0u;
-          const int kd = in ? sh.mkind[i] : 0;
-          bool done = false;
-#pragma unroll 1
-          for (;;) {
-            const int j = d + kHalf;
-            const bool inr = j >= 0 && j < 32;
-            const bool act = in && i >= start;
-            const bool st = act && (!inr || ((sm >> (j & 31)) & 1u));
-            const bool ac = act && inr && ((am >> (j & 31)) & 1u);
-            const unsigned ev = __ballot_sync(0xffffffffu, st || ac);
-            if (!ev) break;
-            const int el = __ffs(ev) - 1;
-            const int e = 32 * h + el;
-            const unsigned info = __shfl_sync(0xffffffffu, (st ? 1u : 0u) | (((om >> (j & 31)) & 1u) << 1) | ((unsigned)kd << 2), el);
-            if (info & 1u) {
-              len = e;
-              why = inr ? kStopPrev : kStopRange;
-              done = true;
-              break;
-            }
-            if (info & 2u) {
-              len = e;
-              err = 1;
-              why = kStopOverflow;
-              done = true;
-              break;
-            }
-            if (lane == 0) {
-              sh.acc_i[nacc] = e;
-              sh.acck[e] = (int8_t)nacc;
-              sh.acc_d[nacc] = d;
-            }
-            ++nacc;
-            const int k = (int)(info >> 2);
-            d += k == 1 ? 1 : (k == 2 ? -1 : 0);
-            start = e + 1;
-            if (nacc == kMaxAcc) {
-              len = e + 1;
-              why = kStopFull;
-              done = true;
-              break;
-            }
-          }
-          if (done) break;
-        }
+      if (warp == 0) {  // ---- walk (warm: warp 0 ran it on the partial masks while polling)
+        const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane);
         if (lane == 0) {
-          sh.len = len;
-          sh.nacc = nacc;
-          sh.cmin = len;
-          sh.err = err;
-          sh.why = why;
-          sh.dend = d;
-        }
+          sh.len = wo.len;
+          sh.nacc = wo.nacc;
+          sh.cmin = wo.len;
+          sh.err = wo.err;
+          sh.why = wo.why;
         }
       }
       group_sync(1, kPollThreads);
@@ -1121,13 +1172,6 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             sh.co[i] = grid ? cell_of(a.g, o.x, o.y, o.z) : -1;
             sh.ia[i] = (int64_t)pid;
             sh.ib[i] = kind == 2 ? nd - 1 : -1;
-            const int k = sh.acck[i];
-            if (kind == 2 && k >= 0 && pid != (uint64_t)(nd - 1)) {  // the particle the deletion relabels
-              const double4 q = ld_cg(a.s.pos + (nd - 1));
-              sh.xq[k][0] = q.x;
-              sh.xq[k][1] = q.y;
-              sh.xq[k][2] = q.z;
-            }
           }
         }
       }
@@ -1139,40 +1183,6 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       const bool bm = a.m.nb <= (uint32_t)kBitWords * 32u && a.m.dims >= 3;
       {
         const int nacc = sh.nacc;
-        // commit ordering data of accepted move k: the cell / brick of the
-        // particle a deletion relabels (its position forwarded from an earlier
-        // accepted move of the round that wrote that index)
-        if (tid < nacc) {
-          const int k = tid, i = sh.acc_i[k];
-          sh.tcl[k] = -1;
-          sh.tbl[k] = -1;
-          sh.tbar[k] = 0;
-          sh.deps[k] = 0u;
-          if (sh.mkind[i] == 2 && sh.ia[i] != sh.ib[i]) {
-            const int64_t q = sh.ib[i];
-            // q written by the previous round's commits (possibly still in
-            // flight when xq was loaded): order this commit after everything
-            for (int j = 0; j < sh.done.nacc; ++j)
-              if (sh.done.acc_ia[j] == q || sh.done.acc_ib[j] == q) sh.tbar[k] = 1;
-            double x = sh.xq[k][0], y = sh.xq[k][1], z = sh.xq[k][2];
-            for (int j = k - 1; j >= 0; --j) {
-              const int ij = sh.acc_i[j];
-              if (sh.ia[ij] != q && sh.ib[ij] != q) continue;
-              const int kj = sh.mkind[ij];
-              if (kj == 2 || sh.ib[ij] == q) {
-                sh.tbar[k] = 1;  // index reused by a deletion's relabel: order after everything
-              } else {
-                const Proposal& pj = sh.ring[(base + ij) % kRing];
-                x = pj.x;
-                y = pj.y;
-                z = pj.z;
-              }
-              break;
-            }
-            sh.tcl[k] = grid ? cell_of(a.g, x, y, z) : -1;
-            sh.tbl[k] = (int)mbrick(a.m, mpoint(a.m, x, y, z));
-          }
-        }
         if (bm)
           for (int q = tid; q < nacc * 54; q += kPollThreads) {
             const int k = q / 54, rem = q % 54;
@@ -1211,13 +1221,6 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             }
           }
           if (c) atomicMin(&sh.cmin, i);
-        }
-        // commit order: accepted k after accepted j < k when they share a
-        // reference cell, a brick or a particle index
-        for (int q = tid; q < nacc * nacc; q += kPollThreads) {
-          const int k = q / nacc, j = q % nacc;
-          if (j >= k) continue;
-          if (commits_overlap(a, sh, k, j)) atomicOr(&sh.deps[k], 1u << j);
         }
         // two accepted moves of a round update disjoint sets of neighbour
         // energies (no changed points within 2 r_c), so every e_j sees its
@@ -1288,7 +1291,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         t->kind = kind;
         t->slot = i;
         t->d = sh.acc_d[lane];
-        t->deps = sh.deps[lane] & ((1u << lane) - 1u);
+        t->deps = 0u;
         st_release(&t->tag, (uint64_t)r);
       }
     } else if (warp >= 2 && warp < 2 + kMaxMoves / 32) {  // hand the round to the helpers
@@ -1337,6 +1340,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       cp_async_wait();
     }
     fit = fit_of(a, nbase);
+    if (tid == 0) sh.arrived = 0;
     __syncthreads();
     base = nbase;
     n = nn;
@@ -1449,7 +1453,7 @@ bool engine2_supported(const Chain& c) {
   if (std::getenv("GCMC_ENGINE_V1")) return false;
   if (c.grid.kind == GCMC_ALL_PAIRS || c.params.max_displacement > 0.0) return false;
   const int mg = kThreads / c.engine_group;
-  return (c.engine_ctas - 1) * mg > kMaxAcc && (c.engine_ctas - 1) * mg <= kMaxSlots;
+  return (c.engine_ctas - 1) * mg > kMaxAcc + 1 && (c.engine_ctas - 1) * mg <= kMaxSlots;
 }
 
 gcmc_status epart_build(Chain& c, double2* out) {
@@ -1530,7 +1534,7 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
     a.tail_bp = 2.0 / 3.0 * sr9 - sr3;
   }
   a.nslots = (G - 1) * MG;
-  a.fitmax = a.nslots - kMaxAcc < kMaxMoves ? a.nslots - kMaxAcc : kMaxMoves;
+  a.fitmax = a.nslots - kMaxAcc - 1 < kMaxMoves ? a.nslots - kMaxAcc - 1 : kMaxMoves;  // + committer
   {
     const char* f = std::getenv("GCMC_FITMAX");
     if (f && std::atoi(f) > 0 && std::atoi(f) < a.fitmax) a.fitmax = std::atoi(f);
