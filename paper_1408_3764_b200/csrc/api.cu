@@ -689,6 +689,17 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
         std::fprintf(stderr, "\n[engine prof] raw eval:");
         for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[16 + k] / R);
         const double ne = (double)(xp[68] ? xp[68] : 1);
+        if (std::getenv("GCMC_ROUND_LOG")) {
+          unsigned long long dbg[8];
+          cudaMemcpy(dbg, c.prof + 3000, sizeof dbg, cudaMemcpyDeviceToHost);
+          std::fprintf(stderr, "\n[dbg] near=%llu flag=%llu nacc=%llu pn=%llx pt1=%llx reach=%llu pt0=%llx base=%llu",
+                       dbg[0], dbg[1], dbg[2], dbg[3], dbg[4], dbg[5], dbg[6], dbg[7]);
+          std::vector<unsigned long long> rl(800);
+          cudaMemcpy(rl.data(), c.prof + 256, 800 * 8, cudaMemcpyDeviceToHost);
+          for (int q = 1; q < 12; ++q)
+            std::fprintf(stderr, "\n[round %d] base=%llu len=%llu nacc=%llu cmin=%llu why=%llu", q, rl[4 * q],
+                         rl[4 * q + 1], rl[4 * q + 2] & 0xffff, rl[4 * q + 2] >> 16, rl[4 * q + 3]);
+        }
         std::fprintf(stderr, "\n[engine prof] commit task (per move, %llu): atab=%.0f commit=%.0f setup+waits=%.0f traverse=%.0f\n",
                      xp[68], xp[64] / ne, xp[65] / ne, xp[66] / ne, xp[67] / ne);
       }

@@ -94,6 +94,7 @@ struct ATab {  // accepted move k of a round, exact (sequencer -> commit groups 
 // accepted moves are committed (structural + the movers' e).
 constexpr int kECount = 8;
 constexpr int kSFlag = 16;
+constexpr int kFlagWords = 64;
 
 struct EngineArgs {
   Grid g;
@@ -567,9 +568,20 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const uint64_t pn = pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z);
           bool near = false;
           if (lane < d.nacc) near = mnear(a.m, pn, d.acc[lane].pt0) || mnear(a.m, pn, d.acc[lane].pt1);
-          if (__any_sync(0xffffffffu, near) && lane == 0)
+          const bool anynear = __any_sync(0xffffffffu, near);
+          if (anynear && lane == 0)
             while (ld_acquire(a.flags + kSFlag) < (uint64_t)(r - 1)) nap();
           __syncwarp();
+          if (a.prof && r == 2 && G.i == 0 && lane == 0) {
+            a.prof[3000] = anynear;
+            a.prof[3001] = ld_acquire(a.flags + kSFlag);
+            a.prof[3002] = d.nacc;
+            a.prof[3003] = pn;
+            a.prof[3004] = d.acc[0].pt1;
+            a.prof[3005] = a.m.reach;
+            a.prof[3006] = d.acc[0].pt0;
+            a.prof[3007] = d.base;
+          }
           pc.mark(7);
           if (lane == 0) {
             const uint32_t bb = mbrick(a.m, pn);
@@ -1247,6 +1259,12 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(3);
+      if (tid == 0 && a.prof && r < 200) {
+        a.prof[256 + 4 * r] = base;
+        a.prof[256 + 4 * r + 1] = (unsigned long long)sh.len;
+        a.prof[256 + 4 * r + 2] = (unsigned long long)sh.nacc | ((unsigned long long)sh.cmin << 16);
+        a.prof[256 + 4 * r + 3] = (unsigned long long)sh.why;
+      }
       if (tid == 0 && sh.cmin < sh.len) {
         const int c = sh.cmin;
         sh.len = c;
@@ -1541,7 +1559,7 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
   }
   if (!c.eng2_buf) {
     const size_t bytes = kDecStride * 8 + 2 * (size_t)kMaxSlots * kResWords * 8 +
-                         2 * (size_t)kMaxSlots * sizeof(SlotExt) + 2 * kMaxAcc * sizeof(ATab) + 16 * 8;
+                         2 * (size_t)kMaxSlots * sizeof(SlotExt) + 2 * kMaxAcc * sizeof(ATab) + kFlagWords * 8;
     if ((e = cudaMalloc(&c.eng2_buf, bytes))) return cuda_error(e, "alloc engine2");
     c.eng2_bytes = bytes;
   }
