@@ -244,8 +244,11 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   int kind = 0;
   uint64_t pid = 0, nn = 0;
   double esu = 0.0, esw = 0.0;
+  PhaseClock cc;
+  cc.start(a.prof && lane == 0);
   if (mine) {
     while (ld_acquire(&t->tag) != (uint64_t)rr) nap();
+    cc.mark(0);
     kind = (int)__ldcg(&t->kind);
     nn = __ldcg(&t->nn);
     pid = kind == 1 ? 0 : (uint64_t)__ldcg(&t->ia);
@@ -261,6 +264,7 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
       esu = __ldcg(&o->su);
       esw = __ldcg(&o->sw);
     }
+    cc.mark(1);
     commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
     tc = touch_of(a.m, kind, pid, nn, c);
     if (kind == 2 && pid != nn - 1) {
@@ -269,6 +273,7 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
       esw = el.y;
     }
   }
+  cc.mark(2);
   bool dep = false;
   unsigned exm = 0;
 #pragma unroll 1
@@ -297,12 +302,14 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
     else if (pid != nn - 1) __stcg(a.ep + pid, make_double2(esu, esw));
   };
+  cc.mark(3);
   long long e1, e2, e3;
   if (mine && !dep) {
     commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
     set_e();
   }
   const unsigned deps = __ballot_sync(0xffffffffu, dep);
+  cc.mark(4);
   if (deps) {
     __syncwarp();  // same warp: stores before the barrier are visible to loads after it
 #pragma unroll 1
@@ -320,9 +327,17 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
       __syncwarp();
     }
   }
+  cc.mark(5);
   if (mine) __threadfence();
   __syncwarp();
   if (lane == 0) st_release(a.flags + kSFlag, (uint64_t)rr);
+  cc.mark(6);
+  if (cc.on) {
+    for (int q = 0; q < 7; ++q) a.prof[80 + q] += cc.acc[q];
+    a.prof[87] += 1;
+    a.prof[88] += (unsigned long long)__popc(deps);
+    a.prof[89] += (unsigned long long)nacc;
+  }
 }
 
 // Commit task for accepted move k of round r - 1 (a reserved group): the
