@@ -60,9 +60,9 @@ constexpr int kMaxAcc = 32;               // accepted moves per round (= reserve
 constexpr int kRing = 512;                // proposal ring (>= 2 * kMaxMoves)
 constexpr int kHalf = 16;                 // N offsets d = -16..15 <-> bit d + 16
 constexpr int kDecHdr = 4;
-constexpr int kDecEnt = 3;
-constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 100
-constexpr int kDecStride = 128;
+constexpr int kDecEnt = 4;
+constexpr int kDecWords = kDecHdr + kDecEnt * kMaxAcc;  // 132
+constexpr int kDecStride = 160;
 constexpr int kResWords = 3;
 constexpr int kPollWarps = 12;
 constexpr int kMaxSlots = 768;            // buffer sizing: evaluator groups
@@ -94,6 +94,7 @@ struct ATab {  // accepted move k of a round, exact (sequencer -> commit groups 
 // accepted moves are committed (structural + the movers' e).
 constexpr int kECount = 8;
 constexpr int kSFlag = 16;
+constexpr int kGo = 24;      // last round whose evaluations are complete (commits may store)
 constexpr int kFlagWords = 64;
 
 struct EngineArgs {
@@ -137,6 +138,7 @@ struct AccE {
   uint64_t pt0, pt1;  // brick points: new (displace / insert), old (displace / delete)
   int64_t ia, ib;     // particle (insert: its new index), last index (delete)
   int kind;
+  int cn, co;         // reference cells of the new / old position (-1: none)
 };
 struct Dec {
   uint64_t base, n;
@@ -159,7 +161,7 @@ __device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, u
 
 // Warp: wait for D_r (self-validating tagged words) and decode it.
 __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane) {
-  constexpr int PER = (kDecWords + 31) / 32;  // 4
+  constexpr int PER = (kDecWords + 31) / 32;  // 5
   uint64_t w[PER];
   for (;;) {
     w[0] = ld_relaxed(a.dec + lane);
@@ -203,9 +205,13 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
       } else if (f == 1) {
         d.acc[e].kind = (int)(p >> 32) & 3;
         d.acc[e].ia = (int64_t)(uint32_t)p;
-      } else {
+      } else if (f == 2) {
         const uint32_t ib = (uint32_t)p;
         d.acc[e].ib = ib == 0xffffffffu ? -1 : (int64_t)ib;
+      } else {
+        const int cn = (int)(p & 0xffffff), co = (int)((p >> 24) & 0xffffff);
+        d.acc[e].cn = cn == 0xffffff ? -1 : cn;
+        d.acc[e].co = co == 0xffffff ? -1 : co;
       }
     }
   }
@@ -217,6 +223,9 @@ template <int T>
 struct EvalShared {
   Proposal ring[kRing];
   Dec d;
+  int nprev;                      // the previous decision's accepted moves (replica update)
+  uint32_t prev_pt0[kMaxAcc], prev_pt1[kMaxAcc];
+  int prev_kind[kMaxAcc];
   WinWs<T> ws[kThreads / T];
   struct G {
     int task;        // 0 none, 1 evaluate move i, 2 energy update of accepted entry k
@@ -225,6 +234,7 @@ struct EvalShared {
     double ox, oy, oz;
     int64_t excl;    // energy update: particle id excluded (the mover)
     int sgn0, sgn1;  // energy update: window signs
+    uint32_t nearS;  // moves in flight whose changed points may be within r_c of n
   } gs[kThreads / T];
 };
 
@@ -303,6 +313,11 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     else if (pid != nn - 1) __stcg(a.ep + pid, make_double2(esu, esw));
   };
   cc.mark(3);
+  // stores only once the round being evaluated against the old state is done
+  if (lane == 0)
+    while (ld_acquire(a.flags + kGo) < (uint64_t)rr + 1) nap();
+  __syncwarp();
+  cc.mark(7);
   long long e1, e2, e3;
   if (mine && !dep) {
     commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
@@ -334,6 +349,7 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   cc.mark(6);
   if (cc.on) {
     for (int q = 0; q < 7; ++q) a.prof[80 + q] += cc.acc[q];
+    a.prof[90] += cc.acc[7];
     a.prof[87] += 1;
     a.prof[88] += (unsigned long long)__popc(deps);
     a.prof[89] += (unsigned long long)nacc;
@@ -368,14 +384,14 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
     nent0 = nent;
     if (kind != 1) nent = win_add<T>(a.m, a.b, ws, nent, ox, oy, oz, lane);
     if (kind == 2) nent0 = nent;
-    win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);
-    // every commit of the round has landed (a relabel changes record ids in
-    // bricks these windows may read)
+    // every commit of the round has landed (they change the records and
+    // occupancies these windows read; the replica still holds the old counts)
     if (lane == 0) {
       while (ld_acquire(a.flags + kSFlag) != (uint64_t)rr) nap();
       ec.mark(1);
     }
     __syncwarp();
+    win_finish<T>(a.m, ws, nullptr, nent, nent0, lane);
     if (lane == 0) {
       G.kind = kind;
       G.nx = kind == 2 ? ox : nx;
@@ -444,6 +460,33 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
   if (ec.on) atomicAdd(a.prof + 68, 1ull);
 }
 
+// Change of Σ pair(x, ·) caused by the in-flight accepted move t: minus the
+// pair with its old position, plus the pair with its new one (each only
+// within r_c), as its commit and energy update will apply them.
+__device__ __noinline__ void pair_delta(const EngineArgs& a, const ATab* t, double x, double y,
+                                        double z, double& cu, double& cw) {
+  cu = cw = 0.0;
+  const int k = (int)__ldcg(&t->kind);
+  if (k != 1) {
+    const double r2 = min_image_dist2(x, y, z, __ldcg(&t->ox), __ldcg(&t->oy), __ldcg(&t->oz), a.b);
+    if (r2 <= a.b.rc2) {
+      double u, w;
+      lj_pair_clamped(r2, a.b, u, w);
+      cu = __dsub_rn(cu, u);
+      cw = __dsub_rn(cw, w);
+    }
+  }
+  if (k != 2) {
+    const double r2 = min_image_dist2(x, y, z, __ldcg(&t->nx), __ldcg(&t->ny), __ldcg(&t->nz), a.b);
+    if (r2 <= a.b.rc2) {
+      double u, w;
+      lj_pair_clamped(r2, a.b, u, w);
+      cu = __dadd_rn(cu, u);
+      cw = __dadd_rn(cw, w);
+    }
+  }
+}
+
 // S(n) without particle xp, re-summed by one warp over the window's
 // candidates in a fixed order (used when pair(n, x_pid) is too large to
 // subtract without losing precision).
@@ -499,6 +542,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
 
   if (occ_s)
     for (uint32_t i = tid; i < a.m.nb; i += kThreads) occ_s[i] = (uint8_t)__ldcg(a.m.occ + i);
+  if (tid == 0) sh.nprev = 0;
   uint64_t ring_hi = a.nmoves < (uint64_t)kRing ? a.nmoves : (uint64_t)kRing;
   if (tid < 32) {
     ring_fill(a, sh.ring, 0, ring_hi, lane);
@@ -512,18 +556,27 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     if (tid < 32) {
       poll_dec(a, r, sh.d, lane);
       const Dec& d = sh.d;
-      // replica: the previous round's commits (a--, b++)
-      if (occ_s && lane < d.nacc) {
-        const int k = d.acc[lane].kind;
+      // replica = memory: the commits of the moves the PREVIOUS decision
+      // listed have landed (a--, b++); this decision's run after this
+      // round's evaluations
+      if (occ_s && lane < sh.nprev) {
+        const int k = sh.prev_kind[lane];
         if (k != 1) {
-          const uint32_t ba = mbrick(a.m, d.acc[lane].pt1);
+          const uint32_t ba = mbrick(a.m, sh.prev_pt1[lane]);
           atomicSub(occ_w + (ba >> 2), 1u << (8 * (ba & 3)));
         }
         if (k != 2) {
-          const uint32_t bb = mbrick(a.m, d.acc[lane].pt0);
+          const uint32_t bb = mbrick(a.m, sh.prev_pt0[lane]);
           atomicAdd(occ_w + (bb >> 2), 1u << (8 * (bb & 3)));
         }
       }
+      __syncwarp();
+      if (lane < d.nacc) {
+        sh.prev_kind[lane] = d.acc[lane].kind;
+        sh.prev_pt0[lane] = (uint32_t)d.acc[lane].pt0;
+        sh.prev_pt1[lane] = (uint32_t)d.acc[lane].pt1;
+      }
+      if (lane == 0) sh.nprev = d.nacc;
       if (lane < MG) {
         const int s = slot - g + lane;
         const int fit = d.stop ? 0 : fit_of(a, d.base);
@@ -576,33 +629,41 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         }
         int nent = 0;
         pc.mark(6);
+        // The previous round's accepted moves (this decision's list) are not
+        // committed yet: the state read here is the one before them, and
+        // their effect is added exactly (pair terms of their changed
+        // positions, occupancy counts); a candidate particle whose index they
+        // touch stops the walk.
+        uint64_t pn = kNoPoint;
         if (kind != 2) {
           if (pr.wmask != kNoMask) nent = window_bricks_mask(a.m, pr.wmask, pr.bpt, ws.brick, lane);
           else nent = win_add<T>(a.m, a.b, ws, 0, pr.x, pr.y, pr.z, lane);
-          // a window brick changed by an in-flight commit of round r-1: read after it
-          const uint64_t pn = pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z);
-          bool near = false;
-          if (lane < d.nacc) near = mnear(a.m, pn, d.acc[lane].pt0) || mnear(a.m, pn, d.acc[lane].pt1);
-          const bool anynear = __any_sync(0xffffffffu, near);
-          if (anynear && lane == 0)
-            while (ld_acquire(a.flags + kSFlag) < (uint64_t)(r - 1)) nap();
-          __syncwarp();
-          if (a.prof && r == 2 && G.i == 0 && lane == 0) {
-            a.prof[3000] = anynear;
-            a.prof[3001] = ld_acquire(a.flags + kSFlag);
-            a.prof[3002] = d.nacc;
-            a.prof[3003] = pn;
-            a.prof[3004] = d.acc[0].pt1;
-            a.prof[3005] = a.m.reach;
-            a.prof[3006] = d.acc[0].pt0;
-            a.prof[3007] = d.base;
+          pn = pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z);
+          const int cb = grid ? (pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z)) : -1;
+          const uint32_t bb = mbrick(a.m, pn);
+          // occupancy corrections and S(n) neighbours among the moves in flight
+          int dob = 0, docb = 0;
+          bool nearS = false;
+          if (lane < d.nacc) {
+            const AccE& A = d.acc[lane];
+            if (A.kind != 1 && mbrick(a.m, A.pt1) == bb) --dob;
+            if (A.kind != 2 && mbrick(a.m, A.pt0) == bb) ++dob;
+            if (grid && A.kind != 1 && A.co == cb) --docb;
+            if (grid && A.kind != 2 && A.cn == cb) ++docb;
+            nearS = mnear(a.m, pn, A.pt0) || mnear(a.m, pn, A.pt1);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            dob += __shfl_xor_sync(0xffffffffu, dob, o);
+            docb += __shfl_xor_sync(0xffffffffu, docb, o);
+          }
+          const unsigned nm = __ballot_sync(0xffffffffu, nearS);
+          if (lane == 0) {
+            ob = (occ_s ? (int)occ_s[bb] : __ldcg(a.m.occ + bb)) + dob;
+            if (grid) ocb = __ldcg(a.g.occ + cb) + docb;
+            G.nearS = nm;
           }
           pc.mark(7);
-          if (lane == 0) {
-            const uint32_t bb = mbrick(a.m, pn);
-            ob = occ_s ? (int)occ_s[bb] : __ldcg(a.m.occ + bb);
-            if (grid) ocb = __ldcg(a.g.occ + (pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z)));
-          }
           win_finish<T>(a.m, ws, occ_s, nent, nent, lane);
         }
         if (lane == 0) {
@@ -613,10 +674,13 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           ws.cx[0] = pr.x;
           ws.cy[0] = pr.y;
           ws.cz[0] = pr.z;
-          if (kind == 2) ws.total = 0;
+          if (kind == 2) {
+            ws.total = 0;
+            G.nearS = 0u;
+          }
         }
         pc.mark(8);
-        // the particle's e / position vs the previous round's in-flight commits
+        // the candidate particle's position / e vs the moves in flight
         if (kind != 1 && valid) {
           const uint64_t po = mpoint(a.m, xox, xoy, xoz);
           for (int k = 0; k < d.nacc; ++k) {
@@ -626,9 +690,10 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
             } else if (mnear(a.m, po, A.pt0) || mnear(a.m, po, A.pt1)) {
               const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + k;
               while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
-              const int ak = (int)__ldcg(&t->kind);
-              if (ak != 2 && within_rc(a.b, xox, xoy, xoz, __ldcg(&t->nx), __ldcg(&t->ny), __ldcg(&t->nz))) cf = true;
-              if (ak != 1 && within_rc(a.b, xox, xoy, xoz, __ldcg(&t->ox), __ldcg(&t->oy), __ldcg(&t->oz))) cf = true;
+              double cu = 0.0, cw = 0.0;
+              pair_delta(a, t, xox, xoy, xoz, cu, cw);
+              eu = __dadd_rn(eu, cu);
+              ew = __dadd_rn(ew, cw);
             }
           }
         }
@@ -644,6 +709,21 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       if (gw == lw) {
         su = __shfl_sync(0xffffffffu, su, 0);
         sw = __shfl_sync(0xffffffffu, sw, 0);
+        if (G.nearS) {  // S(n) after the moves in flight (fixed-order sum of their pair changes)
+          double cu = 0.0, cw = 0.0;
+          if ((G.nearS >> lane) & 1u) {
+            const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + lane;
+            while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
+            pair_delta(a, t, pr.x, pr.y, pr.z, cu, cw);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            cu = __dadd_rn(cu, __shfl_xor_sync(0xffffffffu, cu, o));
+            cw = __dadd_rn(cw, __shfl_xor_sync(0xffffffffu, cw, o));
+          }
+          su = __dadd_rn(su, cu);
+          sw = __dadd_rn(sw, cw);
+        }
         double du = 0.0, dw = 0.0, mu_ = 0.0, mw = 0.0, p = 0.0;
         bool slow = false;
         if (valid) {
@@ -672,6 +752,18 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const int64_t xp = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)pid, src);
           double au, aw;
           resum_excl<T>(a, ws, pr.x, pr.y, pr.z, xp, lane, au, aw);
+          if (G.nearS) {
+            double cu = 0.0, cw = 0.0;
+            if ((G.nearS >> lane) & 1u)
+              pair_delta(a, a.atab + (size_t)((r - 1) & 1) * kMaxAcc + lane, pr.x, pr.y, pr.z, cu, cw);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              cu = __dadd_rn(cu, __shfl_xor_sync(0xffffffffu, cu, o));
+              cw = __dadd_rn(cw, __shfl_xor_sync(0xffffffffu, cw, o));
+            }
+            au = __dadd_rn(au, cu);
+            aw = __dadd_rn(aw, cw);
+          }
           if (lane == src) {
             mu_ = au;
             mw = aw;
@@ -961,7 +1053,12 @@ __device__ __forceinline__ void compose_dec(uint32_t r, uint64_t base, uint64_t 
       const int kind = sh.mkind[i];
       if (f == 0) p = (uint64_t)(sh.ptn[i] & kNoPoint) | ((uint64_t)(sh.pto[i] & kNoPoint) << 24);
       else if (f == 1) p = ((uint64_t)kind << 32) | (uint64_t)(uint32_t)sh.ia[i];
-      else p = sh.ib[i] < 0 ? 0xffffffffull : (uint64_t)(uint32_t)sh.ib[i];
+      else if (f == 2) p = sh.ib[i] < 0 ? 0xffffffffull : (uint64_t)(uint32_t)sh.ib[i];
+      else {
+        const uint64_t cn = kind != 2 && sh.cn[i] >= 0 ? (uint64_t)sh.cn[i] : 0xffffffull;
+        const uint64_t co = kind != 1 && sh.co[i] >= 0 ? (uint64_t)sh.co[i] : 0xffffffull;
+        p = cn | (co << 24);
+      }
     }
     sh.dw[idx] = tagw(r, p);
   }
@@ -1155,6 +1252,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         atomicAdd(&sh.arrived, 1);
       }
       group_sync(1, kPollThreads);
+      // every evaluation of round r has read its state: the previous round's
+      // commits may store now
+      if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);
       pc.mark(1);
       if (warp == 0) {  // ---- walk (warm: warp 0 ran it on the partial masks while polling)
         const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane);
@@ -1381,7 +1481,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     ++r;
     if (stop) break;
   }
-  // the last round's commits / statistics / trace
+  if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);  // the last decision's commits
+  // the last round's statistics / trace
   if (warp >= kPollWarps) helpers(a, sh, warp, lane);
   __syncthreads();
   if (a.prof && tid == 0) {
