@@ -487,12 +487,15 @@ __device__ __noinline__ void pair_delta(const EngineArgs& a, const ATab* t, doub
   }
 }
 
-// S(n) without particle xp, re-summed by one warp over the window's
-// candidates in a fixed order (used when pair(n, x_pid) is too large to
-// subtract without losing precision).
+// S(n) after the in-flight moves in `near`, without particle xp (-1: none),
+// re-summed by one warp in a fixed order: the window's records except xp and
+// the old positions of those moves, plus the pairs with their new positions.
+// Used when a pair to subtract is too large to subtract without losing
+// precision (the mover's own pair, or an in-flight move's old position).
 template <int T>
 __device__ __noinline__ void resum_excl(const EngineArgs& a, const WinWs<T>& ws, double px, double py,
-                                        double pz, int64_t xp, int lane, double& au, double& aw) {
+                                        double pz, int64_t xp, unsigned near, const ATab* tab,
+                                        int lane, double& au, double& aw) {
   au = 0.0;
   aw = 0.0;
   for (int f = lane; f < ws.total; f += 32) {
@@ -512,15 +515,34 @@ __device__ __noinline__ void resum_excl(const EngineArgs& a, const WinWs<T>& ws,
     }
     const int idx = (int)ws.brick[e] * a.m.cap + k;
     if ((int64_t)__ldcg(a.m.rid + idx) == xp) continue;
-    const double r2 = min_image_dist2(px, py, pz, __ldcg(a.m.rx + idx), __ldcg(a.m.ry + idx),
-                                      __ldcg(a.m.rz + idx), a.b);
+    const double rx = __ldcg(a.m.rx + idx), ry = __ldcg(a.m.ry + idx), rz = __ldcg(a.m.rz + idx);
+    bool gone = false;
+    for (unsigned m = near; m; m &= m - 1) {
+      const ATab* t = tab + (__ffs(m) - 1);
+      if (__ldcg(&t->kind) != 1 && rx == __ldcg(&t->ox) && ry == __ldcg(&t->oy) && rz == __ldcg(&t->oz))
+        gone = true;
+    }
+    if (gone) continue;
+    const double r2 = min_image_dist2(px, py, pz, rx, ry, rz, a.b);
     if (r2 <= a.b.rc2) lj_accum(a.b, r2, 1.0, au, aw);
+  }
+  double cu = 0.0, cw = 0.0;
+  if ((near >> lane) & 1u) {
+    const ATab* t = tab + lane;
+    if (__ldcg(&t->kind) != 2) {
+      const double r2 = min_image_dist2(px, py, pz, __ldcg(&t->nx), __ldcg(&t->ny), __ldcg(&t->nz), a.b);
+      if (r2 <= a.b.rc2) lj_accum(a.b, r2, 1.0, cu, cw);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     au = __dadd_rn(au, __shfl_xor_sync(0xffffffffu, au, o));
     aw = __dadd_rn(aw, __shfl_xor_sync(0xffffffffu, aw, o));
+    cu = __dadd_rn(cu, __shfl_xor_sync(0xffffffffu, cu, o));
+    cw = __dadd_rn(cw, __shfl_xor_sync(0xffffffffu, cw, o));
   }
+  au = __dadd_rn(au, cu);
+  aw = __dadd_rn(aw, cw);
 }
 
 template <int T>
@@ -709,20 +731,27 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       if (gw == lw) {
         su = __shfl_sync(0xffffffffu, su, 0);
         sw = __shfl_sync(0xffffffffu, sw, 0);
+        const ATab* tabr = a.atab + (size_t)((r - 1) & 1) * kMaxAcc;
         if (G.nearS) {  // S(n) after the moves in flight (fixed-order sum of their pair changes)
           double cu = 0.0, cw = 0.0;
+          bool huge = false;
           if ((G.nearS >> lane) & 1u) {
-            const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + lane;
+            const ATab* t = tabr + lane;
             while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
             pair_delta(a, t, pr.x, pr.y, pr.z, cu, cw);
+            huge = fabs(cu) > kHugeTerm || fabs(cw) > kHugeTerm;
           }
+          if (__any_sync(0xffffffffu, huge)) {
+            resum_excl<T>(a, ws, pr.x, pr.y, pr.z, -1, G.nearS, tabr, lane, su, sw);
+          } else {
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            cu = __dadd_rn(cu, __shfl_xor_sync(0xffffffffu, cu, o));
-            cw = __dadd_rn(cw, __shfl_xor_sync(0xffffffffu, cw, o));
+            for (int o = 16; o > 0; o >>= 1) {
+              cu = __dadd_rn(cu, __shfl_xor_sync(0xffffffffu, cu, o));
+              cw = __dadd_rn(cw, __shfl_xor_sync(0xffffffffu, cw, o));
+            }
+            su = __dadd_rn(su, cu);
+            sw = __dadd_rn(sw, cw);
           }
-          su = __dadd_rn(su, cu);
-          sw = __dadd_rn(sw, cw);
         }
         double du = 0.0, dw = 0.0, mu_ = 0.0, mw = 0.0, p = 0.0;
         bool slow = false;
@@ -751,19 +780,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           sl &= sl - 1;
           const int64_t xp = (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)pid, src);
           double au, aw;
-          resum_excl<T>(a, ws, pr.x, pr.y, pr.z, xp, lane, au, aw);
-          if (G.nearS) {
-            double cu = 0.0, cw = 0.0;
-            if ((G.nearS >> lane) & 1u)
-              pair_delta(a, a.atab + (size_t)((r - 1) & 1) * kMaxAcc + lane, pr.x, pr.y, pr.z, cu, cw);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              cu = __dadd_rn(cu, __shfl_xor_sync(0xffffffffu, cu, o));
-              cw = __dadd_rn(cw, __shfl_xor_sync(0xffffffffu, cw, o));
-            }
-            au = __dadd_rn(au, cu);
-            aw = __dadd_rn(aw, cw);
-          }
+          resum_excl<T>(a, ws, pr.x, pr.y, pr.z, xp, G.nearS, tabr, lane, au, aw);
           if (lane == src) {
             mu_ = au;
             mw = aw;
