@@ -500,6 +500,14 @@ gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w) {
   return total_energy(c, u, w);
 }
 
+extern "C" gcmc_status gcmc_debug_energies(gcmc_dev* h, double* maint, double* fresh) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  return epart_dump(c, maint, fresh);
+}
+
 gcmc_status gcmc_energy_drift(gcmc_dev* h, double* max_du, double* max_dw) {
   Chain& c = *H(h);
   cudaSetDevice(c.device);
@@ -696,14 +704,24 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
           std::fprintf(stderr, "\n[engine prof] committer (per round, %llu rounds, %.2f commits, %.2f ordered): atab=%.0f move+ext=%.0f commit_load=%.0f deps=%.0f stores=%.0f ordered=%.0f fence=%.0f go_wait=%.0f",
                        cp[7], cp[9] / nr, cp[8] / nr, cp[0] / nr, cp[1] / nr, cp[2] / nr, cp[3] / nr, cp[4] / nr, cp[5] / nr, cp[6] / nr, cp[10] / nr);
         }
+        {
+          unsigned long long d2[5];
+          cudaMemcpy(d2, c.prof + 3100, sizeof d2, cudaMemcpyDeviceToHost);
+          if (d2[0]) std::fprintf(stderr, "\n[dbg] post-commit sightings=%llu last round=%llu go=%llu etrav=%llu k=%llu", d2[0], d2[1], d2[2], d2[3], d2[4]);
+          unsigned long long d3[4];
+          cudaMemcpy(d3, c.prof + 3110, sizeof d3, cudaMemcpyDeviceToHost);
+          if (d3[0]) std::fprintf(stderr, "\n[dbg] eval sightings=%llu round=%llu go=%llu sflag=%llu", d3[0], d3[1], d3[2], d3[3]);
+        }
         if (std::getenv("GCMC_ROUND_LOG")) {
+          { unsigned long long el[604]; cudaMemcpy(el, c.prof + 3300, sizeof el, cudaMemcpyDeviceToHost);
+            for (unsigned long long q = 0; q < el[0] && q < 150; ++q) std::fprintf(stderr, "\n[eupd] r=%llu k=%llu kind=%llu nb=%llu cand=%llu", el[4 + 4 * q], el[5 + 4 * q] & 255, el[5 + 4 * q] >> 8, el[6 + 4 * q], el[7 + 4 * q]); }
           unsigned long long dbg[8];
           cudaMemcpy(dbg, c.prof + 3000, sizeof dbg, cudaMemcpyDeviceToHost);
           std::fprintf(stderr, "\n[dbg] near=%llu flag=%llu nacc=%llu pn=%llx pt1=%llx reach=%llu pt0=%llx base=%llu",
                        dbg[0], dbg[1], dbg[2], dbg[3], dbg[4], dbg[5], dbg[6], dbg[7]);
           std::vector<unsigned long long> rl(800);
           cudaMemcpy(rl.data(), c.prof + 256, 800 * 8, cudaMemcpyDeviceToHost);
-          for (int q = 1; q < 12; ++q)
+          for (int q = 1; q < 40; ++q)
             std::fprintf(stderr, "\n[round %d] base=%llu len=%llu nacc=%llu cmin=%llu why=%llu", q, rl[4 * q],
                          rl[4 * q + 1], rl[4 * q + 2] & 0xffff, rl[4 * q + 2] >> 16, rl[4 * q + 3]);
         }

@@ -95,6 +95,7 @@ bool engine2_supported(const Chain& c);
 gcmc_status engine2_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
 gcmc_status epart_build(Chain& c, double2* out);
 gcmc_status epart_drift(Chain& c, double* du, double* dw);
+gcmc_status epart_dump(Chain& c, double* maint, double* fresh);
 
 // Error text in the reference's wording.
 std::string overflow_message(const Chain& c, int64_t cell, int64_t occ);
