@@ -354,15 +354,15 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
-                         "kernel": "k_engine (persistent whole-GPU Metropolis loop)",
+                         "kernel": "k_engine2 (persistent whole-GPU Metropolis loop, maintained per-particle energies)",
                          "alg_bytes_per_move": ALG_BYTES_PER_MOVE,
                          "note": "serial Markov chain: latency-bound, not HBM-bound; see "
                                  "ns_per_round and DESIGN.md"},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            # per step: one engine launch + one look-ahead proposal generation
-            # per 2^21-move chunk (gcmc_run_moves)
-            "gpu_launches": 2 * a.steps * ((a.moves_per_step + (1 << 21) - 1) >> 21),
+            # per step and 2^21-move chunk (gcmc_run_moves): the engine plus the
+            # look-ahead proposal generation (k_gen, k_annotate)
+            "gpu_launches": 3 * a.steps * ((a.moves_per_step + (1 << 21) - 1) >> 21),
             "ns_per_move": 1e9 * t_dev / moves_rank,
             "ns_per_round": 1e9 * (eng_ms / 1e3) / max(rounds, 1),
             "moves_per_round": moves_rank / max(rounds, 1),
