@@ -1285,6 +1285,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(2);
+#pragma unroll 1
+      for (int vrep = 0; vrep < a.walk_reps; ++vrep) {
+      if (vrep == 1) pc.mark(7);
       {  // ---- read / write sets of the consumed moves (one L2 hop for x_pid)
         const int len = sh.len + sh.err;  // the overflowing move's data is reported too
         const int nacc = sh.nacc;
@@ -1338,6 +1341,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           }
       }
       group_sync(1, kPollThreads);
+      pc.mark(8);
       {
         const int len = sh.len, nacc = sh.nacc;
         const int first = nacc ? sh.acc_i[0] : len;
@@ -1374,12 +1378,25 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           const int k1 = q / nacc, k2 = q % nacc;
           if (k2 >= k1) continue;
           const int i = sh.acc_i[k1], j = sh.acc_i[k2];
+          // brick prefilter (reach 2 covers 2 r_c), exact distances only when near
+          const uint32_t pi0 = sh.ptn[i], pi1 = sh.pto[i], pj0 = sh.ptn[j], pj1 = sh.pto[j];
+          auto near2 = [&](uint32_t p, uint32_t q) {
+            if (p == (uint32_t)kNoPoint || q == (uint32_t)kNoPoint) return false;
+            return axis_near(pt_x(p), pt_x(q), a.m.dims, 2) && axis_near(pt_y(p), pt_y(q), a.m.dims, 2) &&
+                   axis_near(pt_z(p), pt_z(q), a.m.dims, 2);
+          };
+          if (!(near2(pi0, pj0) || near2(pi0, pj1) || near2(pi1, pj0) || near2(pi1, pj1))) continue;
           if (far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) continue;
           atomicMin(&sh.cmin, i);
         }
+        group_sync(1, kPollThreads);
+        pc.mark(9);
       }
       group_sync(1, kPollThreads);
-      if (bm) {  // clear the bitmap words this round set
+      pc.mark(10);
+      group_sync(1, kPollThreads);
+      pc.mark(11);
+      if (bm) {  // clear the bitmap words this round set (read by the verify above: after its barrier)
         const int nacc = sh.nacc;
         for (int q = tid; q < nacc * 54; q += kPollThreads) {
           const int k = q / 54, rem = q % 54;
@@ -1390,6 +1407,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         }
       }
       group_sync(1, kPollThreads);
+      }
       pc.mark(3);
       if (tid == 0 && a.prof && r < 200) {
         a.prof[256 + 4 * r] = base;

@@ -46,7 +46,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Phase timers (GCMC_ENGINE_PROFILE=1): accumulated clock64 cycles per phase.
+// Phase timers: accumulated clock64 cycles per phase. Compiled in only with
+// -DGCMC_PHASE_TIMERS (tools/build_variant.py prof -DGCMC_PHASE_TIMERS, then
+// GCMC_LIB=... GCMC_ENGINE_PROFILE=1): twelve live 64-bit counters in every
+// thread of the persistent kernel cost registers (and spills) otherwise.
+#ifdef GCMC_PHASE_TIMERS
 struct PhaseClock {
   unsigned long long acc[12] = {0};
   unsigned long long t = 0;
@@ -66,5 +70,14 @@ struct PhaseClock {
     for (int k = 0; k < 12; ++k) p[k] = acc[k];
   }
 };
+#else
+struct PhaseClock {
+  static constexpr bool on = false;
+  unsigned long long acc[12];
+  __device__ __forceinline__ void start(bool) {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush(unsigned long long*) {}
+};
+#endif
 
 }  // namespace gcmcb
