@@ -407,7 +407,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     __syncwarp();
     slot_table_warp<MG>(a, sh.Q, 0, cta_slot0, sh.stab, lane);
   }
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   uint64_t b0 = 0;  // base the prefix Q / slot table refer to
   uint32_t r = 1;
   PhaseClock pc;
@@ -444,6 +445,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       }
       cp_async_wait();
     }
+    __syncwarp();
     __syncthreads();
     const Dec& d = sh.d;
     if (d.stop) break;
@@ -1059,7 +1061,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     __syncwarp();
     if (lane == 0) round_shape(a, sh.Q, 0, 0, sh.fit, sh.used);
   }
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   uint64_t base = 0, n = sh.ks.n;
   int bias = a.bias0;
   uint64_t rounds = 0;
@@ -1067,7 +1070,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   int rate = 0;         // drift of N per move, 1/256 units
   float rate_f = 0.0f;
   if (warp == 0) compose_dec(r, base, n, 0, bias, 0, rate, sh, lane);
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   broadcast_dec(a, sh, tid);
   PhaseClock pc, ph;
   pc.start(a.prof && tid == 0);
@@ -1275,6 +1279,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       helpers(a, sh, warp, lane);  // previous round, concurrently with the poll
       ph.mark(0);
     }
+    __syncwarp();
     __syncthreads();
     pc.mark(4);  // wait for helpers
     // -------------------- close the round
@@ -1323,6 +1328,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         ++sh.stops[sh.why];
       }
     }
+    __syncwarp();
     __syncthreads();
     if (a.stamp && tid == 0) a.stamp[8 * ((r + 1) & 8191)] = gtimer();  // publish of D_{r+1}
     broadcast_dec(a, sh, tid);
@@ -1341,6 +1347,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     } else if (tid < 32 + kMaxMoves) {
       sh.macc[tid - 32] = sh.mcov[tid - 32] = sh.mcf[tid - 32] = sh.mov[tid - 32] = 0;
     }
+    __syncwarp();
     __syncthreads();
     pc.mark(5);  // next shape (after the publish)
     ph.mark(1);
@@ -1352,7 +1359,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   }
   // the last round's commits / statistics / trace
   if (warp >= kPollWarps) helpers(a, sh, warp, lane);
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   if (a.prof && tid == 0) {
     pc.flush(a.prof);
     a.prof[15] = rounds;

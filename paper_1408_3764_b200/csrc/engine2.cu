@@ -570,7 +570,8 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     ring_fill(a, sh.ring, 0, ring_hi, lane);
     cp_async_wait();
   }
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   PhaseClock pc;
   pc.start(a.prof && blockIdx.x == 1 && tid == 0);
   for (uint32_t r = 1;; ++r) {
@@ -616,6 +617,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       }
       cp_async_wait();
     }
+    __syncwarp();
     __syncthreads();
     pc.mark(1);
     const Dec& d = sh.d;
@@ -1224,7 +1226,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     ring_fill(a, sh.ring, 0, ring_hi, lane);
     cp_async_wait();
   }
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   uint64_t base = 0, n = sh.ks.n;
   uint64_t rounds = 0, etarget = 0;  // energy updates expected through the previous round
   int fit = fit_of(a, 0);
@@ -1233,7 +1236,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     sh.nacc = 0;
     compose_dec(r, base, n, 0, 0, sh, lane);
   }
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
   PhaseClock pc;
   pc.start(a.prof && tid == 0);
@@ -1389,6 +1393,19 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           if (far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) continue;
           atomicMin(&sh.cmin, i);
         }
+#ifdef GCMC_PHASE_TIMERS
+        if (a.prof) {
+          const unsigned long long c0 = clock64();
+          atomicMax(a.prof + 3400, c0);
+          group_sync(1, kPollThreads);
+          const unsigned long long c1 = clock64();
+          atomicMax(a.prof + 3401, c1);
+          if (tid == 0) {
+            a.prof[3402] += ld_acquire(reinterpret_cast<uint64_t*>(a.prof + 3401)) - c1;
+            a.prof[3403] += c1 - c0;
+          }
+        }
+#endif
         group_sync(1, kPollThreads);
         pc.mark(9);
       }
@@ -1427,6 +1444,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     } else {
       helpers(a, sh, warp, lane);  // previous round, concurrently with the poll
     }
+    __syncwarp();
     __syncthreads();
     pc.mark(4);
     // -------------------- close the round
@@ -1494,6 +1512,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     // the previous round's energy updates must land before D_{r+1}
     if (tid == 32 * 15)
       while (ld_acquire(a.flags + kECount) < etarget) __nanosleep(a.poll_ns);
+    __syncwarp();
     __syncthreads();
     if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
     etarget += (uint64_t)nacc;
@@ -1509,6 +1528,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     }
     fit = fit_of(a, nbase);
     if (tid == 0) sh.arrived = 0;
+    __syncwarp();
     __syncthreads();
     base = nbase;
     n = nn;
@@ -1519,7 +1539,8 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);  // the last decision's commits
   // the last round's statistics / trace
   if (warp >= kPollWarps) helpers(a, sh, warp, lane);
-  __syncthreads();
+  __syncwarp();
+    __syncthreads();
   if (a.prof && tid == 0) {
     pc.flush(a.prof);
     a.prof[15] = rounds;

@@ -40,8 +40,14 @@ struct WinWs {
   double red[T / 32][2];
 };
 
+// Named barrier over a group of warps. The non-.aligned form: the warps of a
+// group reach it from lane-divergent code (one lane polling a flag, lanes
+// leaving a loop at different trip counts), where the .aligned bar.sync is
+// undefined behaviour (in practice it counts a warp as arrived when its first
+// lanes do, releasing the barrier early). The __syncwarp reconverges first.
 __device__ __forceinline__ void group_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // Warp 0 of the group, step 1 (per window): the pruned brick window of a
