@@ -67,7 +67,9 @@ constexpr int kResWords = 3;
 constexpr int kPollWarps = 12;
 constexpr int kMaxSlots = 768;            // buffer sizing: evaluator groups
 constexpr double kHugeTerm = 1e4;
-constexpr int kBitWords = 4096;          // verify bitmap: up to 131072 bricks         // |pair(n, x_pid)| above this: re-sum without pid
+constexpr int kBitWords = 4096;
+constexpr int kEBuf = 384;              // buffered energy updates per group in shared memory
+constexpr int kEBig = 4096;             // ... and in global memory beyond that          // verify bitmap: up to 131072 bricks         // |pair(n, x_pid)| above this: re-sum without pid
 
 struct OffRec {  // one candidate N offset of a slot (accepted offsets; all when tracing)
   double du, dw;  // ΔU, ΔW
@@ -95,6 +97,7 @@ struct ATab {  // accepted move k of a round, exact (sequencer -> commit groups 
 constexpr int kECount = 8;
 constexpr int kSFlag = 16;
 constexpr int kGo = 24;      // last round whose evaluations are complete (commits may store)
+constexpr int kETrav = 32;   // energy-update traversals done (cumulative)
 constexpr int kFlagWords = 64;
 
 struct EngineArgs {
@@ -116,6 +119,7 @@ struct EngineArgs {
   SlotExt* ext;     // [2][nslots]
   ATab* atab;       // [2][kMaxAcc]
   uint64_t* flags;  // see kECount / kSFlag
+  double4* ebig;    // [kMaxAcc][kEBig] energy-update overflow buffers
   int smem_occ;
   unsigned poll_ns, epoll_ns;
   int walk_reps;  // diagnostics: walk repeated (GCMC_WALK_REPS)
@@ -142,6 +146,7 @@ struct AccE {
 };
 struct Dec {
   uint64_t base, n;
+  uint64_t ctot;  // accepted moves through the listed round (cumulative, this launch)
   int nacc, stop;
   AccE acc[kMaxAcc];
 };
@@ -197,6 +202,8 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
     else if (idx == 2) {
       d.nacc = nacc;
       d.stop = (int)((p >> 9) & 1);
+    } else if (idx == 3) {
+      d.ctot = p;
     } else if (idx >= kDecHdr) {
       const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
       if (f == 0) {
@@ -223,6 +230,11 @@ template <int T>
 struct EvalShared {
   Proposal ring[kRing];
   Dec d;
+  struct EBuf {                   // buffered neighbour energy updates (energy_update)
+    uint32_t id[kEBuf];            // particle | pass << 31
+    double u[kEBuf], w[kEBuf];
+    int n;
+  } eb[kThreads / T];
   int nprev;                      // the previous decision's accepted moves (replica update)
   uint32_t prev_pt0[kMaxAcc], prev_pt1[kMaxAcc];
   int prev_kind[kMaxAcc];
@@ -239,13 +251,17 @@ struct EvalShared {
 };
 
 // The structural commits of the accepted moves of round rr (one warp, lane
-// k = accepted move k): store, reference grid and brick mirror (commit.cuh)
-// and the movers' e. Every lane loads first; a commit whose cells, bricks or
-// particles overlap an earlier one of the round is re-loaded and applied
-// after it in move order (a later insertion reusing the index an earlier
-// deletion vacated needs no order: the deletion's loads precede every store,
-// unless it is itself ordered). Then flags[kSFlag] = rr.
-__device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_t rr, int lane) {
+// k = accepted move k): store, reference grid and brick mirror (commit.cuh).
+// Everything is loaded while round rr + 1 is still being evaluated against
+// the old state; stores start once its evaluations are complete (flags[kGo]).
+// A commit whose cells, bricks or particles overlap an earlier one of the
+// round is re-loaded and applied after it in move order (a later insertion
+// reusing the index an earlier deletion vacated needs no order: the
+// deletion's loads precede every store, unless it is itself ordered). The
+// movers' e (set / relabel copy) are written in move order after the
+// round's neighbour energy updates have been applied. Then flags[kSFlag] = rr.
+__device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_t rr, uint64_t ctot,
+                                          int lane) {
   const bool mine = lane < nacc;
   const ATab* t = a.atab + (size_t)(rr & 1) * kMaxAcc + lane;
   MoveData md{};
@@ -277,11 +293,6 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     cc.mark(1);
     commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
     tc = touch_of(a.m, kind, pid, nn, c);
-    if (kind == 2 && pid != nn - 1) {
-      const double2 el = __ldcg(a.ep + (nn - 1));
-      esu = el.x;
-      esw = el.y;
-    }
   }
   cc.mark(2);
   bool dep = false;
@@ -307,22 +318,17 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     }
   }
   if (__ballot_sync(0xffffffffu, dep) & exm) dep = true;
-  auto set_e = [&]() {
-    if (kind == 0) __stcg(a.ep + pid, make_double2(esu, esw));
-    else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
-    else if (pid != nn - 1) __stcg(a.ep + pid, make_double2(esu, esw));
-  };
   cc.mark(3);
-  // stores only once the round being evaluated against the old state is done
-  if (lane == 0)
+  // stores only once the round being evaluated against the old state is
+  // done, and the round's energy updates have found their neighbours
+  if (lane == 0) {
     while (ld_acquire(a.flags + kGo) < (uint64_t)rr + 1) nap();
+    while (ld_acquire(a.flags + kETrav) < ctot) nap();
+  }
   __syncwarp();
   cc.mark(7);
   long long e1, e2, e3;
-  if (mine && !dep) {
-    commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
-    set_e();
-  }
+  if (mine && !dep) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
   const unsigned deps = __ballot_sync(0xffffffffu, dep);
   cc.mark(4);
   if (deps) {
@@ -331,21 +337,32 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     for (int j = 0; j < nacc; ++j) {
       if (((deps >> j) & 1u) && lane == j) {
         load_move(a.s, kind, pid, md);
-        if (kind == 2 && pid != nn - 1) {
-          const double2 el = __ldcg(a.ep + (nn - 1));
-          esu = el.x;
-          esw = el.y;
-        }
         commit_move(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, e1, e2, e3);
-        set_e();
       }
       __syncwarp();
     }
   }
   cc.mark(5);
+  // the movers' e, after the neighbour updates of the round (a relabel copy
+  // must carry them), in move order
+  if (lane == 0)
+    while (ld_acquire(a.flags + kECount) < ctot) nap();
+  __syncwarp();
+#pragma unroll 1
+  for (int j = 0; j < nacc; ++j) {
+    if (lane == j) {
+      if (kind == 0) __stcg(a.ep + pid, make_double2(esu, esw));
+      else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
+      else if (pid != nn - 1) __stcg(a.ep + pid, __ldcg(a.ep + (nn - 1)));
+    }
+    __syncwarp();
+  }
   if (mine) __threadfence();
   __syncwarp();
   if (lane == 0) st_release(a.flags + kSFlag, (uint64_t)rr);
+#ifdef GCMC_DBGDELAY
+  __nanosleep(3000);  // robustness test: a committer that returns late
+#endif
   cc.mark(6);
   if (cc.on) {
     for (int q = 0; q < 7; ++q) a.prof[80 + q] += cc.acc[q];
@@ -356,14 +373,19 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   }
 }
 
-// Commit task for accepted move k of round r - 1 (a reserved group): the
-// structural commit, then the energy update — the neighbours' e_j lose the
-// pair with the old position and gain the pair with the new one — once every
-// commit of the round whose bricks its windows read has landed.
+// Energy update of accepted move k of round r - 1 (a reserved group): the
+// neighbours' e_j lose the pair with the old position and gain the pair with
+// the new one. The neighbours are found on the state BEFORE the round's
+// commits while round r is being evaluated (the round's accepted moves are
+// more than 2 r_c apart, so none of them changes this move's neighbour set;
+// the mover's own record is the one at its old position); the updates are
+// buffered and applied (old window first, then new) once round r's
+// evaluations are complete, before any relabel copy of the round.
 template <int T>
 __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& sh, WinWs<T>& ws, const uint8_t* occ_s,
                               uint32_t r, int g, int gt, int gw, int lane, int bar_id) {
   auto& G = sh.gs[g];
+  auto& B = sh.eb[g];
   const uint32_t rr = r - 1;
   PhaseClock ec;
   ec.start(a.prof && G.k == 0 && gt == 0);
@@ -384,14 +406,7 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
     nent0 = nent;
     if (kind != 1) nent = win_add<T>(a.m, a.b, ws, nent, ox, oy, oz, lane);
     if (kind == 2) nent0 = nent;
-    // every commit of the round has landed (they change the records and
-    // occupancies these windows read; the replica still holds the old counts)
-    if (lane == 0) {
-      while (ld_acquire(a.flags + kSFlag) != (uint64_t)rr) nap();
-      ec.mark(1);
-    }
-    __syncwarp();
-    win_finish<T>(a.m, ws, nullptr, nent, nent0, lane);
+    win_finish<T>(a.m, ws, occ_s, nent, nent0, lane);  // replica = the state before the round's commits
     if (lane == 0) {
       G.kind = kind;
       G.nx = kind == 2 ? ox : nx;
@@ -402,23 +417,15 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
       G.oz = oz;
       G.sgn0 = kind == 2 ? -1 : 1;
       G.sgn1 = -1;
+      B.n = 0;
     }
   }
   group_sync(bar_id, T);
-  ec.mark(2);
+  ec.mark(1);
   const int total = ws.total;
   const double c0x = G.nx, c0y = G.ny, c0z = G.nz, c1x = G.ox, c1y = G.oy, c1z = G.oz;
   const double s0 = (double)G.sgn0, s1 = (double)G.sgn1;
-  // the mover's own record (displace / insert) is the one at exactly its new
-  // position, whatever id a later relabel of the round gave it
-  const bool excl = G.kind != 2;
-  // a displacement's two windows may share neighbours: the old window's
-  // updates land before the new window's (fixed order -> reproducible bits)
-  for (int pass = 0; pass < 2; ++pass) {
-  if (pass == 1) {
-    __threadfence();
-    group_sync(bar_id, T);
-  }
+  const bool has_old = G.kind != 1;
   for (int f = gt; f < total; f += T) {
     int e, k;
     if (f < kCandMax) {
@@ -435,21 +442,62 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
       k = f - ws.pre[lo];
     }
     const bool w1 = e >= ws.nent0;
-    if ((pass == 0) != (w1 || G.kind == 2)) continue;
     const int idx = (int)ws.brick[e] * a.m.cap + k;
-    const int32_t rid = __ldcg(a.m.rid + idx);
     const double rx = __ldcg(a.m.rx + idx), ry = __ldcg(a.m.ry + idx), rz = __ldcg(a.m.rz + idx);
-    if (excl && rx == c0x && ry == c0y && rz == c0z) continue;
+    if (has_old && rx == c1x && ry == c1y && rz == c1z) continue;  // the mover itself
     const double r2 = w1 ? min_image_dist2(c1x, c1y, c1z, rx, ry, rz, a.b)
                          : min_image_dist2(c0x, c0y, c0z, rx, ry, rz, a.b);
     if (r2 <= a.b.rc2) {
       double u, w;
       lj_pair_clamped(r2, a.b, u, w);
       const double sg = w1 ? s1 : s0;
-      atomicAdd(&a.ep[rid].x, __dmul_rn(sg, u));
-      atomicAdd(&a.ep[rid].y, __dmul_rn(sg, w));
+      const int32_t rid = __ldcg(a.m.rid + idx);
+      const int q = atomicAdd(&B.n, 1);
+      const int pass = (w1 || G.kind == 2) ? 0 : 1;  // old window first
+      if (q < kEBuf) {
+        B.id[q] = (uint32_t)rid | ((uint32_t)pass << 31);
+        B.u[q] = __dmul_rn(sg, u);
+        B.w[q] = __dmul_rn(sg, w);
+      } else {
+        if (q - kEBuf < kEBig) a.ebig[(size_t)G.k * kEBig + (q - kEBuf)] = make_double4(__longlong_as_double((long long)rid | ((long long)pass << 40)), __dmul_rn(sg, u), __dmul_rn(sg, w), 0.0);
+      }
     }
   }
+  __threadfence();
+  group_sync(bar_id, T);
+  if (gt == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + kETrav), 1ull);
+    while (ld_acquire(a.flags + kGo) < (uint64_t)r) nap();
+  }
+  group_sync(bar_id, T);
+  ec.mark(2);
+  const int nb = B.n;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      __threadfence();
+      group_sync(bar_id, T);
+    }
+    for (int q = gt; q < nb; q += T) {
+      uint32_t id;
+      double du, dw;
+      int ps;
+      if (q < kEBuf) {
+        id = B.id[q] & 0x7fffffffu;
+        ps = (int)(B.id[q] >> 31);
+        du = B.u[q];
+        dw = B.w[q];
+      } else {
+        const double4 v = ld_cg(a.ebig + (size_t)G.k * kEBig + (q - kEBuf));
+        const long long bits = __double_as_longlong(v.x);
+        id = (uint32_t)(bits & 0x7fffffffll);
+        ps = (int)(bits >> 40);
+        du = v.y;
+        dw = v.z;
+      }
+      if (ps != pass) continue;
+      atomicAdd(&a.ep[id].x, du);
+      atomicAdd(&a.ep[id].y, dw);
+    }
   }
   __threadfence();
   group_sync(bar_id, T);
@@ -621,9 +669,10 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     __syncthreads();
     pc.mark(1);
     const Dec& d = sh.d;
-    if (G.task == 3 && gt < 32) commit_round(a, d.nacc, r - 1, lane);
+    const bool stop_r = d.stop;  // this round's decision (sh.d is rewritten by the next decode)
+    if (G.task == 3 && gt < 32) commit_round(a, d.nacc, r - 1, d.ctot, lane);
     if (G.task == 2) energy_update<T>(a, sh, ws, occ_s, r, g, gt, gw, lane, bar_id);
-    if (d.stop) break;
+    if (stop_r) break;
     if (G.task == 1) {
       const int lw = g % (kGW < 4 ? kGW : 4);  // leader warp (groups on different sub-partitions)
       const uint64_t mv = d.base + (uint64_t)G.i;
@@ -855,6 +904,11 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       }
     }
     pc.mark(5);
+    // every warp of the CTA is done with this round's decision, tasks and
+    // shared state before warp 0 decodes the next one (a late group would
+    // otherwise read the next decision's stop flag / task)
+    __syncwarp();
+    __syncthreads();
   }
   if (a.prof && blockIdx.x == 1 && tid == 0) pc.flush(a.prof + 16);
 }
@@ -1060,12 +1114,13 @@ __device__ __noinline__ bool far_apart(const EngineArgs& a, const SeqShared& sh,
 }
 
 __device__ __forceinline__ void compose_dec(uint32_t r, uint64_t base, uint64_t n, int nacc,
-                                            int stop, SeqShared& sh, int lane) {
+                                            int stop, uint64_t ctot, SeqShared& sh, int lane) {
   for (int idx = lane; idx < kDecHdr + kDecEnt * nacc; idx += 32) {
     uint64_t p = 0;
     if (idx == 0) p = base;
     else if (idx == 1) p = n;
     else if (idx == 2) p = (uint64_t)nacc | ((uint64_t)stop << 9);
+    else if (idx == 3) p = ctot;
     else if (idx >= kDecHdr) {
       const int e = (idx - kDecHdr) / kDecEnt, f = (idx - kDecHdr) % kDecEnt;
       const int i = sh.acc_i[e];
@@ -1230,11 +1285,12 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     __syncthreads();
   uint64_t base = 0, n = sh.ks.n;
   uint64_t rounds = 0, etarget = 0;  // energy updates expected through the previous round
+  int prev_nacc = 0;
   int fit = fit_of(a, 0);
   uint32_t r = 1;
   if (warp == 0) {
     sh.nacc = 0;
-    compose_dec(r, base, n, 0, 0, sh, lane);
+    compose_dec(r, base, n, 0, 0, 0, sh, lane);
   }
   __syncwarp();
     __syncthreads();
@@ -1458,7 +1514,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     const uint64_t nn = (uint64_t)((int64_t)n + dn);
     const bool stop = nbase >= a.nmoves || sh.err;
     if (warp == 0) {
-      compose_dec(r + 1, nbase, nn, nacc, stop, sh, lane);
+      compose_dec(r + 1, nbase, nn, nacc, stop, etarget + (uint64_t)nacc, sh, lane);
     } else if (warp == 1) {  // exact accepted moves for the evaluators' e tests / updates
       if (lane < nacc) {
         const int i = sh.acc_i[lane];
@@ -1510,12 +1566,16 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
     }
     // the previous round's energy updates must land before D_{r+1}
-    if (tid == 32 * 15)
+    if (tid == 32 * 15) {
       while (ld_acquire(a.flags + kECount) < etarget) __nanosleep(a.poll_ns);
+      if (prev_nacc)
+        while (ld_acquire(a.flags + kSFlag) < (uint64_t)(r - 1)) __nanosleep(a.poll_ns);
+    }
     __syncwarp();
     __syncthreads();
     if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
     etarget += (uint64_t)nacc;
+    prev_nacc = nacc;
     pc.mark(5);
     // next round's ring (while the evaluators work)
     if (warp == 0) {
@@ -1748,7 +1808,8 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
   }
   if (!c.eng2_buf) {
     const size_t bytes = kDecStride * 8 + 2 * (size_t)kMaxSlots * kResWords * 8 +
-                         2 * (size_t)kMaxSlots * sizeof(SlotExt) + 2 * kMaxAcc * sizeof(ATab) + kFlagWords * 8;
+                         2 * (size_t)kMaxSlots * sizeof(SlotExt) + 2 * kMaxAcc * sizeof(ATab) + kFlagWords * 8 +
+                         (size_t)kMaxAcc * kEBig * sizeof(double4);
     if ((e = cudaMalloc(&c.eng2_buf, bytes))) return cuda_error(e, "alloc engine2");
     c.eng2_bytes = bytes;
   }
@@ -1762,6 +1823,8 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
   a.atab = reinterpret_cast<ATab*>(p);
   p += 2 * kMaxAcc * sizeof(ATab);
   a.flags = reinterpret_cast<uint64_t*>(p);
+  p += kFlagWords * 8;
+  a.ebig = reinterpret_cast<double4*>(p);
   {
     const char* e1 = std::getenv("GCMC_POLL_NS");
     a.poll_ns = e1 ? (unsigned)std::atoi(e1) : 64u;
