@@ -1384,102 +1384,72 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(6);  // read / write sets
-      // ---- verify: every consumed move against the accepted moves before it.
-      // A brick bitmap (bricks within reach 1 of a changed point) filters the
-      // spatial tests; index / target-cell tests are a few compares per pair.
-      const bool bm = a.m.nb <= (uint32_t)kBitWords * 32u && a.m.dims >= 3;
-      {
-        const int nacc = sh.nacc;
-        if (bm)
-          for (int q = tid; q < nacc * 54; q += kPollThreads) {
-            const int k = q / 54, rem = q % 54;
-            const int i = sh.acc_i[k];
-            const uint32_t pt = rem >= 27 ? sh.pto[i] : sh.ptn[i];
-            if (pt == (uint32_t)kNoPoint) continue;
-            const uint32_t id = nbr_brick(a.m, pt, rem % 27);
-            atomicOr(&sh.nbits[id >> 5], 1u << (id & 31));
-          }
-      }
-      group_sync(1, kPollThreads);
-      pc.mark(8);
+      // ---- verify (warp-cooperative): lane k holds accepted move k; each warp
+      // takes consumed moves i (in increasing order) and tests i against every
+      // accepted move before it at once — index overlap, the target brick /
+      // cell of i, and (brick-near, then exact distance) a changed position
+      // within r_c of a point i read. Plus: accepted moves pairwise more than
+      // 2 r_c apart (disjoint neighbour-energy updates, reproducible bits).
       {
         const int len = sh.len, nacc = sh.nacc;
-        const int first = nacc ? sh.acc_i[0] : len;
-        for (int i = first + 1 + tid; i < len; i += kPollThreads) {
-          bool c = false;
-          int kk = 0;
-          for (; kk < nacc && sh.acc_i[kk] < i; ++kk)
-            if (conflict(a, sh, i, sh.acc_i[kk])) c = true;
-          if (!c) {
-            bool hit = !bm;
-            if (bm) {
-              if (sh.ptn[i] != (uint32_t)kNoPoint) {
-                const uint32_t id = mbrick(a.m, sh.ptn[i]);
-                hit |= (sh.nbits[id >> 5] >> (id & 31)) & 1u;
-              }
-              if (sh.pto[i] != (uint32_t)kNoPoint) {
-                const uint32_t id = mbrick(a.m, sh.pto[i]);
-                hit |= (sh.nbits[id >> 5] >> (id & 31)) & 1u;
-              }
-            }
-            if (hit) {
-              const Proposal& pi = sh.ring[(base + i) % kRing];
-              for (int k = 0; k < kk && !c; ++k)
-                c = conflict_xyz(a, sh, pi, sh.ring[(base + sh.acc_i[k]) % kRing], i, sh.acc_i[k]);
-            }
-          }
-          if (c) atomicMin(&sh.cmin, i);
+        int ja = 1 << 30;
+        int64_t aa = -1, ab = -1;
+        uint32_t an = (uint32_t)kNoPoint, ao = (uint32_t)kNoPoint;
+        int acn = -1, aco = -1;
+        if (lane < nacc) {
+          ja = sh.acc_i[lane];
+          aa = sh.ia[ja];
+          ab = sh.ib[ja];
+          an = sh.ptn[ja];
+          ao = sh.pto[ja];
+          acn = sh.cn[ja];
+          aco = sh.co[ja];
         }
-        // two accepted moves of a round update disjoint sets of neighbour
-        // energies (no changed points within 2 r_c), so every e_j sees its
-        // updates in chain order whatever the round boundaries: bitwise
-        // reproducible trajectories
-        for (int q = tid; q < nacc * nacc; q += kPollThreads) {
-          const int k1 = q / nacc, k2 = q % nacc;
-          if (k2 >= k1) continue;
-          const int i = sh.acc_i[k1], j = sh.acc_i[k2];
-          // brick prefilter (reach 2 covers 2 r_c), exact distances only when near
-          const uint32_t pi0 = sh.ptn[i], pi1 = sh.pto[i], pj0 = sh.ptn[j], pj1 = sh.pto[j];
+        const uint32_t abn = an != (uint32_t)kNoPoint ? mbrick(a.m, an) : 0xffffffffu;
+        const uint32_t abo = ao != (uint32_t)kNoPoint ? mbrick(a.m, ao) : 0xffffffffu;
+        if (an == (uint32_t)kNoPoint) acn = -2;
+        if (ao == (uint32_t)kNoPoint) aco = -2;
+        const int first = nacc ? sh.acc_i[0] : len;
+#pragma unroll 1
+        for (int i = first + 1 + warp; i < len; i += kPollWarps) {
+          const int kind = sh.mkind[i];
+          const int64_t la = kind != 1 ? sh.ia[i] : -1;
+          const uint32_t ln = sh.ptn[i], lo = sh.pto[i];
+          const int lcn = sh.cn[i];
+          bool c = false;
+          if (ja < i) {
+            if (la >= 0 && (la == aa || la == ab)) c = true;
+            if (ln != (uint32_t)kNoPoint) {
+              const uint32_t lb = mbrick(a.m, ln);
+              if (lb == abo || lb == abn || (grid && (lcn == aco || lcn == acn))) c = true;
+            }
+            if (!c && ((ln != (uint32_t)kNoPoint && (mnear(a.m, ln, ao) || mnear(a.m, ln, an))) ||
+                       (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, ao) || mnear(a.m, lo, an)))))
+              c = conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + ja) % kRing], i, ja);
+          }
+          if (__any_sync(0xffffffffu, c)) {
+            if (lane == 0) atomicMin(&sh.cmin, i);
+            break;  // this warp's later moves are beyond the cut
+          }
+        }
+        // accepted pairs: warp w takes k1 = w + 1, w + 13, ...; lane = k2 < k1
+#pragma unroll 1
+        for (int k1 = warp + 1; k1 < nacc; k1 += kPollWarps) {
+          const int i = sh.acc_i[k1];
+          const uint32_t pi0 = sh.ptn[i], pi1 = sh.pto[i];
           auto near2 = [&](uint32_t p, uint32_t q) {
             if (p == (uint32_t)kNoPoint || q == (uint32_t)kNoPoint) return false;
             return axis_near(pt_x(p), pt_x(q), a.m.dims, 2) && axis_near(pt_y(p), pt_y(q), a.m.dims, 2) &&
                    axis_near(pt_z(p), pt_z(q), a.m.dims, 2);
           };
-          if (!(near2(pi0, pj0) || near2(pi0, pj1) || near2(pi1, pj0) || near2(pi1, pj1))) continue;
-          if (far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) continue;
-          atomicMin(&sh.cmin, i);
-        }
-#ifdef GCMC_PHASE_TIMERS
-        if (a.prof) {
-          const unsigned long long c0 = clock64();
-          atomicMax(a.prof + 3400, c0);
-          group_sync(1, kPollThreads);
-          const unsigned long long c1 = clock64();
-          atomicMax(a.prof + 3401, c1);
-          if (tid == 0) {
-            a.prof[3402] += ld_acquire(reinterpret_cast<uint64_t*>(a.prof + 3401)) - c1;
-            a.prof[3403] += c1 - c0;
-          }
-        }
-#endif
-        group_sync(1, kPollThreads);
-        pc.mark(9);
-      }
-      group_sync(1, kPollThreads);
-      pc.mark(10);
-      group_sync(1, kPollThreads);
-      pc.mark(11);
-      if (bm) {  // clear the bitmap words this round set (read by the verify above: after its barrier)
-        const int nacc = sh.nacc;
-        for (int q = tid; q < nacc * 54; q += kPollThreads) {
-          const int k = q / 54, rem = q % 54;
-          const int i = sh.acc_i[k];
-          const uint32_t pt = rem >= 27 ? sh.pto[i] : sh.ptn[i];
-          if (pt == (uint32_t)kNoPoint) continue;
-          sh.nbits[nbr_brick(a.m, pt, rem % 27) >> 5] = 0u;
+          bool c = false;
+          if (lane < k1 && (near2(pi0, an) || near2(pi0, ao) || near2(pi1, an) || near2(pi1, ao)))
+            c = !far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + ja) % kRing], i, ja);
+          if (__any_sync(0xffffffffu, c) && lane == 0) atomicMin(&sh.cmin, i);
         }
       }
       group_sync(1, kPollThreads);
+      pc.mark(9);
       }
       pc.mark(3);
       if (tid == 0 && a.prof && r < 200) {
