@@ -1346,7 +1346,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       group_sync(1, kPollThreads);
       pc.mark(2);
 #pragma unroll 1
-      for (int vrep = 0; vrep < a.walk_reps; ++vrep) {
+      for (int vrep = 0; vrep < (a.walk_reps == 2 ? 2 : 1); ++vrep) {
       if (vrep == 1) pc.mark(7);
       {  // ---- read / write sets of the consumed moves (one L2 hop for x_pid)
         const int len = sh.len + sh.err;  // the overflowing move's data is reported too
@@ -1411,7 +1411,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         if (ao == (uint32_t)kNoPoint) aco = -2;
         const int first = nacc ? sh.acc_i[0] : len;
 #pragma unroll 1
-        for (int i = first + 1 + warp; i < len; i += kPollWarps) {
+        for (int i = first + 1 + warp; i < len && a.walk_reps != 5; i += kPollWarps) {
           const int kind = sh.mkind[i];
           const int64_t la = kind != 1 ? sh.ia[i] : -1;
           const uint32_t ln = sh.ptn[i], lo = sh.pto[i];
@@ -1434,7 +1434,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         }
         // accepted pairs: warp w takes k1 = w + 1, w + 13, ...; lane = k2 < k1
 #pragma unroll 1
-        for (int k1 = warp + 1; k1 < nacc; k1 += kPollWarps) {
+        for (int k1 = warp + 1; k1 < nacc && a.walk_reps != 5; k1 += kPollWarps) {
           const int i = sh.acc_i[k1];
           const uint32_t pi0 = sh.ptn[i], pi1 = sh.pto[i];
           auto near2 = [&](uint32_t p, uint32_t q) {
