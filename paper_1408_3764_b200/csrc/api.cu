@@ -698,11 +698,11 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
         for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[16 + k] / R);
         const double ne = (double)(xp[68] ? xp[68] : 1);
         {
-          unsigned long long cp[11];
+          unsigned long long cp[12];
           cudaMemcpy(cp, c.prof + 80, sizeof cp, cudaMemcpyDeviceToHost);
           const double nr = (double)(cp[7] ? cp[7] : 1);
-          std::fprintf(stderr, "\n[engine prof] committer (per round, %llu rounds, %.2f commits, %.2f ordered): atab=%.0f move+ext=%.0f commit_load=%.0f deps=%.0f stores=%.0f ordered=%.0f fence=%.0f go_wait=%.0f",
-                       cp[7], cp[9] / nr, cp[8] / nr, cp[0] / nr, cp[1] / nr, cp[2] / nr, cp[3] / nr, cp[4] / nr, cp[5] / nr, cp[6] / nr, cp[10] / nr);
+          std::fprintf(stderr, "\n[engine prof] committer (per round, %llu rounds, %.2f commits, %.2f ordered): atab=%.0f move+ext=%.0f commit_load=%.0f deps=%.0f stores=%.0f ordered=%.0f fence=%.0f go_wait=%.0f forwarded=%.2f",
+                       cp[7], cp[9] / nr, cp[8] / nr, cp[0] / nr, cp[1] / nr, cp[2] / nr, cp[3] / nr, cp[4] / nr, cp[5] / nr, cp[6] / nr, cp[10] / nr, cp[11] / nr);
         }
         {
           unsigned long long d2[5];

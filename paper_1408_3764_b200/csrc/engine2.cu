@@ -295,6 +295,34 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     tc = touch_of(a.m, kind, pid, nn, c);
   }
   cc.mark(2);
+  // Forwarding: a deletion that relabels a particle inserted earlier in this
+  // round takes that particle's data (position, reference slot, record) from
+  // the insertion's lane instead of waiting for its stores; its own stores
+  // then follow the insertion's (pass B below).
+  int fsrc = -1;
+  {
+    const int64_t myq = (mine && kind == 2 && pid != nn - 1) ? (int64_t)(nn - 1) : -2;
+#pragma unroll 1
+    for (int j = 0; j < nacc - 1; ++j) {
+      const int kj = __shfl_sync(0xffffffffu, kind, j);
+      const uint64_t nnj = __shfl_sync(0xffffffffu, nn, j);
+      if (j < lane && kj == 1 && (int64_t)nnj == myq) fsrc = j;
+    }
+    const int f = fsrc >= 0 ? fsrc : lane;
+    const double fx = __shfl_sync(0xffffffffu, md.nx, f), fy = __shfl_sync(0xffffffffu, md.ny, f),
+                 fz = __shfl_sync(0xffffffffu, md.nz, f);
+    const int focb = __shfl_sync(0xffffffffu, c.occ_cb, f), fcb = __shfl_sync(0xffffffffu, c.cb, f);
+    const int fbb = __shfl_sync(0xffffffffu, c.bb, f), fobb = __shfl_sync(0xffffffffu, c.occ_bb, f);
+    if (fsrc >= 0) {
+      c.qx = fx;
+      c.qy = fy;
+      c.qz = fz;
+      c.rslot_q = focb;
+      c.bslot_q = fbb * a.m.cap + fobb;
+      c.cl = fcb;
+      tc = touch_of(a.m, kind, pid, nn, c);
+    }
+  }
   bool dep = false;
   unsigned exm = 0;
 #pragma unroll 1
@@ -314,10 +342,23 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
         tm.part[0] = -1;
         exm |= 1u << j;
       }
+      if (j == fsrc) {  // the forwarded particle's index, cell and record are expected
+        tm.part[1] = -1;
+        tm.cell[2] = -1;
+        tm.brick[2] = -1;
+      }
       if (touches(tm, tj)) dep = true;
     }
   }
-  if (__ballot_sync(0xffffffffu, dep) & exm) dep = true;
+  // an exempted / forwarded commit is ordered after its partner when the
+  // partner itself is (it then loads or stores late)
+#pragma unroll 1
+  for (int it = 0; it < 32; ++it) {
+    const unsigned b = __ballot_sync(0xffffffffu, dep);
+    const bool nd = dep || (b & exm) || (fsrc >= 0 && ((b >> fsrc) & 1u));
+    if (__ballot_sync(0xffffffffu, nd) == b) break;
+    dep = nd;
+  }
   cc.mark(3);
   // stores only once the round being evaluated against the old state is
   // done, and the round's energy updates have found their neighbours
@@ -328,7 +369,9 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   __syncwarp();
   cc.mark(7);
   long long e1, e2, e3;
-  if (mine && !dep) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+  if (mine && !dep && fsrc < 0) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+  __syncwarp();  // pass B: forwarded deletions after their insertions
+  if (mine && !dep && fsrc >= 0) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
   const unsigned deps = __ballot_sync(0xffffffffu, dep);
   cc.mark(4);
   if (deps) {
@@ -357,18 +400,23 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     }
     __syncwarp();
   }
-  if (mine) __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release(a.flags + kSFlag, (uint64_t)rr);
+  __syncwarp();  // every lane's stores happen-before lane 0's (cumulative) release
+  if (lane == 0) {
+    __threadfence();
+    st_release(a.flags + kSFlag, (uint64_t)rr);
+  }
 #ifdef GCMC_DBGDELAY
   __nanosleep(3000);  // robustness test: a committer that returns late
 #endif
   cc.mark(6);
+  const unsigned fwd_mask = __ballot_sync(0xffffffffu, fsrc >= 0 && !dep);
+  (void)fwd_mask;
   if (cc.on) {
     for (int q = 0; q < 7; ++q) a.prof[80 + q] += cc.acc[q];
     a.prof[90] += cc.acc[7];
     a.prof[87] += 1;
     a.prof[88] += (unsigned long long)__popc(deps);
+    a.prof[91] += (unsigned long long)__popc(fwd_mask);
     a.prof[89] += (unsigned long long)nacc;
   }
 }
