@@ -980,6 +980,7 @@ struct SeqShared {
   uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
   uint8_t mkind[kMaxMoves];
   int len, nacc, err, cmin, why, dend, arrived;
+  unsigned long long vmax, vsum;  // diagnostics
   int wscr_i[kMaxAcc], wscr_d[kMaxAcc];  // walk dry runs (discarded)
   int8_t wscr_k[kMaxMoves];
   int acc_i[kMaxAcc], acc_d[kMaxAcc];
@@ -1192,6 +1193,7 @@ __device__ __forceinline__ void compose_dec(uint32_t r, uint64_t base, uint64_t 
 __device__ __noinline__ void helpers(const EngineArgs& a, SeqShared& sh, int warp, int lane) {
   const Round& D = sh.done;
   if (D.len == 0) return;
+  if (a.walk_reps == 6) return;  // diagnostics only (statistics / trace skipped)
   auto ext_of = [&](int s) -> const SlotExt* {
     const SlotExt* ex = a.ext + (size_t)D.par * a.nslots + s;
     while (ld_acquire(&ex->tag) != (uint64_t)D.r) nap();
@@ -1321,6 +1323,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     sh.done.len = 0;
     sh.done.nacc = 0;
     sh.arrived = 0;
+    sh.vmax = sh.vsum = 0;
     sh.err = 0;
     for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
   }
@@ -1432,70 +1435,68 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(6);  // read / write sets
-      // ---- verify (warp-cooperative): lane k holds accepted move k; each warp
-      // takes consumed moves i (in increasing order) and tests i against every
-      // accepted move before it at once — index overlap, the target brick /
-      // cell of i, and (brick-near, then exact distance) a changed position
-      // within r_c of a point i read. Plus: accepted moves pairwise more than
-      // 2 r_c apart (disjoint neighbour-energy updates, reproducible bits).
+      // ---- verify: one thread per consumed move i, against every accepted
+      // move before it (their data read from shared memory, broadcast):
+      // index overlap, the target brick / cell of i, and (brick-near, then
+      // exact distance) a changed position within r_c of a point i read. An
+      // accepted move is also checked against the accepted moves before it:
+      // more than 2 r_c apart (disjoint neighbour-energy updates, so every e_j
+      // sees its updates in chain order: reproducible bits).
+#ifdef GCMC_PHASE_TIMERS
+      const unsigned long long vt0 = clock64();
+#endif
       {
         const int len = sh.len, nacc = sh.nacc;
-        int ja = 1 << 30;
-        int64_t aa = -1, ab = -1;
-        uint32_t an = (uint32_t)kNoPoint, ao = (uint32_t)kNoPoint;
-        int acn = -1, aco = -1;
-        if (lane < nacc) {
-          ja = sh.acc_i[lane];
-          aa = sh.ia[ja];
-          ab = sh.ib[ja];
-          an = sh.ptn[ja];
-          ao = sh.pto[ja];
-          acn = sh.cn[ja];
-          aco = sh.co[ja];
-        }
-        const uint32_t abn = an != (uint32_t)kNoPoint ? mbrick(a.m, an) : 0xffffffffu;
-        const uint32_t abo = ao != (uint32_t)kNoPoint ? mbrick(a.m, ao) : 0xffffffffu;
-        if (an == (uint32_t)kNoPoint) acn = -2;
-        if (ao == (uint32_t)kNoPoint) aco = -2;
         const int first = nacc ? sh.acc_i[0] : len;
 #pragma unroll 1
-        for (int i = first + 1 + warp; i < len && a.walk_reps != 5; i += kPollWarps) {
+        for (int i = first + 1 + tid; i < len && a.walk_reps != 5; i += kPollThreads) {
           const int kind = sh.mkind[i];
           const int64_t la = kind != 1 ? sh.ia[i] : -1;
           const uint32_t ln = sh.ptn[i], lo = sh.pto[i];
-          const int lcn = sh.cn[i];
+          const uint32_t lb = ln != (uint32_t)kNoPoint ? mbrick(a.m, ln) : 0xfffffffeu;
+          const int lcn = ln != (uint32_t)kNoPoint ? sh.cn[i] : -3;
+          const int ki = sh.acck[i];  // >= 0: i itself is accepted (k-th)
           bool c = false;
-          if (ja < i) {
-            if (la >= 0 && (la == aa || la == ab)) c = true;
-            if (ln != (uint32_t)kNoPoint) {
-              const uint32_t lb = mbrick(a.m, ln);
-              if (lb == abo || lb == abn || (grid && (lcn == aco || lcn == acn))) c = true;
-            }
-            if (!c && ((ln != (uint32_t)kNoPoint && (mnear(a.m, ln, ao) || mnear(a.m, ln, an))) ||
-                       (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, ao) || mnear(a.m, lo, an)))))
-              c = conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + ja) % kRing], i, ja);
-          }
-          if (__any_sync(0xffffffffu, c)) {
-            if (lane == 0) atomicMin(&sh.cmin, i);
-            break;  // this warp's later moves are beyond the cut
-          }
-        }
-        // accepted pairs: warp w takes k1 = w + 1, w + 13, ...; lane = k2 < k1
 #pragma unroll 1
-        for (int k1 = warp + 1; k1 < nacc && a.walk_reps != 5; k1 += kPollWarps) {
-          const int i = sh.acc_i[k1];
-          const uint32_t pi0 = sh.ptn[i], pi1 = sh.pto[i];
-          auto near2 = [&](uint32_t p, uint32_t q) {
-            if (p == (uint32_t)kNoPoint || q == (uint32_t)kNoPoint) return false;
-            return axis_near(pt_x(p), pt_x(q), a.m.dims, 2) && axis_near(pt_y(p), pt_y(q), a.m.dims, 2) &&
-                   axis_near(pt_z(p), pt_z(q), a.m.dims, 2);
-          };
-          bool c = false;
-          if (lane < k1 && (near2(pi0, an) || near2(pi0, ao) || near2(pi1, an) || near2(pi1, ao)))
-            c = !far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + ja) % kRing], i, ja);
-          if (__any_sync(0xffffffffu, c) && lane == 0) atomicMin(&sh.cmin, i);
+          for (int k = 0; k < nacc; ++k) {
+            const int j = sh.acc_i[k];
+            if (j >= i) break;
+            const int64_t aa = sh.ia[j], ab = sh.ib[j];
+            const uint32_t an = sh.ptn[j], ao = sh.pto[j];
+            if (la >= 0 && (la == aa || la == ab)) { c = true; break; }
+            if ((ao != (uint32_t)kNoPoint && (lb == mbrick(a.m, ao) || (grid && lcn == sh.co[j]))) ||
+                (an != (uint32_t)kNoPoint && (ln == an || (grid && lcn == sh.cn[j])))) { c = true; break; }
+            if ((ln != (uint32_t)kNoPoint && (mnear(a.m, ln, ao) || mnear(a.m, ln, an))) ||
+                (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, ao) || mnear(a.m, lo, an)))) {
+              if (conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
+            }
+            if (ki >= 0) {  // two accepted moves: changed points more than 2 r_c apart
+              auto near2 = [&](uint32_t p, uint32_t q) {
+                if (p == (uint32_t)kNoPoint || q == (uint32_t)kNoPoint) return false;
+                return axis_near(pt_x(p), pt_x(q), a.m.dims, 2) && axis_near(pt_y(p), pt_y(q), a.m.dims, 2) &&
+                       axis_near(pt_z(p), pt_z(q), a.m.dims, 2);
+              };
+              if ((near2(ln, an) || near2(ln, ao) || near2(lo, an) || near2(lo, ao)) &&
+                  !far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
+            }
+          }
+          if (c) atomicMin(&sh.cmin, i);
         }
       }
+#ifdef GCMC_PHASE_TIMERS
+      if (a.prof && lane == 0) {
+        const unsigned long long d = clock64() - vt0;
+        atomicMax(&sh.vmax, d);
+        atomicAdd(&sh.vsum, d);
+      }
+      group_sync(1, kPollThreads);
+      if (a.prof && tid == 0) {
+        a.prof[3500] += sh.vmax;
+        a.prof[3501] += sh.vsum / kPollWarps;
+        sh.vmax = 0;
+        sh.vsum = 0;
+      }
+#endif
       group_sync(1, kPollThreads);
       pc.mark(9);
       }
