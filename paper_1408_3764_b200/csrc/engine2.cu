@@ -54,10 +54,13 @@ namespace gcmcb {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kMaxMoves = 256;            // moves per round
+#ifndef GCMC_E2_MOVES
+#define GCMC_E2_MOVES 256
+#endif
+constexpr int kMaxMoves = GCMC_E2_MOVES;  // moves per round
 constexpr int kMH = kMaxMoves / 32;       // moves per walk lane
 constexpr int kMaxAcc = 32;               // accepted moves per round (= reserved e-update groups)
-constexpr int kRing = 512;                // proposal ring (>= 2 * kMaxMoves)
+constexpr int kRing = 2 * kMaxMoves;      // proposal ring (>= 2 * kMaxMoves)
 constexpr int kHalf = 16;                 // N offsets d = -16..15 <-> bit d + 16
 constexpr int kDecHdr = 4;
 constexpr int kDecEnt = 4;
