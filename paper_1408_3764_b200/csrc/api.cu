@@ -712,9 +712,9 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
           unsigned long long d2[5];
           cudaMemcpy(d2, c.prof + 3100, sizeof d2, cudaMemcpyDeviceToHost);
           if (d2[0]) std::fprintf(stderr, "\n[dbg] post-commit sightings=%llu last round=%llu go=%llu etrav=%llu k=%llu", d2[0], d2[1], d2[2], d2[3], d2[4]);
-          unsigned long long d5[2];
+          unsigned long long d5[4];
           cudaMemcpy(d5, c.prof + 3500, sizeof d5, cudaMemcpyDeviceToHost);
-          std::fprintf(stderr, "\n[dbg] verify per warp: max=%.0f mean=%.0f", d5[0] / R, d5[1] / R);
+          std::fprintf(stderr, "\n[dbg] verify per warp: max=%.0f mean=%.0f iters/round=%.1f xyz calls/round=%.2f", d5[0] / R, d5[1] / R, d5[2] / R, d5[3] / R);
           unsigned long long d4[4];
           cudaMemcpy(d4, c.prof + 3400, sizeof d4, cudaMemcpyDeviceToHost);
           std::fprintf(stderr, "\n[dbg] barrier: tid0 wait=%.0f last-arrival-after-tid0=%.0f", d4[3] / R, d4[2] / R);

@@ -984,6 +984,7 @@ struct SeqShared {
   uint8_t mkind[kMaxMoves];
   int len, nacc, err, cmin, why, dend, arrived;
   unsigned long long vmax, vsum;  // diagnostics
+  unsigned viters, vcalls;
   int wscr_i[kMaxAcc], wscr_d[kMaxAcc];  // walk dry runs (discarded)
   int8_t wscr_k[kMaxMoves];
   int acc_i[kMaxAcc], acc_d[kMaxAcc];
@@ -1327,6 +1328,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     sh.done.nacc = 0;
     sh.arrived = 0;
     sh.vmax = sh.vsum = 0;
+    sh.viters = sh.vcalls = 0;
     sh.err = 0;
     for (int k = 0; k < kNStop; ++k) sh.stops[k] = 0;
   }
@@ -1469,8 +1471,14 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             if (la >= 0 && (la == aa || la == ab)) { c = true; break; }
             if ((ao != (uint32_t)kNoPoint && (lb == mbrick(a.m, ao) || (grid && lcn == sh.co[j]))) ||
                 (an != (uint32_t)kNoPoint && (ln == an || (grid && lcn == sh.cn[j])))) { c = true; break; }
+#ifdef GCMC_PHASE_TIMERS
+            if (a.prof) atomicAdd(&sh.viters, 1u);
+#endif
             if ((ln != (uint32_t)kNoPoint && (mnear(a.m, ln, ao) || mnear(a.m, ln, an))) ||
                 (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, ao) || mnear(a.m, lo, an)))) {
+#ifdef GCMC_PHASE_TIMERS
+              if (a.prof) atomicAdd(&sh.vcalls, 1u);
+#endif
               if (conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
             }
             if (ki >= 0) {  // two accepted moves: changed points more than 2 r_c apart
@@ -1496,6 +1504,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       if (a.prof && tid == 0) {
         a.prof[3500] += sh.vmax;
         a.prof[3501] += sh.vsum / kPollWarps;
+        a.prof[3502] += sh.viters;
+        a.prof[3503] += sh.vcalls;
+        sh.viters = sh.vcalls = 0;
         sh.vmax = 0;
         sh.vsum = 0;
       }
@@ -1669,10 +1680,18 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
 template <int T>
 __global__ void __launch_bounds__(kThreads, 1) k_engine2(EngineArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  // The arguments live in shared memory: the engine passes them by reference
+  // to out-of-line functions, which makes the compiler copy a by-value kernel
+  // parameter to the local-memory stack — every field read (m.dims, b.rc2, ...)
+  // would then be a local load, an L2 round trip with the L1 given to shared
+  // memory.
+  __shared__ EngineArgs sa;
+  if (threadIdx.x == 0) sa = a;
+  __syncthreads();
   if (blockIdx.x == 0)
-    sequencer(a, smem);
+    sequencer(sa, smem);
   else
-    evaluator<T>(a, smem);
+    evaluator<T>(sa, smem);
 }
 
 // e[i] from scratch: one thread per particle over its 3x3x3 brick window
