@@ -978,15 +978,8 @@ struct Round {  // a decided round, handed to the helper warps
 
 enum Stop { kStopEnd, kStopRange, kStopPrev, kStopVerify, kStopFull, kStopOverflow, kNStop };
 
-struct AccV {  // an accepted move's write set, packed for the verify
-  int j, ia, ib;
-  uint32_t an, ao, bn, bo;
-  int cn, co;
-};
-
 struct SeqShared {
   Proposal ring[kRing];
-  AccV av[kMaxAcc];
   uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
   uint8_t mkind[kMaxMoves];
   int len, nacc, err, cmin, why, dend, arrived;
@@ -1460,59 +1453,42 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       {
         const int len = sh.len, nacc = sh.nacc;
         const int first = nacc ? sh.acc_i[0] : len;
-        // accepted moves, packed once (one 32-B record each, broadcast reads)
-        if (tid < nacc) {
-          const int j = sh.acc_i[tid];
-          AccV v;
-          v.j = j;
-          v.ia = (int)sh.ia[j];
-          v.ib = (int)sh.ib[j];
-          v.an = sh.ptn[j];
-          v.ao = sh.pto[j];
-          v.bn = v.an != (uint32_t)kNoPoint ? mbrick(a.m, v.an) : 0xfffffffdu;
-          v.bo = v.ao != (uint32_t)kNoPoint ? mbrick(a.m, v.ao) : 0xfffffffdu;
-          v.cn = v.an != (uint32_t)kNoPoint ? sh.cn[j] : -4;
-          v.co = v.ao != (uint32_t)kNoPoint ? sh.co[j] : -4;
-          sh.av[tid] = v;
-        }
-        group_sync(1, kPollThreads);
 #pragma unroll 1
         for (int i = first + 1 + tid; i < len && a.walk_reps != 5; i += kPollThreads) {
           const int kind = sh.mkind[i];
-          const int la = kind != 1 ? (int)sh.ia[i] : -5;
+          const int64_t la = kind != 1 ? sh.ia[i] : -1;
           const uint32_t ln = sh.ptn[i], lo = sh.pto[i];
           const uint32_t lb = ln != (uint32_t)kNoPoint ? mbrick(a.m, ln) : 0xfffffffeu;
-          const int lcn = ln != (uint32_t)kNoPoint && grid ? sh.cn[i] : -3;
-          const bool acc_i = sh.acck[i] >= 0;
-          // all accepted moves before i, without early exit (independent iterations)
-          unsigned hard = 0, soft = 0;
-#pragma unroll 4
+          const int lcn = ln != (uint32_t)kNoPoint ? sh.cn[i] : -3;
+          const int ki = sh.acck[i];  // >= 0: i itself is accepted (k-th)
+          bool c = false;
+#pragma unroll 1
           for (int k = 0; k < nacc; ++k) {
-            const AccV v = sh.av[k];
-            const bool before = v.j < i;
-            const bool h = (la >= 0 && (la == v.ia || la == v.ib)) || lb == v.bo || lb == v.bn ||
-                           lcn == v.co || lcn == v.cn;
-            const bool nr = (ln != (uint32_t)kNoPoint && (mnear(a.m, ln, v.ao) || mnear(a.m, ln, v.an))) ||
-                            (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, v.ao) || mnear(a.m, lo, v.an)));
-            hard |= (before && h) ? 1u << k : 0u;
-            soft |= (before && !h && (nr || acc_i)) ? 1u << k : 0u;
-          }
-          bool c = hard != 0;
-          // rare: exact distances for brick-near pairs; accepted pairs 2 r_c apart
-          for (unsigned m = soft; m && !c; m &= m - 1) {
-            const int k = __ffs(m) - 1;
-            const AccV v = sh.av[k];
-            const bool nr = (ln != (uint32_t)kNoPoint && (mnear(a.m, ln, v.ao) || mnear(a.m, ln, v.an))) ||
-                            (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, v.ao) || mnear(a.m, lo, v.an)));
-            if (nr && conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + v.j) % kRing], i, v.j)) c = true;
-            if (!c && acc_i) {
+            const int j = sh.acc_i[k];
+            if (j >= i) break;
+            const int64_t aa = sh.ia[j], ab = sh.ib[j];
+            const uint32_t an = sh.ptn[j], ao = sh.pto[j];
+            if (la >= 0 && (la == aa || la == ab)) { c = true; break; }
+            if ((ao != (uint32_t)kNoPoint && (lb == mbrick(a.m, ao) || (grid && lcn == sh.co[j]))) ||
+                (an != (uint32_t)kNoPoint && (ln == an || (grid && lcn == sh.cn[j])))) { c = true; break; }
+#ifdef GCMC_PHASE_TIMERS
+            if (a.prof) atomicAdd(&sh.viters, 1u);
+#endif
+            if ((ln != (uint32_t)kNoPoint && (mnear(a.m, ln, ao) || mnear(a.m, ln, an))) ||
+                (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, ao) || mnear(a.m, lo, an)))) {
+#ifdef GCMC_PHASE_TIMERS
+              if (a.prof) atomicAdd(&sh.vcalls, 1u);
+#endif
+              if (conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
+            }
+            if (ki >= 0) {  // two accepted moves: changed points more than 2 r_c apart
               auto near2 = [&](uint32_t p, uint32_t q) {
                 if (p == (uint32_t)kNoPoint || q == (uint32_t)kNoPoint) return false;
                 return axis_near(pt_x(p), pt_x(q), a.m.dims, 2) && axis_near(pt_y(p), pt_y(q), a.m.dims, 2) &&
                        axis_near(pt_z(p), pt_z(q), a.m.dims, 2);
               };
-              if ((near2(ln, v.an) || near2(ln, v.ao) || near2(lo, v.an) || near2(lo, v.ao)) &&
-                  !far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + v.j) % kRing], i, v.j)) c = true;
+              if ((near2(ln, an) || near2(ln, ao) || near2(lo, an) || near2(lo, ao)) &&
+                  !far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
             }
           }
           if (c) atomicMin(&sh.cmin, i);
