@@ -978,8 +978,31 @@ struct Round {  // a decided round, handed to the helper warps
 
 enum Stop { kStopEnd, kStopRange, kStopPrev, kStopVerify, kStopFull, kStopOverflow, kNStop };
 
+struct AccV {  // an accepted move's write set, packed for the verify
+  int j, ia, ib;
+  uint32_t an, ao, bn, bo;
+  int cn, co;
+};
+
+// 1 when both packed brick points exist and lie within r bricks of each
+// other on every axis (cyclic), computed without branches.
+__device__ __forceinline__ unsigned near_bits(uint32_t p, uint32_t q, int d, int r) {
+  int dx = (int)(p & 0xffu) - (int)(q & 0xffu);
+  int dy = (int)((p >> 8) & 0xffu) - (int)((q >> 8) & 0xffu);
+  int dz = (int)((p >> 16) & 0xffu) - (int)((q >> 16) & 0xffu);
+  dx = abs(dx);
+  dy = abs(dy);
+  dz = abs(dz);
+  dx = min(dx, d - dx);
+  dy = min(dy, d - dy);
+  dz = min(dz, d - dz);
+  return (unsigned)(p != (uint32_t)kNoPoint) & (unsigned)(q != (uint32_t)kNoPoint) & (unsigned)(dx <= r) &
+         (unsigned)(dy <= r) & (unsigned)(dz <= r);
+}
+
 struct SeqShared {
   Proposal ring[kRing];
+  AccV av[kMaxAcc];
   uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
   uint8_t mkind[kMaxMoves];
   int len, nacc, err, cmin, why, dend, arrived;
@@ -1453,42 +1476,58 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       {
         const int len = sh.len, nacc = sh.nacc;
         const int first = nacc ? sh.acc_i[0] : len;
+        // the accepted moves' write sets, packed once (broadcast reads below)
+        if (tid < nacc) {
+          const int j = sh.acc_i[tid];
+          AccV v;
+          v.j = j;
+          v.ia = (int)sh.ia[j];
+          v.ib = (int)sh.ib[j];
+          v.an = sh.ptn[j];
+          v.ao = sh.pto[j];
+          v.bn = v.an != (uint32_t)kNoPoint ? mbrick(a.m, v.an) : 0xfffffffdu;
+          v.bo = v.ao != (uint32_t)kNoPoint ? mbrick(a.m, v.ao) : 0xfffffffdu;
+          v.cn = v.an != (uint32_t)kNoPoint && grid ? sh.cn[j] : -4;
+          v.co = v.ao != (uint32_t)kNoPoint && grid ? sh.co[j] : -4;
+          sh.av[tid] = v;
+        }
+        group_sync(1, kPollThreads);
+        const int dm = a.m.dims, rch = a.m.reach;
 #pragma unroll 1
         for (int i = first + 1 + tid; i < len && a.walk_reps != 5; i += kPollThreads) {
           const int kind = sh.mkind[i];
-          const int64_t la = kind != 1 ? sh.ia[i] : -1;
+          const int la = kind != 1 ? (int)sh.ia[i] : -5;
           const uint32_t ln = sh.ptn[i], lo = sh.pto[i];
           const uint32_t lb = ln != (uint32_t)kNoPoint ? mbrick(a.m, ln) : 0xfffffffeu;
-          const int lcn = ln != (uint32_t)kNoPoint ? sh.cn[i] : -3;
-          const int ki = sh.acck[i];  // >= 0: i itself is accepted (k-th)
-          bool c = false;
-#pragma unroll 1
+          const int lcn = ln != (uint32_t)kNoPoint && grid ? sh.cn[i] : -3;
+          const unsigned acci = sh.acck[i] >= 0 ? 1u : 0u;
+          // Branch-free over every accepted move (uniform trip count, no
+          // divergence): hard = certain conflicts, soft = needs an exact test.
+          unsigned hard = 0u, soft = 0u;
+#pragma unroll 2
           for (int k = 0; k < nacc; ++k) {
-            const int j = sh.acc_i[k];
-            if (j >= i) break;
-            const int64_t aa = sh.ia[j], ab = sh.ib[j];
-            const uint32_t an = sh.ptn[j], ao = sh.pto[j];
-            if (la >= 0 && (la == aa || la == ab)) { c = true; break; }
-            if ((ao != (uint32_t)kNoPoint && (lb == mbrick(a.m, ao) || (grid && lcn == sh.co[j]))) ||
-                (an != (uint32_t)kNoPoint && (ln == an || (grid && lcn == sh.cn[j])))) { c = true; break; }
-#ifdef GCMC_PHASE_TIMERS
-            if (a.prof) atomicAdd(&sh.viters, 1u);
-#endif
-            if ((ln != (uint32_t)kNoPoint && (mnear(a.m, ln, ao) || mnear(a.m, ln, an))) ||
-                (lo != (uint32_t)kNoPoint && (mnear(a.m, lo, ao) || mnear(a.m, lo, an)))) {
-#ifdef GCMC_PHASE_TIMERS
-              if (a.prof) atomicAdd(&sh.vcalls, 1u);
-#endif
-              if (conflict_xyz(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
-            }
-            if (ki >= 0) {  // two accepted moves: changed points more than 2 r_c apart
-              auto near2 = [&](uint32_t p, uint32_t q) {
-                if (p == (uint32_t)kNoPoint || q == (uint32_t)kNoPoint) return false;
-                return axis_near(pt_x(p), pt_x(q), a.m.dims, 2) && axis_near(pt_y(p), pt_y(q), a.m.dims, 2) &&
-                       axis_near(pt_z(p), pt_z(q), a.m.dims, 2);
-              };
-              if ((near2(ln, an) || near2(ln, ao) || near2(lo, an) || near2(lo, ao)) &&
-                  !far_apart(a, sh, sh.ring[(base + i) % kRing], sh.ring[(base + j) % kRing], i, j)) { c = true; break; }
+            const AccV v = sh.av[k];
+            const unsigned before = (unsigned)(v.j < i);
+            const unsigned idx = (unsigned)(la >= 0) & ((unsigned)(la == v.ia) | (unsigned)(la == v.ib));
+            const unsigned tgt = (unsigned)(lb == v.bo) | (unsigned)(lb == v.bn) | (unsigned)(lcn == v.co) |
+                                 (unsigned)(lcn == v.cn);
+            const unsigned nr = near_bits(ln, v.ao, dm, rch) | near_bits(ln, v.an, dm, rch) |
+                                near_bits(lo, v.ao, dm, rch) | near_bits(lo, v.an, dm, rch);
+            const unsigned n2 = acci & (near_bits(ln, v.an, dm, 2) | near_bits(ln, v.ao, dm, 2) |
+                                        near_bits(lo, v.an, dm, 2) | near_bits(lo, v.ao, dm, 2));
+            hard |= (before & (idx | tgt)) << k;
+            soft |= (before & (nr | n2)) << k;
+          }
+          bool c = hard != 0u;
+          // rare: exact distances (r_c; 2 r_c between accepted moves)
+          for (unsigned m = c ? 0u : soft; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            const AccV v = sh.av[k];
+            const Proposal& pi = sh.ring[(base + i) % kRing];
+            const Proposal& pj = sh.ring[(base + v.j) % kRing];
+            if (conflict_xyz(a, sh, pi, pj, i, v.j) || (acci && !far_apart(a, sh, pi, pj, i, v.j))) {
+              c = true;
+              break;
             }
           }
           if (c) atomicMin(&sh.cmin, i);
