@@ -228,6 +228,22 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
   __syncwarp();
 }
 
+// 1 when both packed brick points exist and lie within r bricks of each
+// other on every axis (cyclic), computed without branches.
+__device__ __forceinline__ unsigned near_bits(uint32_t p, uint32_t q, int d, int r) {
+  int dx = (int)(p & 0xffu) - (int)(q & 0xffu);
+  int dy = (int)((p >> 8) & 0xffu) - (int)((q >> 8) & 0xffu);
+  int dz = (int)((p >> 16) & 0xffu) - (int)((q >> 16) & 0xffu);
+  dx = abs(dx);
+  dy = abs(dy);
+  dz = abs(dz);
+  dx = min(dx, d - dx);
+  dy = min(dy, d - dy);
+  dz = min(dz, d - dz);
+  return (unsigned)(p != (uint32_t)kNoPoint) & (unsigned)(q != (uint32_t)kNoPoint) & (unsigned)(dx <= r) &
+         (unsigned)(dy <= r) & (unsigned)(dz <= r);
+}
+
 // =================================================================== evaluator
 template <int T>
 struct EvalShared {
@@ -805,13 +821,23 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         }
         pc.mark(8);
         // the candidate particle's position / e vs the moves in flight
-        if (kind != 1 && valid) {
-          const uint64_t po = mpoint(a.m, xox, xoy, xoz);
+        if (kind != 1) {
+          // branch-free scan of the moves in flight (uniform trip count), then
+          // the rare brick-near ones exactly, in move order
+          const uint32_t po = valid ? (uint32_t)mpoint(a.m, xox, xoy, xoz) : (uint32_t)kNoPoint;
+          const int ip = valid ? (int)pid : -7;
+          const int dm = a.m.dims, rch = a.m.reach;
+          unsigned hit = 0u, nearm = 0u;
+#pragma unroll 2
           for (int k = 0; k < d.nacc; ++k) {
             const AccE& A = d.acc[k];
-            if ((int64_t)pid == A.ia || (int64_t)pid == A.ib) {
-              cf = true;
-            } else if (mnear(a.m, po, A.pt0) || mnear(a.m, po, A.pt1)) {
+            hit |= ((unsigned)(ip == (int)A.ia) | (unsigned)(ip == (int)A.ib)) << k;
+            nearm |= (near_bits(po, (uint32_t)A.pt0, dm, rch) | near_bits(po, (uint32_t)A.pt1, dm, rch)) << k;
+          }
+          cf = valid && hit != 0u;
+          if (valid && !cf) {
+            for (unsigned m = nearm; m; m &= m - 1) {
+              const int k = __ffs(m) - 1;
               const ATab* t = a.atab + (size_t)((r - 1) & 1) * kMaxAcc + k;
               while (ld_acquire(&t->tag) != (uint64_t)(r - 1)) nap();
               double cu = 0.0, cw = 0.0;
@@ -983,22 +1009,6 @@ struct AccV {  // an accepted move's write set, packed for the verify
   uint32_t an, ao, bn, bo;
   int cn, co;
 };
-
-// 1 when both packed brick points exist and lie within r bricks of each
-// other on every axis (cyclic), computed without branches.
-__device__ __forceinline__ unsigned near_bits(uint32_t p, uint32_t q, int d, int r) {
-  int dx = (int)(p & 0xffu) - (int)(q & 0xffu);
-  int dy = (int)((p >> 8) & 0xffu) - (int)((q >> 8) & 0xffu);
-  int dz = (int)((p >> 16) & 0xffu) - (int)((q >> 16) & 0xffu);
-  dx = abs(dx);
-  dy = abs(dy);
-  dz = abs(dz);
-  dx = min(dx, d - dx);
-  dy = min(dy, d - dy);
-  dz = min(dz, d - dz);
-  return (unsigned)(p != (uint32_t)kNoPoint) & (unsigned)(q != (uint32_t)kNoPoint) & (unsigned)(dx <= r) &
-         (unsigned)(dy <= r) & (unsigned)(dz <= r);
-}
 
 struct SeqShared {
   Proposal ring[kRing];
@@ -1433,10 +1443,11 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         for (int i = tid; i < len; i += kPollThreads) {
           const Proposal& pr = sh.ring[(base + i) % kRing];
           const int kind = sh.mkind[i];
-          int di = 0;  // N offset before move i
-          for (int k = 0; k < nacc && sh.acc_i[k] < i; ++k) {
-            const int ak = sh.mkind[sh.acc_i[k]];
-            di += ak == 1 ? 1 : (ak == 2 ? -1 : 0);
+          int di = 0;  // N offset before move i (uniform trip count: no divergence)
+          for (int k = 0; k < nacc; ++k) {
+            const int j = sh.acc_i[k];
+            const int ak = sh.mkind[j];
+            di += j < i ? (ak == 1 ? 1 : (ak == 2 ? -1 : 0)) : 0;
           }
           sh.res_d[i] = di;
           const int64_t nd = (int64_t)n + di;
