@@ -407,16 +407,34 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   cc.mark(5);
   // the movers' e, after the neighbour updates of the round (a relabel copy
   // must carry them), in move order
+  // Each lane writes e[x] (displace: pid, insert: its new index, delete: pid
+  // <- e[q], q = n - 1). A deletion's source e[q] is the value the latest
+  // earlier lane of the round wrote to index q, else memory (all loaded in
+  // parallel, then resolved in move order by shuffles); the stores follow
+  // move order (same-index writers: the last one wins).
   if (lane == 0)
     while (ld_acquire(a.flags + kECount) < ctot) nap();
   __syncwarp();
+  const bool copies = mine && kind == 2 && pid != nn - 1;
+  const int64_t ex = !mine ? -1 : (kind == 1 ? (int64_t)nn : (kind == 0 || copies ? (int64_t)pid : -1));
+  const int64_t eq = copies ? (int64_t)(nn - 1) : -2;
+  if (copies) {
+    const double2 el = __ldcg(a.ep + (nn - 1));
+    esu = el.x;
+    esw = el.y;
+  }
+#pragma unroll 1
+  for (int j = 0; j < nacc - 1; ++j) {  // lane j's value reaches later lanes copying index x_j
+    const int64_t xj = __shfl_sync(0xffffffffu, ex, j);
+    const double vu = __shfl_sync(0xffffffffu, esu, j), vw = __shfl_sync(0xffffffffu, esw, j);
+    if (lane > j && xj == eq) {
+      esu = vu;
+      esw = vw;
+    }
+  }
 #pragma unroll 1
   for (int j = 0; j < nacc; ++j) {
-    if (lane == j) {
-      if (kind == 0) __stcg(a.ep + pid, make_double2(esu, esw));
-      else if (kind == 1) __stcg(a.ep + nn, make_double2(esu, esw));
-      else if (pid != nn - 1) __stcg(a.ep + pid, __ldcg(a.ep + (nn - 1)));
-    }
+    if (lane == j && ex >= 0) __stcg(a.ep + ex, make_double2(esu, esw));
     __syncwarp();
   }
   __syncwarp();  // every lane's stores happen-before lane 0's (cumulative) release
