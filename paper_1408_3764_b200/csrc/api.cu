@@ -715,6 +715,11 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
           unsigned long long d5[4];
           cudaMemcpy(d5, c.prof + 3500, sizeof d5, cudaMemcpyDeviceToHost);
           std::fprintf(stderr, "\n[dbg] verify per warp: max=%.0f mean=%.0f iters/round=%.1f xyz calls/round=%.2f", d5[0] / R, d5[1] / R, d5[2] / R, d5[3] / R);
+          unsigned long long lt[18];
+          cudaMemcpy(lt, c.prof + 3600, sizeof lt, cudaMemcpyDeviceToHost);
+          if (lt[12] && lt[14] && lt[17])
+            std::fprintf(stderr, "\n[dbg] latency ns: publish->CTA sees D mean=%.0f max=%.0f; publish->slot result mean=%.0f; publish->last result (per round) mean=%.0f; publish->sequencer has all mean=%.0f",
+                         (double)lt[10] / lt[12], (double)lt[11], (double)lt[13] / lt[14], (double)lt[16] / lt[17], (double)lt[15] / lt[17]);
           unsigned long long d4[4];
           cudaMemcpy(d4, c.prof + 3400, sizeof d4, cudaMemcpyDeviceToHost);
           std::fprintf(stderr, "\n[dbg] barrier: tid0 wait=%.0f last-arrival-after-tid0=%.0f", d4[3] / R, d4[2] / R);

@@ -711,6 +711,14 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
     pc.mark(0);
     if (tid < 32) {
       poll_dec(a, r, sh.d, lane);
+#ifdef GCMC_PHASE_TIMERS
+      if (a.prof && lane == 0 && r > 2) {
+        const unsigned long long dt = gtimer() - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3600 + (r & 1)));
+        atomicAdd(a.prof + 3610, dt);
+        atomicMax(a.prof + 3611, dt);
+        atomicAdd(a.prof + 3612, 1ull);
+      }
+#endif
       const Dec& d = sh.d;
       // replica = memory: the commits of the moves the PREVIOUS decision
       // listed have landed (a--, b++); this decision's run after this
@@ -969,6 +977,14 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const uint64_t pw = lane == 0 ? ((uint64_t)kind | ((uint64_t)accm << 8))
                                         : (lane == 1 ? (uint64_t)cfm : (uint64_t)ovm);
           st_relaxed(rw + (size_t)lane * a.nslots, tagw(r, pw));
+#ifdef GCMC_PHASE_TIMERS
+          if (a.prof && lane == 0 && r > 2) {
+            const unsigned long long dt = gtimer() - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3600 + (r & 1)));
+            atomicAdd(a.prof + 3613, dt);
+            atomicAdd(a.prof + 3614, 1ull);
+            atomicMax(reinterpret_cast<unsigned long long*>(a.prof + 3620 + (r & 7)), dt);
+          }
+#endif
         }
         pc.mark(4);
         // payload for commits / statistics / trace (off the critical path)
@@ -1411,9 +1427,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // not poll: it repeats the walk on the masks as they arrive (results
       // discarded) so that the walk's code is in the instruction cache when
       // the last slot lands.
-      if (warp == 0) {
-        while (*(volatile int*)&sh.arrived < fit)
-          walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+      if (warp == 0) {  // one dry run (the walk's code into the instruction cache), then wait
+        walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+        while (*(volatile int*)&sh.arrived < fit) __nanosleep(32);
       }
       for (int sl = tid - 32; sl >= 0 && sl < fit; sl += kPollThreads - 32) {
         const uint64_t* rw = a.res + (size_t)par * kResWords * a.nslots + sl;
@@ -1439,6 +1455,14 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // every evaluation of round r has read its state: the previous round's
       // commits may store now
       if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);
+#ifdef GCMC_PHASE_TIMERS
+      if (a.prof && tid == 0 && r > 2) {
+        a.prof[3615] += gtimer() - a.prof[3600 + (r & 1)];
+        a.prof[3616] += a.prof[3620 + (r & 7)];
+        a.prof[3620 + ((r + 4) & 7)] = 0;
+        a.prof[3617] += 1;
+      }
+#endif
       pc.mark(1);
       if (warp == 0) {  // ---- walk (warm: warp 0 ran it on the partial masks while polling)
         const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane);
@@ -1674,6 +1698,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     }
     __syncwarp();
     __syncthreads();
+#ifdef GCMC_PHASE_TIMERS
+    if (a.prof && tid == 0) a.prof[3600 + ((r + 1) & 1)] = gtimer();
+#endif
     if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
     etarget += (uint64_t)nacc;
     prev_nacc = nacc;
