@@ -1054,7 +1054,6 @@ struct SeqShared {
   unsigned viters, vcalls;
   int wscr_i[kMaxAcc], wscr_d[kMaxAcc];  // walk dry runs (discarded)
   int8_t wscr_k[kMaxMoves];
-  int chunk_arr[kMaxMoves / 32];  // slots arrived per 32-move chunk (streamed walk)
   int acc_i[kMaxAcc], acc_d[kMaxAcc];
   int res_d[kMaxMoves];
   // read / write sets of the consumed moves (verify)
@@ -1110,16 +1109,11 @@ struct WalkOut {
 // changes only at accepted insertions / deletions.
 __device__ __noinline__ WalkOut walk_warp(const uint32_t* macc, const uint32_t* mcf, const uint32_t* movf,
                                           const uint8_t* mkind, int fit, int* acc_i, int* acc_d,
-                                          int8_t* acck, int lane, const int* chunk_arr) {
+                                          int8_t* acck, int lane) {
   int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
   const int nh = (fit + 31) >> 5;
 #pragma unroll 1
   for (int h = 0; h < nh; ++h) {
-    if (chunk_arr) {  // streaming: this chunk's slots have all arrived
-      const int need = fit - 32 * h < 32 ? fit - 32 * h : 32;
-      while (*(volatile const int*)&chunk_arr[h] < need) __nanosleep(20);
-      __threadfence_block();
-    }
     const int i = lane + 32 * h;
     const bool in = i < fit;
     const uint32_t am = in ? macc[i] : 0u, sm = in ? mcf[i] : 0u, om = in ? movf[i] : 0u;
@@ -1395,11 +1389,11 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   const bool grid = a.g.kind != GCMC_ALL_PAIRS;
   constexpr int kPollThreads = kPollWarps * 32;
   for (int q = tid; q < kBitWords; q += kThreads) sh.nbits[q] = 0u;
-  if (tid < kMaxMoves / 32) sh.chunk_arr[tid] = 0;
   if (tid == 0) {
     sh.ks = *a.st;
     sh.done.len = 0;
     sh.done.nacc = 0;
+    sh.arrived = 0;
     sh.vmax = sh.vsum = 0;
     sh.viters = sh.vcalls = 0;
     sh.err = 0;
@@ -1433,16 +1427,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // not poll: it repeats the walk on the masks as they arrive (results
       // discarded) so that the walk's code is in the instruction cache when
       // the last slot lands.
-      if (warp == 0) {  // the walk, streamed: each 32-move chunk as soon as its slots have arrived
-        const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane,
-                                     sh.chunk_arr);
-        if (lane == 0) {
-          sh.len = wo.len;
-          sh.nacc = wo.nacc;
-          sh.cmin = wo.len;
-          sh.err = wo.err;
-          sh.why = wo.why;
-        }
+      if (warp == 0) {  // one dry run (the walk's code into the instruction cache), then wait
+        walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+        while (*(volatile int*)&sh.arrived < fit) __nanosleep(32);
       }
       for (int sl = tid - 32; sl >= 0 && sl < fit; sl += kPollThreads - 32) {
         const uint64_t* rw = a.res + (size_t)par * kResWords * a.nslots + sl;
@@ -1462,8 +1449,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         sh.macc[sl] = (uint32_t)((w[0] & kPay) >> 8);
         sh.mcf[sl] = (uint32_t)w[1];
         sh.movf[sl] = (uint32_t)w[2];
-        __threadfence_block();
-        atomicAdd(&sh.chunk_arr[sl >> 5], 1);
+        atomicAdd(&sh.arrived, 1);
       }
       group_sync(1, kPollThreads);
       // every evaluation of round r has read its state: the previous round's
@@ -1478,6 +1464,16 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
 #endif
       pc.mark(1);
+      if (warp == 0) {  // ---- walk (warm: warp 0 ran it on the partial masks while polling)
+        const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane);
+        if (lane == 0) {
+          sh.len = wo.len;
+          sh.nacc = wo.nacc;
+          sh.cmin = wo.len;
+          sh.err = wo.err;
+          sh.why = wo.why;
+        }
+      }
       group_sync(1, kPollThreads);
       pc.mark(2);
 #pragma unroll 1
@@ -1719,7 +1715,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       cp_async_wait();
     }
     fit = fit_of(a, nbase);
-    if (tid < kMaxMoves / 32) sh.chunk_arr[tid] = 0;
+    if (tid == 0) sh.arrived = 0;
     __syncwarp();
     __syncthreads();
     base = nbase;
