@@ -778,7 +778,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       const int64_t nd = (int64_t)d.n + dd;
       const bool valid = kind == 1 ? nd >= 0 : nd >= 1;  // kinds 0/2 at N <= 0: counted rejection
       uint64_t pid = 0;
-      double xox = 0.0, xoy = 0.0, xoz = 0.0, eu = 0.0, ew = 0.0;
+      double xox = 0.0, xoy = 0.0, xoz = 0.0, eu = 0.0, ew = 0.0, fpre = 1.0;
       int ocb = 0, ob = 0;
       bool cf = false;
       if (gw == lw) {
@@ -792,6 +792,13 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const double2 e2 = __ldcg(a.ep + pid);
           eu = e2.x;
           ew = e2.y;
+        }
+        // the exchange ratio's prefactor for this lane's N (engine.hpp:28-59,
+        // same operations), computed while the loads above are in flight
+        {
+          const double nn = (double)nd;
+          fpre = kind == 1 ? __ddiv_rn(a.vol, __dmul_rn(a.lambda3, __dadd_rn(nn, 1.0)))
+                           : (kind == 2 ? __ddiv_rn(__dmul_rn(a.lambda3, nn), a.vol) : 1.0);
         }
         int nent = 0;
         pc.mark(6);
@@ -949,11 +956,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
                          : (kind == 1 ? __dmul_rn(a.beta, __dsub_rn(a.mu, du))
                                       : __dmul_rn(-a.beta, __dadd_rn(a.mu, du)));
           const double ex = exp(x);
-          const double nn = (double)nd;
-          if (valid)
-            p = metropolis(kind == 0 ? ex
-                           : (kind == 1 ? __dmul_rn(__ddiv_rn(a.vol, __dmul_rn(a.lambda3, __dadd_rn(nn, 1.0))), ex)
-                                        : __dmul_rn(__ddiv_rn(__dmul_rn(a.lambda3, nn), a.vol), ex)));
+          if (valid) p = metropolis(kind == 0 ? ex : __dmul_rn(fpre, ex));
         }
         const bool acc = valid && pr.acc < p;
         // overflow of the commit (exact: occupancies after the previous round)
