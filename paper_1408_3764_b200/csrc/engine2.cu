@@ -1073,6 +1073,7 @@ struct SeqShared {
   uint32_t nbits[kBitWords];  // verify: bricks near a changed point of the round
   unsigned smp[kMH];          // statistics: sampled steps of the round
   int8_t acck[kMaxMoves];     // accepted index of a consumed move (-1: rejected)
+  uint8_t nbef[kMaxMoves];    // accepted moves before a consumed move
   uint64_t dw[kDecWords];
   int dneed;
   ChainState ks;
@@ -1488,13 +1489,15 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         for (int i = tid; i < len; i += kPollThreads) {
           const Proposal& pr = sh.ring[(base + i) % kRing];
           const int kind = sh.mkind[i];
-          int di = 0;  // N offset before move i (uniform trip count: no divergence)
+          int di = 0, nb = 0;  // N offset before move i (uniform trip count: no divergence)
           for (int k = 0; k < nacc; ++k) {
             const int j = sh.acc_i[k];
             const int ak = sh.mkind[j];
             di += j < i ? (ak == 1 ? 1 : (ak == 2 ? -1 : 0)) : 0;
+            nb += j < i ? 1 : 0;
           }
           sh.res_d[i] = di;
+          sh.nbef[i] = (uint8_t)nb;
           const int64_t nd = (int64_t)n + di;
           sh.ptn[i] = (uint32_t)(kind != 2 ? (pr.wmask != kNoMask ? (uint64_t)pr.bpt : mpoint(a.m, pr.x, pr.y, pr.z)) : kNoPoint);
           sh.cn[i] = (kind != 2 && grid) ? (pr.wmask != kNoMask ? pr.cell : cell_of(a.g, pr.x, pr.y, pr.z)) : -1;
@@ -1557,13 +1560,15 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           const uint32_t lb = ln != (uint32_t)kNoPoint ? mbrick(a.m, ln) : 0xfffffffeu;
           const int lcn = ln != (uint32_t)kNoPoint && grid ? sh.cn[i] : -3;
           const unsigned acci = sh.acck[i] >= 0 ? 1u : 0u;
-          // Branch-free over every accepted move (uniform trip count, no
-          // divergence): hard = certain conflicts, soft = needs an exact test.
+          // Branch-free over the accepted moves before i (acc_i is sorted, so
+          // the trip count differs by at most a few within a warp of
+          // consecutive i): hard = certain conflicts, soft = needs an exact test.
           unsigned hard = 0u, soft = 0u;
+          const int kb = sh.nbef[i];
 #pragma unroll 2
-          for (int k = 0; k < nacc; ++k) {
+          for (int k = 0; k < kb; ++k) {
             const AccV v = sh.av[k];
-            const unsigned before = (unsigned)(v.j < i);
+            const unsigned before = 1u;
             const unsigned idx = (unsigned)(la >= 0) & ((unsigned)(la == v.ia) | (unsigned)(la == v.ib));
             const unsigned tgt = (unsigned)(lb == v.bo) | (unsigned)(lb == v.bn) | (unsigned)(lcn == v.co) |
                                  (unsigned)(lcn == v.cn);
