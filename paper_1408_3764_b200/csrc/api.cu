@@ -720,6 +720,23 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
           if (lt[12] && lt[14] && lt[17])
             std::fprintf(stderr, "\n[dbg] latency ns: publish->CTA sees D mean=%.0f max=%.0f; publish->slot result mean=%.0f; publish->last result (per round) mean=%.0f; publish->sequencer has all mean=%.0f",
                          (double)lt[10] / lt[12], (double)lt[11], (double)lt[13] / lt[14], (double)lt[16] / lt[17], (double)lt[15] / lt[17]);
+          unsigned long long gq[17];
+          cudaMemcpy(gq, c.prof + 3640, sizeof gq, cudaMemcpyDeviceToHost);
+          if (gq[7])
+            std::fprintf(stderr, "\n[dbg] after go (ns): close wait starts=%.0f e updates done=%.0f commits done=%.0f decision published=%.0f",
+                         (double)gq[4] / gq[7], (double)gq[5] / gq[7], (double)gq[6] / gq[7], (double)gq[8] / gq[7]);
+          if (gq[10]) std::fprintf(stderr, "; committer released sflag=%.0f", (double)gq[9] / gq[10]);
+          if (gq[12] && gq[14] && gq[16])
+            std::fprintf(stderr, "; e-update group done (mean)=%.0f committer sees go=%.0f sees e done=%.0f",
+                         (double)gq[11] / gq[12], (double)gq[15] / gq[16], (double)gq[13] / gq[14]);
+          unsigned long long tq[80];
+          cudaMemcpy(tq, c.prof + 3660, sizeof tq, cudaMemcpyDeviceToHost);
+          std::fprintf(stderr, "\n[dbg] commit order causes:");
+          for (int q = 0; q < 64; ++q)
+            if (tq[q]) std::fprintf(stderr, " %s%d.%d=%llu", q < 9 ? "cell" : (q < 18 ? "brick" : (q < 43 ? "part" : "?")),
+                                    q < 18 ? (q % 9) / 3 : (q - 18) / 5, q < 18 ? q % 3 : (q - 18) % 5, tq[q]);
+          std::fprintf(stderr, " | kinds(later,earlier):");
+          for (int q = 0; q < 9; ++q) if (tq[70 + q]) std::fprintf(stderr, " %d,%d=%llu", q / 3, q % 3, tq[70 + q]);
           unsigned long long d4[4];
           cudaMemcpy(d4, c.prof + 3400, sizeof d4, cudaMemcpyDeviceToHost);
           std::fprintf(stderr, "\n[dbg] barrier: tid0 wait=%.0f last-arrival-after-tid0=%.0f", d4[3] / R, d4[2] / R);

@@ -123,14 +123,16 @@ __device__ __forceinline__ void commit_load(const Grid& g, const Mirror& m, cons
 __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, const Store& s,
                                             int32_t* peak, int kind, uint64_t pid, uint64_t n,
                                             const MoveData& d, const CommitIn& c, long long& e1,
-                                            long long& e2, long long& e3) {
+                                            long long& e2, long long& e3, bool skip_index = false) {
   const bool grid = g.kind != GCMC_ALL_PAIRS;
   const uint64_t q = n - 1;
   e1 = e2 = e3 = 0;
   int status = GCMC_OK;
   // ---- store (particles.hpp:28-41)
   if (kind == 0) st_xyz(s.pos + pid, d.nx, d.ny, d.nz);
-  if (kind == 1) st_xyz(s.pos + n, d.nx, d.ny, d.nz);
+  // skip_index: an insertion whose particle a later deletion of the same
+  // batch relabels (and takes its data from registers) leaves index n unused
+  if (kind == 1 && !skip_index) st_xyz(s.pos + n, d.nx, d.ny, d.nz);
   // ---- reference layout
   if (grid) {
     if (c.ref_move) {  // remove_id: the last id fills the hole
@@ -149,7 +151,7 @@ __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, cons
       } else {
         const int32_t id = kind == 1 ? (int32_t)n : (int32_t)pid;
         __stcg(g.slots + slot_index(g, c.cb, c.occ_cb), id);
-        __stcg(s.rslot + id, c.occ_cb);
+        if (!skip_index) __stcg(s.rslot + id, c.occ_cb);
         __stcg(g.occ + c.cb, c.occ_cb + 1);
         atomicMax(peak, c.occ_cb + 1);
       }
@@ -192,7 +194,7 @@ __device__ __forceinline__ int commit_store(const Grid& g, const Mirror& m, cons
         __stcg(m.ry + k, d.ny);
         __stcg(m.rz + k, d.nz);
         __stcg(m.rid + k, id);
-        __stcg(bslot_of(s.pos, id), k);
+        if (!skip_index) __stcg(bslot_of(s.pos, id), k);
         __stcg(m.occ + c.bb, c.occ_bb + 1);
       }
     }

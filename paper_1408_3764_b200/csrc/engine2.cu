@@ -342,8 +342,19 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
       tc = touch_of(a.m, kind, pid, nn, c);
     }
   }
-  bool dep = false;
-  unsigned exm = 0;
+  // Relabel chains at the store's end (insert at n, a deletion relabels it,
+  // another insert at n, ...): a forwarded deletion never reads index q from
+  // memory, and an insertion relabelled away by a later deletion of the
+  // round need not write index n at all (skip_index). Without those
+  // accesses the chain's commits are independent. This holds while no
+  // member of a chain is ordered for another reason (an ordered forwarded
+  // deletion re-loads q from memory); otherwise the round falls back to the
+  // full ordering (dep1 below).
+  const unsigned fwd_src = __reduce_or_sync(0xffffffffu, (mine && fsrc >= 0) ? (1u << fsrc) : 0u);
+  const bool away = mine && kind == 1 && ((fwd_src >> lane) & 1u);
+  const int chain = (fsrc >= 0 ? 1 : 0) | (away ? 2 : 0);
+  bool dep = false, dep1 = false;
+  unsigned exm = 0, exm1 = 0;
 #pragma unroll 1
   for (int j = 0; j < nacc - 1; ++j) {
     Touch tj;
@@ -355,18 +366,51 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
 #pragma unroll
     for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tc.part[x], j);
     const int kj = __shfl_sync(0xffffffffu, kind, j);
+    const int chj = __shfl_sync(0xffffffffu, chain, j);
     if (mine && j < lane) {
       Touch tm = tc;
       if (kind == 1 && kj == 2 && tm.part[0] == tj.part[1]) {
         tm.part[0] = -1;
-        exm |= 1u << j;
+        exm1 |= 1u << j;
       }
       if (j == fsrc) {  // the forwarded particle's index, cell and record are expected
         tm.part[1] = -1;
         tm.cell[2] = -1;
         tm.brick[2] = -1;
       }
-      if (touches(tm, tj)) dep = true;
+      if (touches(tm, tj)) dep1 = true;
+      // chain form: index q of forwarded deletions, index n of inserts relabelled away
+      Touch tm2 = tc, tj2 = tj;
+      if (chain & 1) tm2.part[1] = -1;
+      if (chain & 2) tm2.part[0] = -1;
+      if (chj & 1) tj2.part[1] = -1;
+      if (chj & 2) tj2.part[0] = -1;
+      if (kind == 1 && kj == 2 && tm2.part[0] >= 0 && tm2.part[0] == tj2.part[1]) {
+        tm2.part[0] = -1;
+        exm |= 1u << j;
+      }
+      if (j == fsrc) {
+        tm2.cell[2] = -1;
+        tm2.brick[2] = -1;
+      }
+      if (touches(tm2, tj2)) {
+        dep = true;
+#ifdef GCMC_PHASE_TIMERS
+        if (a.prof) {  // which pair of fields overlaps (diagnostics)
+          int code = 63;
+          for (int x = 0; x < 3 && code == 63; ++x)
+            for (int y = 0; y < 3 && code == 63; ++y) {
+              if (tm2.cell[x] >= 0 && tm2.cell[x] == tj2.cell[y]) code = x * 3 + y;
+              else if (tm2.brick[x] >= 0 && tm2.brick[x] == tj2.brick[y]) code = 9 + x * 3 + y;
+            }
+          for (int x = 0; x < 5 && code == 63; ++x)
+            for (int y = 0; y < 5 && code == 63; ++y)
+              if (tm2.part[x] >= 0 && tm2.part[x] == tj2.part[y]) code = 18 + x * 5 + y;
+          atomicAdd(a.prof + 3660 + code, 1ull);
+          atomicAdd(a.prof + 3730 + kind * 3 + kj, 1ull);
+        }
+#endif
+      }
     }
   }
   // an exempted / forwarded commit is ordered after its partner when the
@@ -378,17 +422,37 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     if (__ballot_sync(0xffffffffu, nd) == b) break;
     dep = nd;
   }
+  const bool chains_free = !__any_sync(0xffffffffu, chain != 0 && dep);
+  if (!chains_free) {  // full ordering
+    dep = dep1;
+    exm = exm1;
+#pragma unroll 1
+    for (int it = 0; it < 32; ++it) {
+      const unsigned b = __ballot_sync(0xffffffffu, dep);
+      const bool nd = dep || (b & exm) || (fsrc >= 0 && ((b >> fsrc) & 1u));
+      if (__ballot_sync(0xffffffffu, nd) == b) break;
+      dep = nd;
+    }
+  }
+  const bool skip_index = chains_free && away;
   cc.mark(3);
   // stores only once the round being evaluated against the old state is
   // done, and the round's energy updates have found their neighbours
   if (lane == 0) {
     while (ld_acquire(a.flags + kGo) < (uint64_t)rr + 1) nap();
+#ifdef GCMC_PHASE_TIMERS
+    if (a.prof && rr > 2) {
+      a.prof[3655] += gtimer() - a.prof[3640 + ((rr + 1) & 1)];
+      a.prof[3656] += 1;
+    }
+#endif
     while (ld_acquire(a.flags + kETrav) < ctot) nap();
   }
   __syncwarp();
   cc.mark(7);
   long long e1, e2, e3;
-  if (mine && !dep && fsrc < 0) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
+  if (mine && !dep && fsrc < 0)
+    commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3, skip_index);
   __syncwarp();  // pass B: forwarded deletions after their insertions
   if (mine && !dep && fsrc >= 0) commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, md, c, e1, e2, e3);
   const unsigned deps = __ballot_sync(0xffffffffu, dep);
@@ -412,8 +476,15 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   // earlier lane of the round wrote to index q, else memory (all loaded in
   // parallel, then resolved in move order by shuffles); the stores follow
   // move order (same-index writers: the last one wins).
-  if (lane == 0)
+  if (lane == 0) {
     while (ld_acquire(a.flags + kECount) < ctot) nap();
+#ifdef GCMC_PHASE_TIMERS
+    if (a.prof && rr > 2) {
+      a.prof[3653] += gtimer() - a.prof[3640 + ((rr + 1) & 1)];
+      a.prof[3654] += 1;
+    }
+#endif
+  }
   __syncwarp();
   const bool copies = mine && kind == 2 && pid != nn - 1;
   const int64_t ex = !mine ? -1 : (kind == 1 ? (int64_t)nn : (kind == 0 || copies ? (int64_t)pid : -1));
@@ -441,6 +512,12 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   if (lane == 0) {
     __threadfence();
     st_release(a.flags + kSFlag, (uint64_t)rr);
+#ifdef GCMC_PHASE_TIMERS
+    if (a.prof && rr > 2) {
+      a.prof[3649] += gtimer() - a.prof[3640 + ((rr + 1) & 1)];
+      a.prof[3650] += 1;
+    }
+#endif
   }
 #ifdef GCMC_DBGDELAY
   __nanosleep(3000);  // robustness test: a committer that returns late
@@ -587,6 +664,12 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
   __threadfence();
   group_sync(bar_id, T);
   if (gt == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + kECount), 1ull);
+#ifdef GCMC_PHASE_TIMERS
+  if (a.prof && gt == 0 && r > 3) {  // ns after go_r: this group's updates applied
+    atomicAdd(a.prof + 3651, gtimer() - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3640 + (r & 1))));
+    atomicAdd(a.prof + 3652, 1ull);
+  }
+#endif
   ec.mark(3);
   if (ec.on)
     for (int q = 0; q < 4; ++q) atomicAdd(a.prof + 64 + q, ec.acc[q]);
@@ -1460,6 +1543,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // commits may store now
       if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);
 #ifdef GCMC_PHASE_TIMERS
+      if (a.prof && tid == 0) a.prof[3640 + (r & 1)] = gtimer();
+#endif
+#ifdef GCMC_PHASE_TIMERS
       if (a.prof && tid == 0 && r > 2) {
         a.prof[3615] += gtimer() - a.prof[3600 + (r & 1)];
         a.prof[3616] += a.prof[3620 + (r & 7)];
@@ -1700,14 +1786,30 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     }
     // the previous round's energy updates must land before D_{r+1}
     if (tid == 32 * 15) {
+#ifdef GCMC_PHASE_TIMERS
+      const unsigned long long w0 = gtimer();
+#endif
       while (ld_acquire(a.flags + kECount) < etarget) __nanosleep(a.poll_ns);
+#ifdef GCMC_PHASE_TIMERS
+      const unsigned long long w1 = gtimer();
+#endif
       if (prev_nacc)
         while (ld_acquire(a.flags + kSFlag) < (uint64_t)(r - 1)) __nanosleep(a.poll_ns);
+#ifdef GCMC_PHASE_TIMERS
+      if (a.prof && r > 2) {  // ns after go_r: wait start, e updates done, commits done
+        const unsigned long long g0 = a.prof[3640 + (r & 1)];
+        a.prof[3644] += w0 - g0;
+        a.prof[3645] += w1 - g0;
+        a.prof[3646] += gtimer() - g0;
+        a.prof[3647] += 1;
+      }
+#endif
     }
     __syncwarp();
     __syncthreads();
 #ifdef GCMC_PHASE_TIMERS
     if (a.prof && tid == 0) a.prof[3600 + ((r + 1) & 1)] = gtimer();
+    if (a.prof && tid == 0 && r > 2) a.prof[3648] += gtimer() - a.prof[3640 + (r & 1)];
 #endif
     if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
     etarget += (uint64_t)nacc;
