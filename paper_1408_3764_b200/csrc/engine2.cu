@@ -279,6 +279,77 @@ struct EvalShared {
 // deletion's loads precede every store, unless it is itself ordered). The
 // movers' e (set / relabel copy) are written in move order after the
 // round's neighbour energy updates have been applied. Then flags[kSFlag] = rr.
+// Branch-free form of touches() (commit.cuh): any shared cell, brick or particle.
+__device__ __forceinline__ bool touches_bf(const Touch& a, const Touch& b) {
+  unsigned hit = 0u;
+#pragma unroll
+  for (int x = 0; x < 3; ++x)
+#pragma unroll
+    for (int y = 0; y < 3; ++y)
+      hit |= ((unsigned)(a.cell[x] >= 0) & (unsigned)(a.cell[x] == b.cell[y])) |
+             ((unsigned)(a.brick[x] >= 0) & (unsigned)(a.brick[x] == b.brick[y]));
+#pragma unroll
+  for (int x = 0; x < 5; ++x)
+#pragma unroll
+    for (int y = 0; y < 5; ++y) hit |= (unsigned)(a.part[x] >= 0) & (unsigned)(a.part[x] == b.part[y]);
+  return hit != 0u;
+}
+
+// Order test of this lane's commit against every earlier one of the round
+// (one form): dep = must follow an earlier commit; exm = earlier deletions
+// whose vacated index this insertion reuses. chain_form releases the relabel
+// chains at the store's end (see commit_round).
+__device__ __forceinline__ void touch_deps(const EngineArgs& a, const Touch& tc, int kind, int chain,
+                                           int fsrc, bool mine, int lane, int nacc, bool chain_form,
+                                           bool& dep, unsigned& exm) {
+  Touch tme = tc;
+  if (chain_form && (chain & 1)) tme.part[1] = -1;
+  if (chain_form && (chain & 2)) tme.part[0] = -1;
+  Touch tsh = tme;  // as seen by later lanes
+#pragma unroll 1
+  for (int j = 0; j < nacc - 1; ++j) {
+    Touch tj;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      tj.cell[x] = __shfl_sync(0xffffffffu, tsh.cell[x], j);
+      tj.brick[x] = __shfl_sync(0xffffffffu, tsh.brick[x], j);
+    }
+#pragma unroll
+    for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tsh.part[x], j);
+    const int kj = __shfl_sync(0xffffffffu, kind, j);
+    if (mine && j < lane) {
+      Touch tm = tme;
+      if (kind == 1 && kj == 2 && tm.part[0] >= 0 && tm.part[0] == tj.part[1]) {
+        tm.part[0] = -1;
+        exm |= 1u << j;
+      }
+      if (j == fsrc) {  // the forwarded particle's index, cell and record are expected
+        tm.part[1] = -1;
+        tm.cell[2] = -1;
+        tm.brick[2] = -1;
+      }
+      if (touches_bf(tm, tj)) {
+        dep = true;
+#ifdef GCMC_PHASE_TIMERS
+        if (a.prof && chain_form) {  // which pair of fields overlaps (diagnostics)
+          int code = 63;
+          for (int x = 0; x < 3 && code == 63; ++x)
+            for (int y = 0; y < 3 && code == 63; ++y) {
+              if (tm.cell[x] >= 0 && tm.cell[x] == tj.cell[y]) code = x * 3 + y;
+              else if (tm.brick[x] >= 0 && tm.brick[x] == tj.brick[y]) code = 9 + x * 3 + y;
+            }
+          for (int x = 0; x < 5 && code == 63; ++x)
+            for (int y = 0; y < 5 && code == 63; ++y)
+              if (tm.part[x] >= 0 && tm.part[x] == tj.part[y]) code = 18 + x * 5 + y;
+          atomicAdd(a.prof + 3660 + code, 1ull);
+          atomicAdd(a.prof + 3730 + kind * 3 + kj, 1ull);
+        }
+#endif
+      }
+    }
+  }
+}
+
 __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_t rr, uint64_t ctot,
                                           int lane) {
   const bool mine = lane < nacc;
@@ -353,66 +424,9 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
   const unsigned fwd_src = __reduce_or_sync(0xffffffffu, (mine && fsrc >= 0) ? (1u << fsrc) : 0u);
   const bool away = mine && kind == 1 && ((fwd_src >> lane) & 1u);
   const int chain = (fsrc >= 0 ? 1 : 0) | (away ? 2 : 0);
-  bool dep = false, dep1 = false;
-  unsigned exm = 0, exm1 = 0;
-#pragma unroll 1
-  for (int j = 0; j < nacc - 1; ++j) {
-    Touch tj;
-#pragma unroll
-    for (int x = 0; x < 3; ++x) {
-      tj.cell[x] = __shfl_sync(0xffffffffu, tc.cell[x], j);
-      tj.brick[x] = __shfl_sync(0xffffffffu, tc.brick[x], j);
-    }
-#pragma unroll
-    for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tc.part[x], j);
-    const int kj = __shfl_sync(0xffffffffu, kind, j);
-    const int chj = __shfl_sync(0xffffffffu, chain, j);
-    if (mine && j < lane) {
-      Touch tm = tc;
-      if (kind == 1 && kj == 2 && tm.part[0] == tj.part[1]) {
-        tm.part[0] = -1;
-        exm1 |= 1u << j;
-      }
-      if (j == fsrc) {  // the forwarded particle's index, cell and record are expected
-        tm.part[1] = -1;
-        tm.cell[2] = -1;
-        tm.brick[2] = -1;
-      }
-      if (touches(tm, tj)) dep1 = true;
-      // chain form: index q of forwarded deletions, index n of inserts relabelled away
-      Touch tm2 = tc, tj2 = tj;
-      if (chain & 1) tm2.part[1] = -1;
-      if (chain & 2) tm2.part[0] = -1;
-      if (chj & 1) tj2.part[1] = -1;
-      if (chj & 2) tj2.part[0] = -1;
-      if (kind == 1 && kj == 2 && tm2.part[0] >= 0 && tm2.part[0] == tj2.part[1]) {
-        tm2.part[0] = -1;
-        exm |= 1u << j;
-      }
-      if (j == fsrc) {
-        tm2.cell[2] = -1;
-        tm2.brick[2] = -1;
-      }
-      if (touches(tm2, tj2)) {
-        dep = true;
-#ifdef GCMC_PHASE_TIMERS
-        if (a.prof) {  // which pair of fields overlaps (diagnostics)
-          int code = 63;
-          for (int x = 0; x < 3 && code == 63; ++x)
-            for (int y = 0; y < 3 && code == 63; ++y) {
-              if (tm2.cell[x] >= 0 && tm2.cell[x] == tj2.cell[y]) code = x * 3 + y;
-              else if (tm2.brick[x] >= 0 && tm2.brick[x] == tj2.brick[y]) code = 9 + x * 3 + y;
-            }
-          for (int x = 0; x < 5 && code == 63; ++x)
-            for (int y = 0; y < 5 && code == 63; ++y)
-              if (tm2.part[x] >= 0 && tm2.part[x] == tj2.part[y]) code = 18 + x * 5 + y;
-          atomicAdd(a.prof + 3660 + code, 1ull);
-          atomicAdd(a.prof + 3730 + kind * 3 + kj, 1ull);
-        }
-#endif
-      }
-    }
-  }
+  bool dep = false;
+  unsigned exm = 0;
+  touch_deps(a, tc, kind, chain, fsrc, mine, lane, nacc, true, dep, exm);
   // an exempted / forwarded commit is ordered after its partner when the
   // partner itself is (it then loads or stores late)
 #pragma unroll 1
@@ -423,9 +437,10 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     dep = nd;
   }
   const bool chains_free = !__any_sync(0xffffffffu, chain != 0 && dep);
-  if (!chains_free) {  // full ordering
-    dep = dep1;
-    exm = exm1;
+  if (!chains_free) {  // full ordering (rare)
+    dep = false;
+    exm = 0u;
+    touch_deps(a, tc, kind, chain, fsrc, mine, lane, nacc, false, dep, exm);
 #pragma unroll 1
     for (int it = 0; it < 32; ++it) {
       const unsigned b = __ballot_sync(0xffffffffu, dep);
