@@ -98,7 +98,7 @@ struct ATab {  // accepted move k of a round, exact (sequencer -> commit groups 
 // flags[]: [kECount] energy updates done (cumulative); [kSFlag] last round whose
 // accepted moves are committed (structural + the movers' e).
 constexpr int kECount = 8;
-constexpr int kSFlag = 16;
+constexpr int kSFlag = 9;   // same line as kECount (polled together)
 constexpr int kGo = 24;      // last round whose evaluations are complete (commits may store)
 constexpr int kETrav = 32;   // energy-update traversals done (cumulative)
 constexpr int kFlagWords = 64;
@@ -168,14 +168,24 @@ __device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, u
 }
 
 // Warp: wait for D_r (self-validating tagged words) and decode it.
-__device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane) {
+// The state D_r's evaluations read must be complete as well: the energy
+// updates through round r - 2 (flags[kECount] >= ctot - nacc) and, when
+// round r - 2 accepted moves, their commits (flags[kSFlag] >= r - 2). Both
+// flags are polled with the decision words, so the sequencer publishes D_r
+// without waiting for them.
+__device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane, bool need_s) {
   constexpr int PER = (kDecWords + 31) / 32;  // 5
   uint64_t w[PER];
   for (;;) {
     w[0] = ld_relaxed(a.dec + lane);
     w[1] = ld_relaxed(a.dec + 32 + lane);
+    const uint64_t fl = lane < 2 ? ld_acquire(a.flags + (lane == 0 ? kECount : kSFlag)) : 0ull;
     const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2);
-    const bool h2ok = tagged(h2, r);
+    const uint64_t h3 = __shfl_sync(0xffffffffu, w[0], 3);
+    const uint64_t ecnt = __shfl_sync(0xffffffffu, fl, 0) & 0xffffffffull;
+    const uint64_t sflg = __shfl_sync(0xffffffffu, fl, 1);
+    const bool h2ok = tagged(h2, r) && tagged(h3, r) &&
+                      ecnt + (h2 & 0xff) >= (h3 & kPay) && (!need_s || sflg + 2 >= (uint64_t)r);
     const int nacc = h2ok ? (int)(h2 & 0xff) : 0;
     const int need = kDecHdr + kDecEnt * nacc;
 #pragma unroll
@@ -457,7 +467,7 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     while (ld_acquire(a.flags + kGo) < (uint64_t)rr + 1) nap();
 #ifdef GCMC_PHASE_TIMERS
     if (a.prof && rr > 2) {
-      a.prof[3655] += gtimer() - a.prof[3640 + ((rr + 1) & 1)];
+      { const unsigned long long tn = gtimer(); a.prof[3655] += tn - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3640 + ((rr + 1) & 1))); }
       a.prof[3656] += 1;
     }
 #endif
@@ -495,7 +505,7 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     while (ld_acquire(a.flags + kECount) < ctot) nap();
 #ifdef GCMC_PHASE_TIMERS
     if (a.prof && rr > 2) {
-      a.prof[3653] += gtimer() - a.prof[3640 + ((rr + 1) & 1)];
+      { const unsigned long long tn = gtimer(); a.prof[3653] += tn - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3640 + ((rr + 1) & 1))); }
       a.prof[3654] += 1;
     }
 #endif
@@ -529,7 +539,7 @@ __device__ __noinline__ void commit_round(const EngineArgs& a, int nacc, uint32_
     st_release(a.flags + kSFlag, (uint64_t)rr);
 #ifdef GCMC_PHASE_TIMERS
     if (a.prof && rr > 2) {
-      a.prof[3649] += gtimer() - a.prof[3640 + ((rr + 1) & 1)];
+      { const unsigned long long tn = gtimer(); a.prof[3649] += tn - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3640 + ((rr + 1) & 1))); }
       a.prof[3650] += 1;
     }
 #endif
@@ -808,7 +818,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
   for (uint32_t r = 1;; ++r) {
     pc.mark(0);
     if (tid < 32) {
-      poll_dec(a, r, sh.d, lane);
+      poll_dec(a, r, sh.d, lane, sh.nprev > 0);
 #ifdef GCMC_PHASE_TIMERS
       if (a.prof && lane == 0 && r > 2) {
         const unsigned long long dt = gtimer() - ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3600 + (r & 1)));
@@ -1510,6 +1520,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     __syncthreads();
   uint64_t base = 0, n = sh.ks.n;
   uint64_t rounds = 0, etarget = 0;  // energy updates expected through the previous round
+  uint64_t need_s = 0;                 // latest round before the last whose commits D_r waits for
   int prev_nacc = 0;
   int fit = fit_of(a, 0);
   uint32_t r = 1;
@@ -1799,27 +1810,9 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         ++sh.stops[sh.why];
       }
     }
-    // the previous round's energy updates must land before D_{r+1}
-    if (tid == 32 * 15) {
-#ifdef GCMC_PHASE_TIMERS
-      const unsigned long long w0 = gtimer();
-#endif
-      while (ld_acquire(a.flags + kECount) < etarget) __nanosleep(a.poll_ns);
-#ifdef GCMC_PHASE_TIMERS
-      const unsigned long long w1 = gtimer();
-#endif
-      if (prev_nacc)
-        while (ld_acquire(a.flags + kSFlag) < (uint64_t)(r - 1)) __nanosleep(a.poll_ns);
-#ifdef GCMC_PHASE_TIMERS
-      if (a.prof && r > 2) {  // ns after go_r: wait start, e updates done, commits done
-        const unsigned long long g0 = a.prof[3640 + (r & 1)];
-        a.prof[3644] += w0 - g0;
-        a.prof[3645] += w1 - g0;
-        a.prof[3646] += gtimer() - g0;
-        a.prof[3647] += 1;
-      }
-#endif
-    }
+    // D_{r+1} goes out at once: the evaluators themselves wait for the
+    // previous round's energy updates and commits (poll_dec)
+    if (prev_nacc) need_s = r - 1;
     __syncwarp();
     __syncthreads();
 #ifdef GCMC_PHASE_TIMERS
@@ -1852,6 +1845,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);  // the last decision's commits
   // the last round's statistics / trace
   if (warp >= kPollWarps) helpers(a, sh, warp, lane);
+  if (tid == 32) while (ld_acquire(a.flags + kSFlag) < need_s) __nanosleep(a.poll_ns);
   __syncwarp();
     __syncthreads();
   if (a.prof && tid == 0) {
