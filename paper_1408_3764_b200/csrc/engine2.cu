@@ -254,6 +254,31 @@ __device__ __forceinline__ unsigned near_bits(uint32_t p, uint32_t q, int d, int
          (unsigned)(dy <= r) & (unsigned)(dz <= r);
 }
 
+// The same test on packed bytes (all three axes at once) when dims <= 127:
+// with t = |dp| < d per axis, u = |2t - d| <= 127, and
+// min(t, d - t) <= reach  <=>  u >= d - 2 reach  (both branches of the min).
+// near_ok adds 0x80 - max(d - 2 reach, 0) per byte (no carries: u <= 127) and
+// wants bit 7 of all three bytes. Points must be valid (not kNoPoint).
+struct NearK {
+  uint32_t dd, add_r, add_2;
+  bool simd;
+};
+__device__ __forceinline__ NearK near_k(int d, int reach) {
+  const auto add = [d](int r) {
+    const int k = d - 2 * r > 0 ? d - 2 * r : 0;
+    const uint32_t b = (uint32_t)(0x80 - k);
+    return b | (b << 8) | (b << 16);
+  };
+  return {(uint32_t)d | ((uint32_t)d << 8) | ((uint32_t)d << 16), add(reach), add(2), d <= 127};
+}
+__device__ __forceinline__ uint32_t near_u(uint32_t p, uint32_t q, uint32_t dd) {
+  const uint32_t t = __vabsdiffu4(p, q);
+  return __vabsdiffu4(t + t, dd);
+}
+__device__ __forceinline__ unsigned near_ok(uint32_t u, uint32_t add) {
+  return ((u + add) & 0x808080u) == 0x808080u ? 1u : 0u;
+}
+
 // =================================================================== evaluator
 template <int T>
 struct EvalShared {
@@ -969,11 +994,25 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           const int ip = valid ? (int)pid : -7;
           const int dm = a.m.dims, rch = a.m.reach;
           unsigned hit = 0u, nearm = 0u;
+          const NearK nk = near_k(dm, rch);
+          if (nk.simd) {
+            const unsigned pv = po != (uint32_t)kNoPoint ? 1u : 0u;
 #pragma unroll 2
-          for (int k = 0; k < d.nacc; ++k) {
-            const AccE& A = d.acc[k];
-            hit |= ((unsigned)(ip == (int)A.ia) | (unsigned)(ip == (int)A.ib)) << k;
-            nearm |= (near_bits(po, (uint32_t)A.pt0, dm, rch) | near_bits(po, (uint32_t)A.pt1, dm, rch)) << k;
+            for (int k = 0; k < d.nacc; ++k) {
+              const AccE& A = d.acc[k];
+              const uint32_t p0 = (uint32_t)A.pt0, p1 = (uint32_t)A.pt1;
+              hit |= ((unsigned)(ip == (int)A.ia) | (unsigned)(ip == (int)A.ib)) << k;
+              const unsigned n0 = near_ok(near_u(po, p0, nk.dd), nk.add_r) & (unsigned)(p0 != (uint32_t)kNoPoint);
+              const unsigned n1 = near_ok(near_u(po, p1, nk.dd), nk.add_r) & (unsigned)(p1 != (uint32_t)kNoPoint);
+              nearm |= (pv & (n0 | n1)) << k;
+            }
+          } else {
+#pragma unroll 2
+            for (int k = 0; k < d.nacc; ++k) {
+              const AccE& A = d.acc[k];
+              hit |= ((unsigned)(ip == (int)A.ia) | (unsigned)(ip == (int)A.ib)) << k;
+              nearm |= (near_bits(po, (uint32_t)A.pt0, dm, rch) | near_bits(po, (uint32_t)A.pt1, dm, rch)) << k;
+            }
           }
           cf = valid && hit != 0u;
           if (valid && !cf) {
@@ -1158,8 +1197,10 @@ struct AccV {  // an accepted move's write set, packed for the verify
 struct SeqShared {
   Proposal ring[kRing];
   AccV av[kMaxAcc];
-  uint32_t macc[kMaxMoves], mcf[kMaxMoves], movf[kMaxMoves];
-  uint8_t mkind[kMaxMoves];
+  alignas(16) uint32_t macc[kMaxMoves];
+  alignas(16) uint32_t mcf[kMaxMoves];
+  alignas(16) uint32_t movf[kMaxMoves];
+  alignas(16) uint8_t mkind[kMaxMoves];
   int len, nacc, err, cmin, why, dend, arrived;
   unsigned long long vmax, vsum;  // diagnostics
   unsigned viters, vcalls;
@@ -1664,6 +1705,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         }
         group_sync(1, kPollThreads);
         const int dm = a.m.dims, rch = a.m.reach;
+        const NearK nk = near_k(dm, rch);
 #pragma unroll 1
         for (int i = first + 1 + tid; i < len && a.walk_reps != 5; i += kPollThreads) {
           const int kind = sh.mkind[i];
@@ -1672,6 +1714,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
           const uint32_t lb = ln != (uint32_t)kNoPoint ? mbrick(a.m, ln) : 0xfffffffeu;
           const int lcn = ln != (uint32_t)kNoPoint && grid ? sh.cn[i] : -3;
           const unsigned acci = sh.acck[i] >= 0 ? 1u : 0u;
+          const unsigned lnv = ln != (uint32_t)kNoPoint ? 1u : 0u, lov = lo != (uint32_t)kNoPoint ? 1u : 0u;
           // Branch-free over the accepted moves before i (acc_i is sorted, so
           // the trip count differs by at most a few within a warp of
           // consecutive i): hard = certain conflicts, soft = needs an exact test.
@@ -1684,10 +1727,22 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
             const unsigned idx = (unsigned)(la >= 0) & ((unsigned)(la == v.ia) | (unsigned)(la == v.ib));
             const unsigned tgt = (unsigned)(lb == v.bo) | (unsigned)(lb == v.bn) | (unsigned)(lcn == v.co) |
                                  (unsigned)(lcn == v.cn);
-            const unsigned nr = near_bits(ln, v.ao, dm, rch) | near_bits(ln, v.an, dm, rch) |
-                                near_bits(lo, v.ao, dm, rch) | near_bits(lo, v.an, dm, rch);
-            const unsigned n2 = acci & (near_bits(ln, v.an, dm, 2) | near_bits(ln, v.ao, dm, 2) |
-                                        near_bits(lo, v.an, dm, 2) | near_bits(lo, v.ao, dm, 2));
+            unsigned nr, n2;
+            if (nk.simd) {
+              const unsigned aov = v.ao != (uint32_t)kNoPoint ? 1u : 0u, anv = v.an != (uint32_t)kNoPoint ? 1u : 0u;
+              const unsigned mno = lnv & aov, mnn = lnv & anv, moo = lov & aov, mon = lov & anv;
+              const uint32_t uno = near_u(ln, v.ao, nk.dd), unn = near_u(ln, v.an, nk.dd);
+              const uint32_t uoo = near_u(lo, v.ao, nk.dd), uon = near_u(lo, v.an, nk.dd);
+              nr = (mno & near_ok(uno, nk.add_r)) | (mnn & near_ok(unn, nk.add_r)) |
+                   (moo & near_ok(uoo, nk.add_r)) | (mon & near_ok(uon, nk.add_r));
+              n2 = acci & ((mno & near_ok(uno, nk.add_2)) | (mnn & near_ok(unn, nk.add_2)) |
+                           (moo & near_ok(uoo, nk.add_2)) | (mon & near_ok(uon, nk.add_2)));
+            } else {
+              nr = near_bits(ln, v.ao, dm, rch) | near_bits(ln, v.an, dm, rch) |
+                   near_bits(lo, v.ao, dm, rch) | near_bits(lo, v.an, dm, rch);
+              n2 = acci & (near_bits(ln, v.an, dm, 2) | near_bits(ln, v.ao, dm, 2) |
+                           near_bits(lo, v.an, dm, 2) | near_bits(lo, v.ao, dm, 2));
+            }
             hard |= (before & (idx | tgt)) << k;
             soft |= (before & (nr | n2)) << k;
           }
