@@ -55,7 +55,7 @@ namespace {
 
 constexpr int kThreads = 512;
 #ifndef GCMC_E2_MOVES
-#define GCMC_E2_MOVES 256
+#define GCMC_E2_MOVES 384
 #endif
 constexpr int kMaxMoves = GCMC_E2_MOVES;  // moves per round
 constexpr int kMH = kMaxMoves / 32;       // moves per walk lane
@@ -2012,7 +2012,7 @@ bool engine2_supported(const Chain& c) {
   if (c.params.engine_mode == 1) return false;
   if (std::getenv("GCMC_ENGINE_V1")) return false;
   if (c.grid.kind == GCMC_ALL_PAIRS || c.params.max_displacement > 0.0) return false;
-  const int mg = kThreads / c.engine_group;
+  const int mg = kThreads / c.engine2_group;
   return (c.engine_ctas - 1) * mg > kMaxAcc + 1 && (c.engine_ctas - 1) * mg <= kMaxSlots;
 }
 
@@ -2077,7 +2077,7 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
     if (st) return st;
     c.e_valid = true;
   }
-  const int T = c.engine_group;
+  const int T = c.engine2_group;
   const int MG = kThreads / T;
   const int G = c.engine_ctas;
   EngineArgs a{};

@@ -48,7 +48,8 @@ struct Chain {
   cudaEvent_t ev[4] = {};
   int sm_count = 0;
   int engine_ctas = 0;        // sequencer + evaluator CTAs
-  int engine_group = 256;     // threads per evaluation slot
+  int engine_group = 256;     // threads per evaluation slot (per-window engine)
+  int engine2_group = 128;    // threads per evaluation slot (engine2)
   int engine_variants = 9;    // N-variants per displace/delete proposal (after the first)
   int engine_bias = -1;       // initial variant order (+1: N expected to grow)
   uint64_t* eng_dec = nullptr;  // engine communication buffers (engine.cu)
