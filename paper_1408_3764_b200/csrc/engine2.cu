@@ -1805,36 +1805,34 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     pc.mark(4);
     // -------------------- close the round
     const int len = sh.len, nacc = sh.nacc;
-    int dn = 0;
-    for (int k = 0; k < nacc; ++k) {
-      const int kd = sh.mkind[sh.acc_i[k]];
-      dn += kd == 1 ? 1 : (kd == 2 ? -1 : 0);
+    int dn;  // N change of the round: one accepted move per lane (nacc <= kMaxAcc = 32)
+    {
+      const int kd = lane < nacc ? (int)sh.mkind[sh.acc_i[lane]] : 0;
+      dn = __reduce_add_sync(0xffffffffu, kd == 1 ? 1 : (kd == 2 ? -1 : 0));
     }
     const uint64_t nbase = base + (uint64_t)len;
     const uint64_t nn = (uint64_t)((int64_t)n + dn);
     const bool stop = nbase >= a.nmoves || sh.err;
+    ATab at;  // warp 1: accepted move `lane`, read here (the ring is refilled after the publish)
     if (warp == 0) {
       compose_dec(r + 1, nbase, nn, nacc, stop, etarget + (uint64_t)nacc, sh, lane);
-    } else if (warp == 1) {  // exact accepted moves for the evaluators' e tests / updates
+    } else if (warp == 1) {
       if (lane < nacc) {
         const int i = sh.acc_i[lane];
         const Proposal& pr = sh.ring[(base + i) % kRing];
-        ATab* t = a.atab + (size_t)par * kMaxAcc + lane;
         const int kind = sh.mkind[i];
-        t->ox = kind != 1 ? sh.xo[i][0] : 0.0;
-        t->oy = kind != 1 ? sh.xo[i][1] : 0.0;
-        t->oz = kind != 1 ? sh.xo[i][2] : 0.0;
-        t->nx = pr.x;
-        t->ny = pr.y;
-        t->nz = pr.z;
-        t->ia = sh.ia[i];
-        t->ib = sh.ib[i];
-        t->nn = (uint64_t)((int64_t)n + sh.acc_d[lane]);
-        t->kind = kind;
-        t->slot = i;
-        t->d = sh.acc_d[lane];
-        t->deps = 0u;
-        st_release(&t->tag, (uint64_t)r);
+        at.ox = kind != 1 ? sh.xo[i][0] : 0.0;
+        at.oy = kind != 1 ? sh.xo[i][1] : 0.0;
+        at.oz = kind != 1 ? sh.xo[i][2] : 0.0;
+        at.nx = pr.x;
+        at.ny = pr.y;
+        at.nz = pr.z;
+        at.ia = sh.ia[i];
+        at.ib = sh.ib[i];
+        at.nn = (uint64_t)((int64_t)n + sh.acc_d[lane]);
+        at.kind = kind;
+        at.slot = i;
+        at.d = sh.acc_d[lane];
       }
     } else if (warp >= 2 && warp < 2 + kMaxMoves / 32) {  // hand the round to the helpers
       Round& D = sh.done;
@@ -1875,6 +1873,23 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
     if (a.prof && tid == 0 && r > 2) a.prof[3648] += gtimer() - a.prof[3640 + (r & 1)];
 #endif
     if (tid < sh.dneed) st_relaxed(a.dec + tid, sh.dw[tid]);
+    if (warp == 1 && lane < nacc) {  // the exact table, after the publish (every reader waits for the tag)
+      ATab* t = a.atab + (size_t)par * kMaxAcc + lane;
+      t->ox = at.ox;
+      t->oy = at.oy;
+      t->oz = at.oz;
+      t->nx = at.nx;
+      t->ny = at.ny;
+      t->nz = at.nz;
+      t->ia = at.ia;
+      t->ib = at.ib;
+      t->nn = at.nn;
+      t->kind = at.kind;
+      t->slot = at.slot;
+      t->d = at.d;
+      t->deps = 0u;
+      st_release(&t->tag, (uint64_t)r);
+    }
     etarget += (uint64_t)nacc;
     prev_nacc = nacc;
     pc.mark(5);
