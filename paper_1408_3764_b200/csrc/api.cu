@@ -214,6 +214,19 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     const int max_ctas = 1 + engine_max_slots() / mg;
     if (c->engine_ctas > max_ctas) c->engine_ctas = max_ctas;
   }
+  // engine2: in a small box the moves of a round conflict early (positions
+  // within r_c, accepted moves within 2 r_c), so most evaluations of a full
+  // round are discarded and only lengthen it. About one slot per 3 r_c^3 of
+  // box, at least 64: 2k (L = 14.5) gets 18 CTAs, 2.5x the moves/s of the whole
+  // GPU at mu = -2 and the same at mu = +1; from 32k up all CTAs.
+  c->engine2_ctas = c->engine_ctas;
+  if (P.engine_ctas <= 1) {
+    const double rc3 = P.r_cut * P.r_cut * P.r_cut;
+    const double want = std::max(64.0, P.box_length * P.box_length * P.box_length / (3.0 * rc3));
+    const int mg2 = 512 / c->engine2_group;
+    const double ctas = 1.0 + std::ceil(want / mg2);
+    if (ctas < (double)c->engine2_ctas) c->engine2_ctas = (int)ctas;
+  }
   c->engine_variants = P.engine_variants > 0 ? (P.engine_variants > 15 ? 15 : P.engine_variants) : 11;
   c->engine_bias = P.engine_bias > 0 ? 1 : -1;
   // Evaluation mirror: bricks of side L/dims >= r_cut (1e-9 relative margin).

@@ -2028,7 +2028,7 @@ bool engine2_supported(const Chain& c) {
   if (std::getenv("GCMC_ENGINE_V1")) return false;
   if (c.grid.kind == GCMC_ALL_PAIRS || c.params.max_displacement > 0.0) return false;
   const int mg = kThreads / c.engine2_group;
-  return (c.engine_ctas - 1) * mg > kMaxAcc + 1 && (c.engine_ctas - 1) * mg <= kMaxSlots;
+  return (c.engine2_ctas - 1) * mg > kMaxAcc + 1 && (c.engine2_ctas - 1) * mg <= kMaxSlots;
 }
 
 gcmc_status epart_build(Chain& c, double2* out) {
@@ -2094,7 +2094,7 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
   }
   const int T = c.engine2_group;
   const int MG = kThreads / T;
-  const int G = c.engine_ctas;
+  const int G = c.engine2_ctas;
   EngineArgs a{};
   a.g = c.grid;
   a.m = c.mirror;

@@ -48,6 +48,7 @@ struct Chain {
   cudaEvent_t ev[4] = {};
   int sm_count = 0;
   int engine_ctas = 0;        // sequencer + evaluator CTAs
+  int engine2_ctas = 0;       // ... of engine2 (fewer in small boxes)
   int engine_group = 256;     // threads per evaluation slot (per-window engine)
   int engine2_group = 128;    // threads per evaluation slot (engine2)
   int engine_variants = 9;    // N-variants per displace/delete proposal (after the first)
