@@ -64,7 +64,7 @@ typedef struct gcmc_params {
   int32_t microcell_capacity; /* 0 = 5 (microcell_grid.hpp:149) */
   int32_t tail_corrections;
   uint64_t max_particles;     /* store capacity; 0 = automatic */
-  int32_t engine_ctas;        /* engine CTAs: 1 sequencer + evaluators (0 = every SM) */
+  int32_t engine_ctas;        /* engine CTAs: 1 sequencer + evaluators (0 = every SM but one; engine2: fewer in small boxes) */
   int32_t engine_group;       /* threads per evaluation slot: 128/256/512 (0 = 256 per-window engine, 128 engine2) */
   int32_t engine_variants;    /* N-variants per displace/delete proposal after the first (0 = 9) */
   int32_t engine_bias;        /* initial variant order: -1 N expected to fall, +1 rise (0 = -1) */
