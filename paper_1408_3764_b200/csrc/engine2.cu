@@ -1258,32 +1258,42 @@ struct WalkOut {
 // The walk (one warp): moves in order, tracking the N offset d (bit d + 16
 // of a move's masks); stops at the first move whose mask says stop (conflict
 // with an in-flight commit, or d outside the evaluated range) or whose accepted
-// commit would overflow. One ballot per 32 moves plus one per event; N
+// commit would overflow. Two ballots per 64 moves plus two per event; N
 // changes only at accepted insertions / deletions.
 __device__ __noinline__ WalkOut walk_warp(const uint32_t* macc, const uint32_t* mcf, const uint32_t* movf,
                                           const uint8_t* mkind, int fit, int* acc_i, int* acc_d,
                                           int8_t* acck, int lane) {
   int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
   const int nh = (fit + 31) >> 5;
+  // two blocks of 32 moves per ballot pair (independent ballots), so a block
+  // without events costs half an iteration
 #pragma unroll 1
-  for (int h = 0; h < nh; ++h) {
-    const int i = lane + 32 * h;
-    const bool in = i < fit;
-    const uint32_t am = in ? macc[i] : 0u, sm = in ? mcf[i] : 0u, om = in ? movf[i] : 0u;
-    const int kd = in ? mkind[i] : 0;
+  for (int h = 0; h < nh; h += 2) {
+    const int i0 = lane + 32 * h, i1 = i0 + 32;
+    const bool in0 = i0 < fit, in1 = i1 < fit;
+    const uint32_t am0 = in0 ? macc[i0] : 0u, sm0 = in0 ? mcf[i0] : 0u, om0 = in0 ? movf[i0] : 0u;
+    const uint32_t am1 = in1 ? macc[i1] : 0u, sm1 = in1 ? mcf[i1] : 0u, om1 = in1 ? movf[i1] : 0u;
+    const unsigned kd0 = in0 ? mkind[i0] : 0u, kd1 = in1 ? mkind[i1] : 0u;
     bool done = false;
 #pragma unroll 1
     for (;;) {
       const int j = d + kHalf;
       const bool inr = j >= 0 && j < 32;
-      const bool act = in && i >= start;
-      const bool st = act && (!inr || ((sm >> (j & 31)) & 1u));
-      const bool ac = act && inr && ((am >> (j & 31)) & 1u);
-      const unsigned ev = __ballot_sync(0xffffffffu, st || ac);
-      if (!ev) break;
-      const int el = __ffs(ev) - 1;
-      const int e = 32 * h + el;
-      const unsigned info = __shfl_sync(0xffffffffu, (st ? 1u : 0u) | (((om >> (j & 31)) & 1u) << 1) | ((unsigned)kd << 2), el);
+      const int jj = j & 31;
+      const bool act0 = in0 && i0 >= start, act1 = in1 && i1 >= start;
+      const bool st0 = act0 && (!inr || ((sm0 >> jj) & 1u));
+      const bool ac0 = act0 && inr && ((am0 >> jj) & 1u);
+      const bool st1 = act1 && (!inr || ((sm1 >> jj) & 1u));
+      const bool ac1 = act1 && inr && ((am1 >> jj) & 1u);
+      const unsigned ev0 = __ballot_sync(0xffffffffu, st0 || ac0);
+      const unsigned ev1 = __ballot_sync(0xffffffffu, st1 || ac1);
+      if (!(ev0 | ev1)) break;
+      const bool first = ev0 != 0u;
+      const int el = __ffs(first ? ev0 : ev1) - 1;
+      const int e = 32 * (first ? h : h + 1) + el;
+      const unsigned mine = first ? ((st0 ? 1u : 0u) | (((om0 >> jj) & 1u) << 1) | (kd0 << 2))
+                                  : ((st1 ? 1u : 0u) | (((om1 >> jj) & 1u) << 1) | (kd1 << 2));
+      const unsigned info = __shfl_sync(0xffffffffu, mine, el);
       if (info & 1u) {
         len = e;
         why = inr ? kStopPrev : kStopRange;
