@@ -168,38 +168,76 @@ def config_dict(a, world):
             "parallelism": f"replicas x{world} (independent chains, seed 1+rank)"}
 
 
-def cpu_baseline(snap, a, box):
+def host_cpu():
+    """(model name, logical cores) of this host (lscpu / os.cpu_count)."""
+    model = "unknown"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:  # pragma: no cover
+        pass
+    return model, os.cpu_count()
+
+
+def snapshot(sim):
+    """Full chain state for the same-trajectory check (outside device timing)."""
+    st = sim.dev.get_state()
+    return {"xyz": sim.dev.positions(), "rng": sim.dev.get_rng().serialize_hex(),
+            "step": st.step, "n": st.n, "u": st.energy, "w": st.virial,
+            "attempted": list(st.attempted), "accepted": list(st.accepted)}
+
+
+def cpu_baseline(s0, s1, a, box):
     """The reference's own Simulation::step loop (oracle/_ref, g++ -O3 with the
     reference's Release flags, 1 core) resumed (engine.hpp:244-252) from the
-    GPU chain's state at the start of the timed steps (positions, RNG, step,
-    U, W) and timed on exactly the moves of the first --cpu-steps timed GPU
-    steps. Returns the baseline dict and the reference's N afterwards (the
-    same trajectory)."""
+    GPU chain's state s0 at the start of the timed steps and timed on exactly
+    the moves of the first --cpu-steps timed GPU steps. The run doubles as a
+    parity check against the GPU chain's state s1 after those steps:
+    positions and RNG state bitwise, step / N / per-kind attempted and
+    accepted counts exact, U and W within 1e-10 relative."""
+    import numpy as np
+
     import oracle as O
 
-    xyz, rng_hex, step, u0, w0 = snap
     timed = a.cpu_steps * a.moves_per_step
+    model, ncpu = host_cpu()
+    same = None
     if os.path.exists(O.REF_SO):
         kind = "reference"
         cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
                            strategy=a.strategy)
-        sim = O.RefSim(cfg, mode=2, xyz=xyz, rng_hex=rng_hex, step=step, energy=u0, virial=w0)
+        sim = O.RefSim(cfg, mode=2, xyz=s0["xyz"], rng_hex=s0["rng"], step=s0["step"],
+                       energy=s0["u"], virial=s0["w"])
         secs, _ = sim.run(timed)
-        n_after = int(sim.state().n)
+        if s1 is not None:
+            st = sim.state()
+            tol = lambda x, y: abs(x - y) <= 1e-10 * max(1.0, abs(y))  # noqa: E731
+            checks = {
+                "positions_bitwise": bool(np.array_equal(sim.positions(), s1["xyz"])),
+                "rng_bitwise": sim.rng_hex() == s1["rng"],
+                "step_n": st.step == s1["step"] and st.n == s1["n"],
+                "counts": all(st.attempted[k] == s1["attempted"][k] - s0["attempted"][k] and
+                              st.accepted[k] == s1["accepted"][k] - s0["accepted"][k]
+                              for k in range(3)),
+                "energy_1e-10": tol(s1["u"], st.energy) and tol(s1["w"], st.virial),
+            }
+            same = {"all": all(checks.values()), **checks}
     else:
         kind = "port"
         p = O.port_params(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
                           strategy=a.strategy)
-        sim = O.PortSim(p, xyz, O.rng_from_hex(rng_hex), energy=u0, virial=w0)
+        sim = O.PortSim(p, s0["xyz"], O.rng_from_hex(s0["rng"]), energy=s0["u"], virial=s0["w"])
         t0 = time.perf_counter()
         sim.run(timed)
         secs = time.perf_counter() - t0
-        n_after = None
     return ({"value": timed / secs, "unit": "moves/s", "cores": 1, "kind": kind,
-             "sample": f"moves {step}..{step + timed} of the same chain (the first "
+             "sample": f"moves {s0['step']}..{s0['step'] + timed} of the same chain (the first "
                        f"{a.cpu_steps} of the {a.steps} timed GPU steps), reference "
                        f"Simulation::step loop resumed from the GPU chain's state there, "
-                       f"{secs:.2f} s, host {os.cpu_count()} cores, 1 used"}, n_after)
+                       f"{secs:.2f} s, 1 thread on host '{model}' ({ncpu} logical cores)"}, same)
 
 
 def run_reference(a, rank, world):
@@ -220,73 +258,14 @@ def run_reference(a, rank, world):
     # (the run stays within a few minutes on one core)
     for _ in range(a.warmup):
         sim.run(a.moves_per_step)
-    per_step = min(a.moves_per_step, 1 << 20)
-    secs = 0.0
-    for _ in range(a.steps):
-        s, _ = sim.run(per_step)
-        secs += s
-    moves = per_step * a.steps
-    v = moves / secs
-    line = {"metric": METRIC, "value": v, "unit": "moves/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(a, 1), "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "moves/s", "cores": 1,
-                             "kind": "reference" if os.path.exists(O.REF_SO) else "port",
-                             "sample": f"{a.warmup} warm-up steps of {a.moves_per_step} moves, then "
-                                       f"{a.steps} timed steps of {per_step} consecutive moves, "
-                                       "reference Simulation::step loop (oracle/_ref, g++ -O3, "
-                                       "proj/CMakeLists Release flags), same start state as the GPU arm"},
-            "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
 
-
-def main():
-    a = parse_args()
-    rank, world, local = dist_env()
-    if a.impl == "reference":
-        run_reference(a, rank, world)
-        return
-    import torch
-
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device")
-    torch.cuda.set_device(local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        pg = dist
-    from paper_1408_3764_b200 import engine as E
-    from paper_1408_3764_b200.config import RunConfig
-
-    box = (a.n0 / a.density) ** (1.0 / 3.0)
-    mu, seed = state_point(a, rank)
-    xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed)
-    cfg = RunConfig(temperature=a.temperature, chemical_potential=mu, box_length=box,
-                    strategy=a.strategy, seed=seed)
-    sim = E.Simulation(cfg, xyz, rng, device=local)
-    st0 = sim.dev.get_state()
-    u0, w0 = st0.energy, st0.virial
-
-    for _ in range(a.warmup):
-        sim.run(a.moves_per_step)
-
-    # CPU baseline: the reference resumed from this exact state (rank 0, N=1 only)
-    cpu, cpu_n = None, None
+    # CPU baseline (rank 0, N=1 only): the reference resumed from this exact
+    # state, timed on the same moves after the GPU's timed region
     if not a.cpu_steps or a.cpu_steps > a.steps:
         a.cpu_steps = a.steps
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        try:
-            stw = sim.dev.get_state()
-            snap = (sim.dev.positions(), sim.dev.get_rng().serialize_hex(), stw.step, stw.energy,
-                    stw.virial)
-            cpu, cpu_n = cpu_baseline(snap, a, box)
-        except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
-                   "sample": f"failed: {e}"}
+    want_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
+    s0 = snapshot(sim) if want_cpu else None
+    s1 = None
 
     def barrier():
         torch.cuda.synchronize()
@@ -298,19 +277,17 @@ def main():
     dev_ms = eng_ms = 0.0
     rounds = 0
     acc0 = sum(sim.dev.get_state().accepted)
-    moves0 = sim.dev.get_state().step
-    n_after_step = []
     with ClockSampler(local) as clk:
-        for _ in range(a.steps):
+        for k in range(a.steps):
             sim.run(a.moves_per_step)
-            n_after_step.append(sim.dev.get_state().n)
             r = sim.last_run
             dev_ms += r.device_ms + r.gen_ms
             eng_ms += r.device_ms
             rounds += r.rounds
+            if want_cpu and k + 1 == a.cpu_steps:
+                s1 = snapshot(sim)  # host read-back between steps: not in the device timing
     barrier()
     acc1 = sum(sim.dev.get_state().accepted)
-    n_timed_end = sim.dev.get_state().n
     # ---- end-to-end through the C ABI (run + checkpoint read-back of state,
     #      RNG and positions to host memory), wall clock
     barrier()
@@ -322,6 +299,14 @@ def main():
         sim.dev.positions()
     barrier()
     e2e_s = time.perf_counter() - t0
+
+    cpu, same = None, None
+    if want_cpu:
+        try:
+            cpu, same = cpu_baseline(s0, s1, a, box)
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {e}"}
 
     moves_rank = a.moves_per_step * a.steps
     t_dev = dev_ms / 1e3
@@ -372,9 +357,9 @@ def main():
         if cpu and cpu.get("value"):
             line["speedup_vs_cpu_e2e"] = e2e / cpu["value"]
             line["speedup_vs_cpu_device"] = value / cpu["value"]
-        if cpu_n is not None:
-            # the CPU reference ran the identical moves: same N afterwards
-            line["cpu_gpu_same_trajectory"] = bool(cpu_n == n_after_step[a.cpu_steps - 1])
+        if same is not None:
+            # the CPU reference ran the identical moves: the full state agrees
+            line["cpu_gpu_same_trajectory"] = same
         print(json.dumps(line), flush=True)
     sim.close()
     if pg:

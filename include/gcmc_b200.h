@@ -13,6 +13,7 @@
  *                                                                            cell_grid.hpp:48-68
  *   gcmc_upload_positions           ParticleStore(std::vector<Vec3>)         particles.hpp:19
  *   gcmc_download_positions         ParticleStore::positions()               particles.hpp:26
+ *   gcmc_store_set                  ParticleStore::set()                     particles.hpp:26
  *   gcmc_build                      NeighborStrategy::build()                strategy.hpp:34
  *   gcmc_delta_displace/insert/     NeighborStrategy::delta_*                strategy.hpp:36-38
  *     delete, gcmc_delta_batch
@@ -63,10 +64,13 @@ typedef struct gcmc_params {
   int32_t cell_capacity;      /* 0 = default_cell_capacity() (cell_grid.hpp:36-38) */
   int32_t microcell_capacity; /* 0 = 5 (microcell_grid.hpp:149) */
   int32_t tail_corrections;
-  uint64_t max_particles;     /* store capacity; 0 = automatic */
+  uint64_t max_particles;     /* initial store capacity (0 = automatic: as many particles as the
+                                 reference grid and the evaluation mirror can hold); the store
+                                 grows as needed, like the reference's std::vector */
   int32_t engine_ctas;        /* engine CTAs: 1 sequencer + evaluators (0 = every SM but one; engine2: fewer in small boxes) */
   int32_t engine_group;       /* threads per evaluation slot: 128/256/512 (0 = 256 per-window engine, 128 engine2) */
-  int32_t engine_variants;    /* N-variants per displace/delete proposal after the first (0 = 9) */
+  int32_t engine_variants;    /* per-window engine: N-variants per displace/delete proposal
+                                 after the first (0 = 11, at most 15) */
   int32_t engine_bias;        /* initial variant order: -1 N expected to fall, +1 rise (0 = -1) */
   int32_t engine_mode;        /* 0 = maintained-energy engine where supported (brick strategies,
                                  max_displacement = 0), 1 = per-window engine always */
@@ -114,6 +118,10 @@ gcmc_status gcmc_destroy(gcmc_dev* h);
 gcmc_status gcmc_upload_positions(gcmc_dev* h, const double* xyz, uint64_t n);
 gcmc_status gcmc_download_positions(gcmc_dev* h, double* xyz, uint64_t capacity, uint64_t* n);
 gcmc_status gcmc_build(gcmc_dev* h);
+/* Overwrites particle pid's position in the store only — the grid is NOT
+ * updated, exactly like ParticleStore::set under a live strategy. For audits'
+ * fault-injection tests (T/test_engine.cpp:186-192). */
+gcmc_status gcmc_store_set(gcmc_dev* h, uint64_t pid, const double pos[3]);
 
 /* Grid geometry: cells per axis, slots per cell, total cells. */
 gcmc_status gcmc_grid_info(gcmc_dev* h, int32_t* dims, int32_t* capacity, uint64_t* ncells);

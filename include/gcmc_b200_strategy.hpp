@@ -101,8 +101,11 @@ class GpuNeighborStrategy final : public gcmc::NeighborStrategy {
   std::size_t commit_insert(const gcmc::Vec3& p) override {
     const double q[3] = {p.x, p.y, p.z};
     uint64_t pid = 0;
-    check(gcmc_commit_insert(h_, q, &pid));
-    store_.append(p);
+    const gcmc_status s = gcmc_commit_insert(h_, q, &pid);
+    // On a cell overflow the device store has already appended the particle,
+    // as the reference's does before insert_id throws (microcell_grid.hpp:253-256).
+    if (s == GCMC_OK || s == GCMC_CELL_OVERFLOW) store_.append(p);
+    check(s);
     return static_cast<std::size_t>(pid);
   }
   void commit_delete(std::size_t pid) override {

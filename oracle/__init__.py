@@ -154,6 +154,11 @@ def ref_lib():
         lib.ref_sim_checkpoint_text.argtypes = [_p, C.c_char_p, _u64, C.POINTER(_u64)]
         lib.ref_sim_stats_row.argtypes = [_p, C.c_char_p, _u64]
         lib.ref_sim_from_checkpoint.argtypes = [C.c_char_p, C.POINTER(_p)]
+        lib.ref_sim_grid_info.argtypes = [_p, _ip, _ip, C.POINTER(_u64)]
+        lib.ref_sim_grid.argtypes = [_p, _ip, _ip]
+        lib.ref_sim_store_set.argtypes = [_p, _u64, _dp]
+        lib.ref_run_with_files.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(_u64)]
+        lib.ref_format_g17.argtypes = [_d, C.c_char_p, _u64]
         lib.ref_parse_config.argtypes = [C.c_char_p, C.POINTER(RefConfig)]
         lib.ref_serialize_config.argtypes = [C.POINTER(RefConfig), C.c_char_p, _u64]
         lib.ref_run_concurrent.argtypes = [C.POINTER(RefConfig), _dp, _u64, C.c_char_p, _d, _d,
@@ -364,6 +369,33 @@ class RefSim:
         buf = C.create_string_buffer(512)
         _chk(ref_lib().ref_sim_stats_row(self.h, buf, 512))
         return buf.value.decode()
+
+    def grid(self):
+        """(occupancy_view, slots_view) of the live strategy (empty for all_pairs)."""
+        d, cap, nc = _i32(), _i32(), _u64()
+        ref_lib().ref_sim_grid_info(self.h, C.byref(d), C.byref(cap), C.byref(nc))
+        occ = np.zeros(nc.value, np.int32)
+        slots = np.zeros(nc.value * cap.value, np.int32)
+        ref_lib().ref_sim_grid(self.h, iptr(occ), iptr(slots))
+        return occ, slots
+
+    def store_set(self, i, pos):
+        """ParticleStore::set behind the strategy's back (T/test_engine.cpp:186-192)."""
+        _chk(ref_lib().ref_sim_store_set(self.h, i, dptr(np.ascontiguousarray(pos, np.float64))))
+
+
+def ref_run_with_files(cfg_text: str, out_dir: str, resume: str | None = None) -> int:
+    """gcmc::run_with_files (driver.hpp:47-116); returns the final step."""
+    fs = _u64()
+    _chk(ref_lib().ref_run_with_files(cfg_text.encode(), out_dir.encode(),
+                                      resume.encode() if resume else None, C.byref(fs)))
+    return fs.value
+
+
+def ref_format_g17(v: float) -> str:
+    buf = C.create_string_buffer(64)
+    ref_lib().ref_format_g17(v, buf, 64)
+    return buf.value.decode()
 
 
 # --------------------------------------------------------------------------

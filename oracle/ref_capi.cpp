@@ -12,7 +12,9 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -522,6 +524,65 @@ int ref_sim_checkpoint_text(void* h, char* buf, uint64_t cap, uint64_t* needed) 
 int ref_sim_stats_row(void* h, char* buf, uint64_t cap) {
   return guarded([&] { copy_str(stats_csv_row(*static_cast<Simulation*>(h)), buf, cap); });
 }
+
+// The reference grid of a live Simulation's strategy (occupancy_view() /
+// slots_view(), microcell_grid.hpp:167-168, cell_grid.hpp:78-79): the engine
+// path's commits (remove_id / relabel_id slot order) are byte-compared
+// against it. dims = capacity = ncells = 0 for all_pairs.
+void ref_sim_grid_info(void* h, int32_t* dims, int32_t* capacity, uint64_t* ncells) {
+  const NeighborStrategy& s = static_cast<Simulation*>(h)->strategy();
+  *dims = 0;
+  *capacity = 0;
+  *ncells = 0;
+  if (const auto* g = dynamic_cast<const CellGridStrategy*>(&s)) {
+    *dims = g->cells_per_dim();
+    *capacity = g->capacity_per_cell();
+    *ncells = g->cell_count();
+  } else if (const auto* m = dynamic_cast<const MicrocellGridStrategy*>(&s)) {
+    *dims = m->dims();
+    *capacity = m->capacity_per_cell();
+    *ncells = m->cell_count();
+  }
+}
+void ref_sim_grid(void* h, int32_t* occ, int32_t* slots) {
+  const NeighborStrategy& s = static_cast<Simulation*>(h)->strategy();
+  std::span<const int32_t> o, sl;
+  if (const auto* g = dynamic_cast<const CellGridStrategy*>(&s)) {
+    o = g->occupancy_view();
+    sl = g->slots_view();
+  } else if (const auto* m = dynamic_cast<const MicrocellGridStrategy*>(&s)) {
+    o = m->occupancy_view();
+    sl = m->slots_view();
+  }
+  if (!o.empty()) std::memcpy(occ, o.data(), o.size() * 4);
+  if (!sl.empty()) std::memcpy(slots, sl.data(), sl.size() * 4);
+}
+
+// ParticleStore::set (particles.hpp:26) on a live Simulation: moves particle
+// i "behind the engine's back", as T/test_engine.cpp:186-192 does.
+int ref_sim_store_set(void* h, uint64_t i, const double* p) {
+  return guarded([&] {
+    auto* s = static_cast<Simulation*>(h);
+    if (i >= s->particles().size()) throw std::out_of_range("store: invalid particle id");
+    s->particles().set(i, {p[0], p[1], p[2]});
+  });
+}
+
+// run_with_files (driver.hpp:47-116) with a config given as key=value text
+// (config.hpp:128-211); resume may be null. Returns the final step.
+int ref_run_with_files(const char* cfg_text, const char* out_dir, const char* resume,
+                       uint64_t* final_step) {
+  return guarded([&] {
+    const RunConfig cfg = parse_config_text(cfg_text);
+    std::optional<std::filesystem::path> rp;
+    if (resume && *resume) rp = std::filesystem::path(resume);
+    const auto r = run_with_files(cfg, out_dir, rp);
+    if (final_step) *final_step = r.final_step;
+  });
+}
+
+// text.hpp:14-18 (std::to_chars general, precision 17).
+void ref_format_g17(double v, char* buf, uint64_t cap) { copy_str(format_g17(v), buf, cap); }
 
 // Restores a Simulation from reference checkpoint text (checkpoint.hpp:24-28).
 int ref_sim_from_checkpoint(const char* text, void** out) {

@@ -51,7 +51,7 @@ TRACE_DTYPE = np.dtype([("kind", "<i4"), ("accepted", "<i4"), ("delta_u", "<f8")
 
 EXPORTS = [
     "gcmc_last_error", "gcmc_version", "gcmc_create", "gcmc_destroy", "gcmc_upload_positions",
-    "gcmc_download_positions", "gcmc_build", "gcmc_grid_info", "gcmc_download_grid",
+    "gcmc_download_positions", "gcmc_build", "gcmc_store_set", "gcmc_grid_info", "gcmc_download_grid",
     "gcmc_rebuild_check", "gcmc_peak_occupancy", "gcmc_delta_displace", "gcmc_delta_insert",
     "gcmc_delta_delete", "gcmc_delta_batch", "gcmc_commit_displace", "gcmc_commit_insert",
     "gcmc_commit_delete", "gcmc_total_energy", "gcmc_energy_drift", "gcmc_seed_rng", "gcmc_set_rng_state",
@@ -89,6 +89,7 @@ def load(path: str = SO):
         "gcmc_upload_positions": [_p, _dp, _u64],
         "gcmc_download_positions": [_p, _dp, _u64, P(_u64)],
         "gcmc_build": [_p],
+        "gcmc_store_set": [_p, _u64, _dp],
         "gcmc_grid_info": [_p, P(_i32), P(_i32), P(_u64)],
         "gcmc_download_grid": [_p, P(_i32), P(_i32)],
         "gcmc_rebuild_check": [_p, C.c_char_p, C.c_size_t, P(_i32)],

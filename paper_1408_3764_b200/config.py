@@ -25,7 +25,9 @@ def _parse_double(text: str) -> float:
 
 
 def _parse_u64(text: str) -> int:
-    if not text.isdigit():
+    """text.hpp:28-34: std::from_chars over the whole text — ASCII digits only,
+    no sign, no overflow past 2^64 - 1."""
+    if not text or any(c not in "0123456789" for c in text) or int(text) >= 1 << 64:
         raise ValueError(f"bad integer value: '{text}'")
     return int(text)
 

@@ -107,6 +107,87 @@ void set_l2_policy(Chain& c) {
     cudaGetLastError();
 }
 
+// Largest particle count the spatial structures admit: every particle has a
+// reference-grid slot and a mirror record, and each overflows before the
+// store could.
+uint64_t store_bound(const Chain& c) {
+  uint64_t b = (uint64_t)c.mirror.nb * (uint64_t)c.mirror.cap;
+  if (c.grid.kind != GCMC_ALL_PAIRS) b = std::min<uint64_t>(b, (uint64_t)c.grid.cap * c.grid.ncells);
+  return b;
+}
+
+// (Re)allocates the hot arena (mirror record planes, brick occupancy, store),
+// the mirror ids, reference back-pointers and maintained energies for `mcap`
+// records per brick and `capn` particles. With `keep`, the live store, its
+// back-pointers and energies move over and the mirror is rebuilt from it.
+gcmc_status arena_alloc(Chain& c, int mcap, uint64_t capn, bool keep) {
+  Mirror& m = c.mirror;
+  const uint64_t n = keep ? c.st_host->n : 0;
+  const size_t nrec = (size_t)m.nb * mcap;
+  const size_t plane = (nrec * sizeof(double) + 255) & ~size_t(255);
+  const size_t occb = ((size_t)m.nb * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t posb = capn * sizeof(double4);
+  void* arena = nullptr;
+  int32_t *rid = nullptr, *rslot = nullptr;
+  double2* ep = nullptr;
+  CK(cudaMalloc(&arena, 3 * plane + occb + posb), "alloc arena");
+  CK(cudaMalloc(&rid, nrec * sizeof(int32_t)), "alloc mirror");
+  CK(cudaMalloc(&rslot, capn * sizeof(int32_t)), "alloc rslot");
+  CK(cudaMalloc(&ep, capn * sizeof(double2)), "alloc energies");
+  char* p = static_cast<char*>(arena);
+  double4* pos = reinterpret_cast<double4*>(p + 3 * plane + occb);
+  CK(cudaMemsetAsync(pos, 0, posb, c.stream), "memset");
+  CK(cudaMemsetAsync(p + 3 * plane, 0, occb, c.stream), "memset");
+  if (n) {
+    CK(cudaMemcpyAsync(pos, c.pos, n * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream), "grow");
+    CK(cudaMemcpyAsync(rslot, c.rslot, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream), "grow");
+    CK(cudaMemcpyAsync(ep, c.ep, n * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream), "grow");
+  }
+  CK(cudaStreamSynchronize(c.stream), "grow");
+  cudaFree(c.arena);
+  cudaFree(m.rid);
+  cudaFree(c.rslot);
+  cudaFree(c.ep);
+  c.arena = arena;
+  c.arena_bytes = 3 * plane + occb + posb;
+  m.rx = reinterpret_cast<double*>(p);
+  m.ry = reinterpret_cast<double*>(p + plane);
+  m.rz = reinterpret_cast<double*>(p + 2 * plane);
+  m.occ = reinterpret_cast<int32_t*>(p + 3 * plane);
+  m.rid = rid;
+  m.cap = mcap;
+  c.pos = pos;
+  c.rslot = rslot;
+  c.ep = ep;
+  c.capn = capn;
+  set_l2_policy(c);
+  return keep ? mirror_build(c) : GCMC_OK;
+}
+
+// Before a batch of m moves: the store must hold every particle the batch can
+// reach (min(N + m, store_bound)), growing like a vector.
+gcmc_status ensure_store(Chain& c, uint64_t m) {
+  const uint64_t need = std::min<uint64_t>(c.st_host->n + m, store_bound(c));
+  if (need <= c.capn) return GCMC_OK;
+  uint64_t cap = std::max<uint64_t>(need, c.capn + c.capn / 2);
+  cap = std::min<uint64_t>(cap, store_bound(c));
+  if (cap >= (1ull << 31)) return set_error(GCMC_ARG, "store capacity must be < 2^31 particles");
+  return arena_alloc(c, c.mirror.cap, cap, true);
+}
+
+// grid_build, doubling the mirror's records per brick while the mirror (not
+// the reference grid) is what overflows.
+gcmc_status build_growing(Chain& c) {
+  gcmc_status s = grid_build(c);
+  while (s == GCMC_CELL_OVERFLOW && c.mirror_full && c.mirror.cap < kMaxCap) {
+    if ((s = arena_alloc(c, std::min(kMaxCap, 2 * c.mirror.cap), std::max(c.capn, store_bound(c)), true)) &&
+        !(s == GCMC_CELL_OVERFLOW && c.mirror_full))
+      return s;
+    if (!s) c.built = true;
+  }
+  return s;
+}
+
 gcmc_status ensure_batch(Chain& c, uint64_t n) {
   if (n <= c.batch_cap) return GCMC_OK;
   if (c.dscratch) cudaFree(c.dscratch);
@@ -118,6 +199,139 @@ gcmc_status ensure_batch(Chain& c, uint64_t n) {
   c.batch_cap = cap;
   return GCMC_OK;
 }
+
+
+#ifdef GCMC_PHASE_TIMERS
+// Phase-timer build only (python tools/build_variant.py prof -DGCMC_PHASE_TIMERS,
+// then GCMC_LIB=...prof.so GCMC_ENGINE_PROFILE=1): per-round phase cycles and
+// latency stamps of the engine, printed to stderr after every chunk.
+#define CKV(expr, where) \
+  do {                   \
+    if ((expr) != cudaSuccess) return; \
+  } while (0)
+void profile_arm(Chain& c) {
+  if (std::getenv("GCMC_ENGINE_PROFILE") && !c.prof) {
+    CKV(cudaMalloc(&c.prof, 4096 * sizeof(unsigned long long)), "prof");
+  }
+  if (c.prof) CKV(cudaMemsetAsync(c.prof, 0, 4096 * sizeof(unsigned long long), c.stream), "prof");
+  const bool lat = std::getenv("GCMC_ENGINE_LATENCY") != nullptr;
+  if (lat && !c.stamp) CKV(cudaMalloc(&c.stamp, 8 * 8192 * sizeof(unsigned long long)), "stamp");
+  if (lat) {
+    std::vector<unsigned long long> init(8 * 8192, 0);
+    for (int k = 0; k < 8192; ++k) init[8 * k + 1] = init[8 * k + 5] = ~0ull;
+    CKV(cudaMemcpyAsync(c.stamp, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c.stream), "stamp");
+  }
+}
+
+void profile_report(Chain& c) {
+  if (!c.prof) return;
+  unsigned long long hp[64];
+  cudaMemcpy(hp, c.prof, sizeof hp, cudaMemcpyDeviceToHost);
+  const double R = (double)(hp[15] ? hp[15] : 1);
+  const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "next_shape", "walk_masks", "walk_iter", "close_to_publish"};
+  std::fprintf(stderr, "[engine prof] rounds %llu sequencer:", hp[15]);
+  for (int k = 1; k < 9; ++k) std::fprintf(stderr, " %s=%.0f", sn[k], hp[k] / R);
+  const char* en[] = {"idle", "poll_D", "assign", "setup_sync", "sums", "publish", "tail",
+                      "s_prop", "s_neww", "s_load", "s_oldw", "s_finish"};
+  std::fprintf(stderr, "\n[engine prof] evaluator(cta1,g0):");
+  for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %s=%.0f", en[k], hp[16 + k] / R);
+  std::fprintf(stderr, "\n[engine prof] helpers: work=%.0f idle=%.0f (cycles/round)\n", hp[32] / R,
+               hp[33] / R);
+  std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",
+               hp[40], hp[41], hp[42], hp[43], hp[44], hp[45]);
+  {
+    unsigned long long xp[80];
+    cudaMemcpy(xp, c.prof, sizeof xp, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "[engine prof] raw seq:");
+    for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[k] / R);
+    std::fprintf(stderr, "\n[engine prof] raw eval:");
+    for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[16 + k] / R);
+    const double ne = (double)(xp[68] ? xp[68] : 1);
+    {
+      unsigned long long cp[12];
+      cudaMemcpy(cp, c.prof + 80, sizeof cp, cudaMemcpyDeviceToHost);
+      const double nr = (double)(cp[7] ? cp[7] : 1);
+      std::fprintf(stderr, "\n[engine prof] committer (per round, %llu rounds, %.2f commits, %.2f ordered): atab=%.0f move+ext=%.0f commit_load=%.0f deps=%.0f stores=%.0f ordered=%.0f fence=%.0f go_wait=%.0f forwarded=%.2f",
+                   cp[7], cp[9] / nr, cp[8] / nr, cp[0] / nr, cp[1] / nr, cp[2] / nr, cp[3] / nr, cp[4] / nr, cp[5] / nr, cp[6] / nr, cp[10] / nr, cp[11] / nr);
+    }
+    {
+      unsigned long long d2[5];
+      cudaMemcpy(d2, c.prof + 3100, sizeof d2, cudaMemcpyDeviceToHost);
+      if (d2[0]) std::fprintf(stderr, "\n[dbg] post-commit sightings=%llu last round=%llu go=%llu etrav=%llu k=%llu", d2[0], d2[1], d2[2], d2[3], d2[4]);
+      unsigned long long d5[4];
+      cudaMemcpy(d5, c.prof + 3500, sizeof d5, cudaMemcpyDeviceToHost);
+      std::fprintf(stderr, "\n[dbg] verify per warp: max=%.0f mean=%.0f iters/round=%.1f xyz calls/round=%.2f", d5[0] / R, d5[1] / R, d5[2] / R, d5[3] / R);
+      unsigned long long lt[18];
+      cudaMemcpy(lt, c.prof + 3600, sizeof lt, cudaMemcpyDeviceToHost);
+      if (lt[12] && lt[14] && lt[17])
+        std::fprintf(stderr, "\n[dbg] latency ns: publish->CTA sees D mean=%.0f max=%.0f; publish->slot result mean=%.0f; publish->last result (per round) mean=%.0f; publish->sequencer has all mean=%.0f",
+                     (double)lt[10] / lt[12], (double)lt[11], (double)lt[13] / lt[14], (double)lt[16] / lt[17], (double)lt[15] / lt[17]);
+      unsigned long long gq[17];
+      cudaMemcpy(gq, c.prof + 3640, sizeof gq, cudaMemcpyDeviceToHost);
+      if (gq[7])
+        std::fprintf(stderr, "\n[dbg] after go (ns): close wait starts=%.0f e updates done=%.0f commits done=%.0f decision published=%.0f",
+                     (double)gq[4] / gq[7], (double)gq[5] / gq[7], (double)gq[6] / gq[7], (double)gq[8] / gq[7]);
+      if (gq[10]) std::fprintf(stderr, "; committer released sflag=%.0f", (double)gq[9] / gq[10]);
+      if (gq[12] && gq[14] && gq[16])
+        std::fprintf(stderr, "; e-update group done (mean)=%.0f committer sees go=%.0f sees e done=%.0f",
+                     (double)gq[11] / gq[12], (double)gq[15] / gq[16], (double)gq[13] / gq[14]);
+      unsigned long long tq[80];
+      cudaMemcpy(tq, c.prof + 3660, sizeof tq, cudaMemcpyDeviceToHost);
+      std::fprintf(stderr, "\n[dbg] commit order causes:");
+      for (int q = 0; q < 64; ++q)
+        if (tq[q]) std::fprintf(stderr, " %s%d.%d=%llu", q < 9 ? "cell" : (q < 18 ? "brick" : (q < 43 ? "part" : "?")),
+                                q < 18 ? (q % 9) / 3 : (q - 18) / 5, q < 18 ? q % 3 : (q - 18) % 5, tq[q]);
+      std::fprintf(stderr, " | kinds(later,earlier):");
+      for (int q = 0; q < 9; ++q) if (tq[70 + q]) std::fprintf(stderr, " %d,%d=%llu", q / 3, q % 3, tq[70 + q]);
+      unsigned long long d4[4];
+      cudaMemcpy(d4, c.prof + 3400, sizeof d4, cudaMemcpyDeviceToHost);
+      std::fprintf(stderr, "\n[dbg] barrier: tid0 wait=%.0f last-arrival-after-tid0=%.0f", d4[3] / R, d4[2] / R);
+      unsigned long long d3[4];
+      cudaMemcpy(d3, c.prof + 3110, sizeof d3, cudaMemcpyDeviceToHost);
+      if (d3[0]) std::fprintf(stderr, "\n[dbg] eval sightings=%llu round=%llu go=%llu sflag=%llu", d3[0], d3[1], d3[2], d3[3]);
+    }
+    if (std::getenv("GCMC_ROUND_LOG")) {
+      { unsigned long long el[604]; cudaMemcpy(el, c.prof + 3300, sizeof el, cudaMemcpyDeviceToHost);
+        for (unsigned long long q = 0; q < el[0] && q < 150; ++q) std::fprintf(stderr, "\n[eupd] r=%llu k=%llu kind=%llu nb=%llu cand=%llu", el[4 + 4 * q], el[5 + 4 * q] & 255, el[5 + 4 * q] >> 8, el[6 + 4 * q], el[7 + 4 * q]); }
+      unsigned long long dbg[8];
+      cudaMemcpy(dbg, c.prof + 3000, sizeof dbg, cudaMemcpyDeviceToHost);
+      std::fprintf(stderr, "\n[dbg] near=%llu flag=%llu nacc=%llu pn=%llx pt1=%llx reach=%llu pt0=%llx base=%llu",
+                   dbg[0], dbg[1], dbg[2], dbg[3], dbg[4], dbg[5], dbg[6], dbg[7]);
+      std::vector<unsigned long long> rl(800);
+      cudaMemcpy(rl.data(), c.prof + 256, 800 * 8, cudaMemcpyDeviceToHost);
+      for (int q = 1; q < 40; ++q)
+        std::fprintf(stderr, "\n[round %d] base=%llu len=%llu nacc=%llu cmin=%llu why=%llu", q, rl[4 * q],
+                     rl[4 * q + 1], rl[4 * q + 2] & 0xffff, rl[4 * q + 2] >> 16, rl[4 * q + 3]);
+    }
+    std::fprintf(stderr, "\n[engine prof] commit task (per move, %llu): atab=%.0f commit=%.0f setup+waits=%.0f traverse=%.0f\n",
+                 xp[68], xp[64] / ne, xp[65] / ne, xp[66] / ne, xp[67] / ne);
+  }
+  if (c.stamp) {
+    std::vector<unsigned long long> st(8 * 8192);
+    cudaMemcpy(st.data(), c.stamp, st.size() * 8, cudaMemcpyDeviceToHost);
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+    int cnt = 0;
+    for (int k = 2; k < 8192 && k < (int)hp[15]; ++k) {
+      const unsigned long long* e = &st[8 * k];
+      if (!e[0] || e[1] == ~0ull || !e[3] || !e[4] || !e[7]) continue;
+      a0 += (double)(long long)(e[1] - e[0]);
+      a1 += (double)(long long)(e[2] - e[0]);
+      a2 += (double)(long long)(e[3] - e[0]);
+      a3 += (double)(long long)(e[4] - e[3]);
+      a4 += (double)(long long)(e[5] - e[0]);
+      a5 += (double)e[6] / (double)e[7];
+      ++cnt;
+    }
+    if (cnt)
+      std::fprintf(stderr, "[engine prof] latency ns (%d rounds): publish->first CTA sees D=%.0f ->last CTA sees D=%.0f ->first result=%.0f ->mean result=%.0f ->last result=%.0f; last result->sequencer has all=%.0f\n",
+                   cnt, a0 / cnt, a1 / cnt, a4 / cnt, a5 / cnt, a2 / cnt, a3 / cnt);
+  }
+}
+#undef CKV
+#else
+void profile_arm(Chain&) {}
+void profile_report(Chain&) {}
+#endif
 
 }  // namespace
 
@@ -186,17 +400,6 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     delete c;
     return set_error(GCMC_ARG, "grid too large (cap * cells must be < 2^31)");
   }
-  const double vol = P.box_length * P.box_length * P.box_length;
-  uint64_t capn = P.max_particles;
-  if (capn == 0) {
-    capn = (uint64_t)(vol * 1.5) + 1024;
-    if (g.kind != GCMC_ALL_PAIRS) capn = std::min<uint64_t>(capn, (uint64_t)g.cap * g.ncells + 1);
-  }
-  if (capn >= (1ull << 31)) {  // particle ids are int32 in the grids and the engine's words
-    delete c;
-    return set_error(GCMC_ARG, "store capacity must be < 2^31 particles");
-  }
-  c->capn = capn;
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device), "props");
   c->sm_count = prop.multiProcessorCount;
@@ -253,32 +456,20 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     int reach = (int)std::ceil(ref_side / m.side);
     m.reach = reach < 1 ? 1 : reach;
   }
+  // Store capacity: the store can never outgrow the reference grid or the
+  // mirror (either overflows first), so by default it holds exactly that many
+  // particles; gcmc_run_moves grows it (with the mirror) if they grow.
+  c->capn = std::max<uint64_t>(P.max_particles, store_bound(*c));
+  if (c->capn >= (1ull << 31)) {  // particle ids are int32 in the grids and the engine's words
+    delete c;
+    return set_error(GCMC_ARG, "store capacity must be < 2^31 particles");
+  }
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
   CK(cudaStreamCreateWithFlags(&c->gen_stream, cudaStreamNonBlocking), "stream");
   for (auto& ev : c->ev) CK(cudaEventCreate(&ev), "event");
   CK(cudaEventCreateWithFlags(&c->ev_mt, cudaEventDisableTiming), "event");
   CK(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming), "event");
-  // Hot arena (every trial move reads it): mirror record planes, brick
-  // occupancy and the particle store, contiguous so one L2 access-policy
-  // window can mark it persisting (set_l2_policy).
-  {
-    Mirror& m = c->mirror;
-    const size_t nrec = (size_t)m.nb * m.cap;
-    const size_t plane = (nrec * sizeof(double) + 255) & ~size_t(255);
-    const size_t occb = ((size_t)m.nb * sizeof(int32_t) + 255) & ~size_t(255);
-    const size_t posb = capn * sizeof(double4);
-    c->arena_bytes = 3 * plane + occb + posb;
-    CK(cudaMalloc(&c->arena, c->arena_bytes), "alloc arena");
-    char* p = static_cast<char*>(c->arena);
-    m.rx = reinterpret_cast<double*>(p);
-    m.ry = reinterpret_cast<double*>(p + plane);
-    m.rz = reinterpret_cast<double*>(p + 2 * plane);
-    m.occ = reinterpret_cast<int32_t*>(p + 3 * plane);
-    c->pos = reinterpret_cast<double4*>(p + 3 * plane + occb);
-  }
-  CK(cudaMemset(c->pos, 0, capn * sizeof(double4)), "memset");
-  CK(cudaMalloc(&c->rslot, capn * sizeof(int32_t)), "alloc rslot");
-  CK(cudaMalloc(&c->ep, capn * sizeof(double2)), "alloc energies");
+  if ((s = arena_alloc(*c, c->mirror.cap, c->capn, false))) return s;
   if (g.ncells) {
     CK(cudaMalloc(&g.occ, g.ncells * sizeof(int32_t)), "alloc occ");
     CK(cudaMalloc(&g.slots, g.ncells * g.cap * sizeof(int32_t)), "alloc slots");
@@ -286,11 +477,6 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
     CK(cudaMemset(g.slots, 0xff, g.ncells * g.cap * sizeof(int32_t)), "memset");  // -1
   }
   {
-    Mirror& m = c->mirror;
-    const size_t nrec = (size_t)m.nb * m.cap;
-    CK(cudaMalloc(&m.rid, nrec * sizeof(int32_t)), "alloc mirror");
-    CK(cudaMemset(m.occ, 0, (size_t)m.nb * sizeof(int32_t)), "memset");
-    set_l2_policy(*c);
     size_t bd, br, be;
     engine_buffer_bytes(engine_max_slots(), &bd, &br, &be);
     CK(cudaMalloc(&c->eng_dec, bd), "alloc engine");
@@ -346,18 +532,25 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
 gcmc_status gcmc_upload_positions(gcmc_dev* h, const double* xyz, uint64_t n) {
   Chain& c = *H(h);
   cudaSetDevice(c.device);
-  if (n > c.capn) return set_error(GCMC_ARG, "more particles than the store capacity");
   if (n && !xyz) return set_error(GCMC_ARG, "null positions");
+  if (n >= (1ull << 31)) return set_error(GCMC_ARG, "store capacity must be < 2^31 particles");
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  if (n > c.capn && (s = arena_alloc(c, c.mirror.cap, n, false))) return s;
   std::vector<double4> tmp(n);
   for (uint64_t i = 0; i < n; ++i) tmp[i] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 0.0);
   if (n) CK(cudaMemcpyAsync(c.pos, tmp.data(), n * sizeof(double4), cudaMemcpyHostToDevice, c.stream), "upload");
-  gcmc_status s = pull_state(c);
-  if (s) return s;
+  // a new store under a new strategy: every slot reads -1 before the binning
+  // (the reference's grid ctors; build() itself only resets the occupancy,
+  // microcell_grid.hpp:194-198, cell_grid.hpp:88-92)
+  if (c.grid.ncells)
+    CK(cudaMemsetAsync(c.grid.slots, 0xff, c.grid.ncells * c.grid.cap * sizeof(int32_t), c.stream),
+       "upload");
   c.st_host->n = n;
   c.st_host->peak = 0;
   c.st_host->error = 0;
   sync_state_to_device(c);
-  return grid_build(c);
+  return build_growing(c);
 }
 
 gcmc_status gcmc_download_positions(gcmc_dev* h, double* xyz, uint64_t capacity, uint64_t* n) {
@@ -379,12 +572,26 @@ gcmc_status gcmc_download_positions(gcmc_dev* h, double* xyz, uint64_t capacity,
   return GCMC_OK;
 }
 
+gcmc_status gcmc_store_set(gcmc_dev* h, uint64_t pid, const double pos[3]) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (!pos) return set_error(GCMC_ARG, "null position");
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  if (pid >= c.st_host->n) return set_error(GCMC_INVALID_PID, "store: invalid particle id");
+  // x, y, z only: the grid, the mirror and its back-pointer word stay as they are
+  CK(cudaMemcpyAsync(reinterpret_cast<double*>(c.pos + pid), pos, 3 * sizeof(double),
+                     cudaMemcpyHostToDevice, c.stream), "store set");
+  CK(cudaStreamSynchronize(c.stream), "store set");
+  return GCMC_OK;
+}
+
 gcmc_status gcmc_build(gcmc_dev* h) {
   Chain& c = *H(h);
   cudaSetDevice(c.device);
   gcmc_status s = pull_state(c);
   if (s) return s;
-  return grid_build(c);
+  return build_growing(c);
 }
 
 gcmc_status gcmc_grid_info(gcmc_dev* h, int32_t* dims, int32_t* capacity, uint64_t* ncells) {
@@ -652,8 +859,10 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
       CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
       std::swap(c.props, c.props_next);
       std::swap(c.mt, c.mt_next);
-    } else if ((s = gen_proposals(c, m, c.stream))) {
-      return s;
+    } else {
+      // a look-ahead copy of c.mt may still be in flight on gen_stream
+      CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
+      if ((s = gen_proposals(c, m, c.stream))) return s;
     }
     c.ahead_n = 0;
     {  // the next batch, on the SM the engine leaves free
@@ -667,135 +876,49 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
       CK(cudaEventRecord(c.ev_ahead, c.gen_stream), "ahead");
       c.ahead_n = mn;
     }
-    if (std::getenv("GCMC_ENGINE_PROFILE") && !c.prof) {
-      CK(cudaMalloc(&c.prof, 4096 * sizeof(unsigned long long)), "prof");
+    // Moves [off, m) of the chunk. When the evaluation mirror (not the
+    // reference grid) runs out of records in a brick, the engine stops before
+    // the move that overflowed with everything before it committed: the
+    // mirror's records per brick double and the chunk continues there, so
+    // the mirror never fails a state the reference accepts (up to kMaxCap).
+    uint64_t off = 0;
+    for (;;) {
+      if ((s = ensure_store(c, m - off))) return s;
+      profile_arm(c);
+      Proposal* const p0 = c.props;
+      c.props += off;
+      CK(cudaEventRecord(c.ev[1], c.stream), "event");
+      s = engine_run(c, m - off, trace ? c.trace + off : nullptr, c.stream);
+      c.props = p0;
+      if (s) return s;
+      CK(cudaEventRecord(c.ev[2], c.stream), "event");
+      if ((s = pull_state(c))) return s;
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+      cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
+      gen_ms += off ? 0.f : a;
+      eng_ms += b;
+      rounds += c.st_host->rounds;
+      profile_report(c);
+      ChainState& st = *c.st_host;
+      if (st.error == GCMC_CELL_OVERFLOW && st.err_c == 1 && c.mirror.cap < kMaxCap) {
+        off += st.moves_done;
+        st.error = 0;
+        sync_state_to_device(c);
+        if ((s = arena_alloc(c, std::min(kMaxCap, 2 * c.mirror.cap), c.capn, true))) return s;
+        continue;
+      }
+      break;
     }
-    if (c.prof) CK(cudaMemsetAsync(c.prof, 0, 4096 * sizeof(unsigned long long), c.stream), "prof");
-    const bool lat = std::getenv("GCMC_ENGINE_LATENCY") != nullptr;
-    if (lat && !c.stamp) CK(cudaMalloc(&c.stamp, 8 * 8192 * sizeof(unsigned long long)), "stamp");
-    if (lat) {
-      std::vector<unsigned long long> init(8 * 8192, 0);
-      for (int k = 0; k < 8192; ++k) init[8 * k + 1] = init[8 * k + 5] = ~0ull;
-      CK(cudaMemcpyAsync(c.stamp, init.data(), init.size() * 8, cudaMemcpyHostToDevice, c.stream), "stamp");
-    }
-    CK(cudaEventRecord(c.ev[1], c.stream), "event");
-    if ((s = engine_run(c, m, trace ? c.trace : nullptr, c.stream))) return s;
-    CK(cudaEventRecord(c.ev[2], c.stream), "event");
     if (trace)
       CK(cudaMemcpyAsync(trace + done, c.trace, m * sizeof(gcmc_trace_rec), cudaMemcpyDeviceToHost,
                          c.stream),
          "trace");
-    if ((s = pull_state(c))) return s;
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
-    cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
-    gen_ms += a;
-    eng_ms += b;
-    rounds += c.st_host->rounds;
-    if (c.prof) {
-      unsigned long long hp[64];
-      cudaMemcpy(hp, c.prof, sizeof hp, cudaMemcpyDeviceToHost);
-      const double R = (double)(hp[15] ? hp[15] : 1);
-      const char* sn[] = {"-", "poll", "walk_tail", "verify", "helpers_wait", "next_shape", "walk_masks", "walk_iter", "close_to_publish"};
-      std::fprintf(stderr, "[engine prof] rounds %llu sequencer:", hp[15]);
-      for (int k = 1; k < 9; ++k) std::fprintf(stderr, " %s=%.0f", sn[k], hp[k] / R);
-      const char* en[] = {"idle", "poll_D", "assign", "setup_sync", "sums", "publish", "tail",
-                          "s_prop", "s_neww", "s_load", "s_oldw", "s_finish"};
-      std::fprintf(stderr, "\n[engine prof] evaluator(cta1,g0):");
-      for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %s=%.0f", en[k], hp[16 + k] / R);
-      std::fprintf(stderr, "\n[engine prof] helpers: work=%.0f idle=%.0f (cycles/round)\n", hp[32] / R,
-                   hp[33] / R);
-      std::fprintf(stderr, "[engine prof] round ends: end=%llu variant=%llu prev=%llu verify=%llu full=%llu overflow=%llu\n",
-                   hp[40], hp[41], hp[42], hp[43], hp[44], hp[45]);
-      {
-        unsigned long long xp[80];
-        cudaMemcpy(xp, c.prof, sizeof xp, cudaMemcpyDeviceToHost);
-        std::fprintf(stderr, "[engine prof] raw seq:");
-        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[k] / R);
-        std::fprintf(stderr, "\n[engine prof] raw eval:");
-        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d=%.0f", k, xp[16 + k] / R);
-        const double ne = (double)(xp[68] ? xp[68] : 1);
-        {
-          unsigned long long cp[12];
-          cudaMemcpy(cp, c.prof + 80, sizeof cp, cudaMemcpyDeviceToHost);
-          const double nr = (double)(cp[7] ? cp[7] : 1);
-          std::fprintf(stderr, "\n[engine prof] committer (per round, %llu rounds, %.2f commits, %.2f ordered): atab=%.0f move+ext=%.0f commit_load=%.0f deps=%.0f stores=%.0f ordered=%.0f fence=%.0f go_wait=%.0f forwarded=%.2f",
-                       cp[7], cp[9] / nr, cp[8] / nr, cp[0] / nr, cp[1] / nr, cp[2] / nr, cp[3] / nr, cp[4] / nr, cp[5] / nr, cp[6] / nr, cp[10] / nr, cp[11] / nr);
-        }
-        {
-          unsigned long long d2[5];
-          cudaMemcpy(d2, c.prof + 3100, sizeof d2, cudaMemcpyDeviceToHost);
-          if (d2[0]) std::fprintf(stderr, "\n[dbg] post-commit sightings=%llu last round=%llu go=%llu etrav=%llu k=%llu", d2[0], d2[1], d2[2], d2[3], d2[4]);
-          unsigned long long d5[4];
-          cudaMemcpy(d5, c.prof + 3500, sizeof d5, cudaMemcpyDeviceToHost);
-          std::fprintf(stderr, "\n[dbg] verify per warp: max=%.0f mean=%.0f iters/round=%.1f xyz calls/round=%.2f", d5[0] / R, d5[1] / R, d5[2] / R, d5[3] / R);
-          unsigned long long lt[18];
-          cudaMemcpy(lt, c.prof + 3600, sizeof lt, cudaMemcpyDeviceToHost);
-          if (lt[12] && lt[14] && lt[17])
-            std::fprintf(stderr, "\n[dbg] latency ns: publish->CTA sees D mean=%.0f max=%.0f; publish->slot result mean=%.0f; publish->last result (per round) mean=%.0f; publish->sequencer has all mean=%.0f",
-                         (double)lt[10] / lt[12], (double)lt[11], (double)lt[13] / lt[14], (double)lt[16] / lt[17], (double)lt[15] / lt[17]);
-          unsigned long long gq[17];
-          cudaMemcpy(gq, c.prof + 3640, sizeof gq, cudaMemcpyDeviceToHost);
-          if (gq[7])
-            std::fprintf(stderr, "\n[dbg] after go (ns): close wait starts=%.0f e updates done=%.0f commits done=%.0f decision published=%.0f",
-                         (double)gq[4] / gq[7], (double)gq[5] / gq[7], (double)gq[6] / gq[7], (double)gq[8] / gq[7]);
-          if (gq[10]) std::fprintf(stderr, "; committer released sflag=%.0f", (double)gq[9] / gq[10]);
-          if (gq[12] && gq[14] && gq[16])
-            std::fprintf(stderr, "; e-update group done (mean)=%.0f committer sees go=%.0f sees e done=%.0f",
-                         (double)gq[11] / gq[12], (double)gq[15] / gq[16], (double)gq[13] / gq[14]);
-          unsigned long long tq[80];
-          cudaMemcpy(tq, c.prof + 3660, sizeof tq, cudaMemcpyDeviceToHost);
-          std::fprintf(stderr, "\n[dbg] commit order causes:");
-          for (int q = 0; q < 64; ++q)
-            if (tq[q]) std::fprintf(stderr, " %s%d.%d=%llu", q < 9 ? "cell" : (q < 18 ? "brick" : (q < 43 ? "part" : "?")),
-                                    q < 18 ? (q % 9) / 3 : (q - 18) / 5, q < 18 ? q % 3 : (q - 18) % 5, tq[q]);
-          std::fprintf(stderr, " | kinds(later,earlier):");
-          for (int q = 0; q < 9; ++q) if (tq[70 + q]) std::fprintf(stderr, " %d,%d=%llu", q / 3, q % 3, tq[70 + q]);
-          unsigned long long d4[4];
-          cudaMemcpy(d4, c.prof + 3400, sizeof d4, cudaMemcpyDeviceToHost);
-          std::fprintf(stderr, "\n[dbg] barrier: tid0 wait=%.0f last-arrival-after-tid0=%.0f", d4[3] / R, d4[2] / R);
-          unsigned long long d3[4];
-          cudaMemcpy(d3, c.prof + 3110, sizeof d3, cudaMemcpyDeviceToHost);
-          if (d3[0]) std::fprintf(stderr, "\n[dbg] eval sightings=%llu round=%llu go=%llu sflag=%llu", d3[0], d3[1], d3[2], d3[3]);
-        }
-        if (std::getenv("GCMC_ROUND_LOG")) {
-          { unsigned long long el[604]; cudaMemcpy(el, c.prof + 3300, sizeof el, cudaMemcpyDeviceToHost);
-            for (unsigned long long q = 0; q < el[0] && q < 150; ++q) std::fprintf(stderr, "\n[eupd] r=%llu k=%llu kind=%llu nb=%llu cand=%llu", el[4 + 4 * q], el[5 + 4 * q] & 255, el[5 + 4 * q] >> 8, el[6 + 4 * q], el[7 + 4 * q]); }
-          unsigned long long dbg[8];
-          cudaMemcpy(dbg, c.prof + 3000, sizeof dbg, cudaMemcpyDeviceToHost);
-          std::fprintf(stderr, "\n[dbg] near=%llu flag=%llu nacc=%llu pn=%llx pt1=%llx reach=%llu pt0=%llx base=%llu",
-                       dbg[0], dbg[1], dbg[2], dbg[3], dbg[4], dbg[5], dbg[6], dbg[7]);
-          std::vector<unsigned long long> rl(800);
-          cudaMemcpy(rl.data(), c.prof + 256, 800 * 8, cudaMemcpyDeviceToHost);
-          for (int q = 1; q < 40; ++q)
-            std::fprintf(stderr, "\n[round %d] base=%llu len=%llu nacc=%llu cmin=%llu why=%llu", q, rl[4 * q],
-                         rl[4 * q + 1], rl[4 * q + 2] & 0xffff, rl[4 * q + 2] >> 16, rl[4 * q + 3]);
-        }
-        std::fprintf(stderr, "\n[engine prof] commit task (per move, %llu): atab=%.0f commit=%.0f setup+waits=%.0f traverse=%.0f\n",
-                     xp[68], xp[64] / ne, xp[65] / ne, xp[66] / ne, xp[67] / ne);
-      }
-      if (c.stamp) {
-        std::vector<unsigned long long> st(8 * 8192);
-        cudaMemcpy(st.data(), c.stamp, st.size() * 8, cudaMemcpyDeviceToHost);
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-        int cnt = 0;
-        for (int k = 2; k < 8192 && k < (int)hp[15]; ++k) {
-          const unsigned long long* e = &st[8 * k];
-          if (!e[0] || e[1] == ~0ull || !e[3] || !e[4] || !e[7]) continue;
-          a0 += (double)(long long)(e[1] - e[0]);
-          a1 += (double)(long long)(e[2] - e[0]);
-          a2 += (double)(long long)(e[3] - e[0]);
-          a3 += (double)(long long)(e[4] - e[3]);
-          a4 += (double)(long long)(e[5] - e[0]);
-          a5 += (double)e[6] / (double)e[7];
-          ++cnt;
-        }
-        if (cnt)
-          std::fprintf(stderr, "[engine prof] latency ns (%d rounds): publish->first CTA sees D=%.0f ->last CTA sees D=%.0f ->first result=%.0f ->mean result=%.0f ->last result=%.0f; last result->sequencer has all=%.0f\n",
-                       cnt, a0 / cnt, a1 / cnt, a4 / cnt, a5 / cnt, a2 / cnt, a3 / cnt);
-      }
+    CK(cudaStreamSynchronize(c.stream), "trace");
+    if (c.st_host->error) {
+      c.ahead_n = 0;  // the look-ahead batch continues a stream the chain did not reach
+      break;
     }
-    if (c.st_host->error) break;
     done += m;
   }
   const ChainState& st = *c.st_host;
@@ -805,7 +928,8 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     sync_state_to_device(c);
     if (err == GCMC_CELL_OVERFLOW && st.err_c == 1) {
       std::ostringstream os;
-      os << "mirror: brick " << st.err_a << " exceeds capacity " << c.mirror.cap;
+      os << "mirror: brick " << st.err_a << " exceeds capacity " << c.mirror.cap
+         << " (the evaluation mirror's limit; density too high)";
       return set_error(GCMC_CELL_OVERFLOW, os.str());
     }
     if (err == GCMC_CELL_OVERFLOW) return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, st.err_a, st.err_b));

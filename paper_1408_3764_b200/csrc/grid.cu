@@ -246,6 +246,7 @@ gcmc_status mirror_build(Chain& c) {
   int overflow = 0;
   if ((e = cudaMemcpyAsync(&overflow, flag, sizeof(int), cudaMemcpyDeviceToHost, s))) return cuda_error(e, "mirror");
   if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "mirror");
+  c.mirror_full = overflow != 0;
   if (overflow) {
     std::ostringstream os;
     os << "mirror: brick " << overflow - 1 << " exceeds capacity " << m.cap

@@ -51,12 +51,13 @@ struct Chain {
   int engine2_ctas = 0;       // ... of engine2 (fewer in small boxes)
   int engine_group = 256;     // threads per evaluation slot (per-window engine)
   int engine2_group = 128;    // threads per evaluation slot (engine2)
-  int engine_variants = 9;    // N-variants per displace/delete proposal (after the first)
+  int engine_variants = 11;   // N-variants per displace/delete proposal (after the first)
   int engine_bias = -1;       // initial variant order (+1: N expected to grow)
   uint64_t* eng_dec = nullptr;  // engine communication buffers (engine.cu)
   uint64_t* eng_res = nullptr;
   void* eng_ext = nullptr;
   bool built = false;
+  bool mirror_full = false;      // the last mirror_build overflowed a brick
   // maintained per-particle pair energy / virial (engine2.cu)
   double2* ep = nullptr;         // [capn]
   bool e_valid = false;

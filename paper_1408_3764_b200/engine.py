@@ -268,6 +268,15 @@ class _Device:
         L.check(self.lib.gcmc_energy_drift(self.h, C.byref(u), C.byref(w)))
         return u.value, w.value
 
+    def rebuild(self):
+        """NeighborStrategy::build() (strategy.hpp:34): bins the store afresh,
+        ascending ids per cell, as the reference's constructors do."""
+        L.check(self.lib.gcmc_build(self.h))
+
+    def store_set(self, pid: int, pos):
+        """ParticleStore::set (particles.hpp:26): the store only, grid untouched."""
+        L.check(self.lib.gcmc_store_set(self.h, pid, L.dptr(np.ascontiguousarray(pos, np.float64))))
+
     def rebuild_check(self) -> Optional[str]:
         buf = C.create_string_buffer(512)
         clean = C.c_int32()
@@ -311,7 +320,7 @@ class GpuNeighborStrategy(_Device):
         return self.cfg.strategy
 
     def build(self):
-        L.check(self.lib.gcmc_build(self.h))
+        self.rebuild()
 
     def delta_displace(self, pid: int, pos) -> PairInteraction:
         p = np.asarray(pos, np.float64)

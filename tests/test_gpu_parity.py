@@ -160,8 +160,6 @@ def oracle_deltas(o, kinds, pids, pts):
 @pytest.mark.parametrize("strategy", ["microcell", "cell_list", "all_pairs"])
 @pytest.mark.parametrize("n0", [2048, 32768])
 def test_deltas_within_tolerance(strategy, n0):
-    if strategy == "all_pairs" and n0 > 4096:
-        pytest.skip("all-pairs oracle too slow")
     box, xyz, _ = config(n0)
     g = E().GpuNeighborStrategy(strategy, xyz, box)
     o = oracle_grid(strategy, xyz, box)
