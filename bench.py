@@ -259,6 +259,60 @@ def run_reference(a, rank, world):
     for _ in range(a.warmup):
         sim.run(a.moves_per_step)
 
+    per_step = min(a.moves_per_step, 1 << 20)
+    secs = 0.0
+    for _ in range(a.steps):
+        s, _ = sim.run(per_step)
+        secs += s
+    moves = per_step * a.steps
+    v = moves / secs
+    line = {"metric": METRIC, "value": v, "unit": "moves/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(a, 1), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "moves/s", "cores": 1,
+                             "kind": "reference" if os.path.exists(O.REF_SO) else "port",
+                             "sample": f"{a.warmup} warm-up steps of {a.moves_per_step} moves, then "
+                                       f"{a.steps} timed steps of {per_step} consecutive moves, "
+                                       "reference Simulation::step loop (oracle/_ref, g++ -O3, "
+                                       "proj/CMakeLists Release flags), same start state as the GPU arm"},
+            "e2e": {"value": v, "unit": "moves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse_args()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    import torch
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    from paper_1408_3764_b200 import engine as E
+    from paper_1408_3764_b200.config import RunConfig
+
+    box = (a.n0 / a.density) ** (1.0 / 3.0)
+    mu, seed = state_point(a, rank)
+    xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed)
+    cfg = RunConfig(temperature=a.temperature, chemical_potential=mu, box_length=box,
+                    strategy=a.strategy, seed=seed)
+    sim = E.Simulation(cfg, xyz, rng, device=local)
+    st0 = sim.dev.get_state()
+    u0, w0 = st0.energy, st0.virial
+
+    for _ in range(a.warmup):
+        sim.run(a.moves_per_step)
+
     # CPU baseline (rank 0, N=1 only): the reference resumed from this exact
     # state, timed on the same moves after the GPU's timed region
     if not a.cpu_steps or a.cpu_steps > a.steps:
