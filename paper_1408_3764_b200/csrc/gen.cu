@@ -71,163 +71,13 @@ struct GenArgs {
   int raw_disp;      // max_displacement > 0: keep u1..u3 raw
 };
 
-__global__ void __launch_bounds__(kThreads) k_gen(GenArgs a) {
-  __shared__ uint64_t raw[2][N];
-  __shared__ double dr[2][N];
-  __shared__ int s_exit, s_count, s_end, s_done;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (a.nmoves == 0) return;
-  int cb = 0;
-  if (tid < N) raw[0][tid] = a.mt[tid];
-  const uint64_t idx0 = a.mt[N];
-  const uint64_t draws0 = a.mt[N + 1];
-  __syncthreads();
-  int entry;
-  if (idx0 >= (uint64_t)N) {
-    twist(raw[0], raw[1]);
-    cb = 1;
-    entry = 0;
-  } else {
-    entry = (int)idx0;
-  }
-  if (tid < N) dr[cb][tid] = to_uniform(temper(raw[cb][tid]));
-  uint64_t emitted = 0, consumed = 0;
-  for (;;) {
-    const int nb = cb ^ 1;
-    twist(raw[cb], raw[nb]);  // lookahead block
-    if (tid < N) dr[nb][tid] = to_uniform(temper(raw[nb][tid]));
-    __syncthreads();
-    if (warp == 0) {
-      const double* d0 = dr[cb];
-      const double* d1 = dr[nb];
-      auto D = [&](int p) { return p < N ? d0[p] : d1[p - N]; };
-      auto len_at = [&](int p) {
-        if (D(p) < a.dp) return 6;             // displace (engine.hpp:296)
-        return D(p + 1) < 0.5 ? 4 : 6;         // remove : insert (engine.hpp:298)
-      };
-      const int seg0 = entry + kSeg * lane;
-      const int seg1 = min(seg0 + kSeg, N);
-      const bool active = seg0 < N;
-      // per entry offset x in [0,6): exit offset (3 bits) and move count (3 bits)
-      uint32_t fmap = 0, cnts = 0;
-      for (int x = 0; x < 6; ++x) {
-        int p = seg0 + x, c = 0;
-        if (active)
-          while (p < seg1) {
-            p += len_at(p);
-            ++c;
-          }
-        const int ex = active ? p - seg1 : x;
-        fmap |= (uint32_t)ex << (3 * x);
-        cnts |= (uint32_t)c << (3 * x);
-      }
-      // inclusive composition scan: G_l = f_l o ... o f_0
-      uint32_t g = fmap;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t h = __shfl_up_sync(0xffffffffu, g, o);
-        if (lane >= o) {
-          uint32_t comp = 0;
-          for (int x = 0; x < 6; ++x) {
-            const uint32_t hx = (h >> (3 * x)) & 7u;
-            comp |= ((g >> (3 * hx)) & 7u) << (3 * x);
-          }
-          g = comp;
-        }
-      }
-      const uint32_t gprev = __shfl_up_sync(0xffffffffu, g, 1);
-      const int x_in = lane == 0 ? 0 : (int)(gprev & 7u);
-      const int my_cnt = active ? (int)((cnts >> (3 * x_in)) & 7u) : 0;
-      int incl = my_cnt;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int block_moves = __shfl_sync(0xffffffffu, incl, 31);
-      // exit of the last active lane = entry into the next block
-      const bool last_active = active && seg1 == N;
-      const int ex = (int)((fmap >> (3 * x_in)) & 7u);
-      if (last_active) s_exit = ex;
-      // emit
-      uint64_t mi = emitted + (uint64_t)(incl - my_cnt);
-      int p = seg0 + x_in;
-      int end_local = -1;
-      if (active)
-        while (p < seg1) {
-          const int len = len_at(p);
-          if (mi < a.nmoves) {
-            Proposal pr;
-            pr.wmask = kNoMask;
-            pr.bpt = 0;
-            pr.cell = 0;
-            const double sel = D(p);
-            if (sel < a.dp) {
-              pr.kind = 0;
-              pr.pick = D(p + 1);
-              const double u1 = D(p + 2), u2 = D(p + 3), u3 = D(p + 4);
-              if (a.raw_disp) {
-                pr.x = u1;
-                pr.y = u2;
-                pr.z = u3;
-              } else {  // point_from (engine.hpp:345-348)
-                pr.x = wrap_axis(__dmul_rn(u1, a.l), a.l);
-                pr.y = wrap_axis(__dmul_rn(u2, a.l), a.l);
-                pr.z = wrap_axis(__dmul_rn(u3, a.l), a.l);
-              }
-              pr.acc = D(p + 5);
-            } else if (D(p + 1) < 0.5) {
-              pr.kind = 2;
-              pr.pick = D(p + 2);
-              pr.acc = D(p + 3);
-              pr.x = pr.y = pr.z = 0.0;
-            } else {
-              pr.kind = 1;
-              pr.pick = 0.0;
-              pr.x = wrap_axis(__dmul_rn(D(p + 2), a.l), a.l);
-              pr.y = wrap_axis(__dmul_rn(D(p + 3), a.l), a.l);
-              pr.z = wrap_axis(__dmul_rn(D(p + 4), a.l), a.l);
-              pr.acc = D(p + 5);
-            }
-            a.out[mi] = pr;
-            if (mi == a.nmoves - 1) end_local = p + len;
-          }
-          ++mi;
-          p += len;
-        }
-      const int endv = __reduce_max_sync(0xffffffffu, end_local);
-      if (lane == 0) {
-        s_count = block_moves;
-        s_end = endv;
-        s_done = (emitted + (uint64_t)block_moves >= a.nmoves) ? 1 : 0;
-      }
-    }
-    __syncthreads();
-    if (s_done) {
-      const int endp = s_end;  // position after the last consumed draw, relative to cb
-      consumed += (uint64_t)(endp - entry);
-      const int fb = endp <= N ? cb : nb;
-      const int fidx = endp <= N ? endp : endp - N;
-      if (tid < N) a.mt[tid] = raw[fb][tid];
-      if (tid == 0) {
-        a.mt[N] = (uint64_t)fidx;
-        a.mt[N + 1] = draws0 + consumed;
-      }
-      return;
-    }
-    emitted += (uint64_t)s_count;
-    consumed += (uint64_t)(N + s_exit - entry);
-    entry = s_exit;
-    cb = nb;
-    __syncthreads();
-  }
-}
-
-// Multi-block form of k_gen: KB blocks of 312 draws per iteration. All
-// threads twist and temper the KB blocks in sequence (the MT recurrence is
-// serial); then warp w parses block w for all six possible entry offsets at
-// once (lane segment maps composed by a warp scan -> the block's entry->exit
-// map), one thread chains the KB block maps from the known entry, and every
-// warp emits its block's moves at its resolved entry and move index. Same
-// output and final MT state as k_gen, ~KB x fewer serial parse steps.
+// KB blocks of 312 draws per iteration. All threads twist and temper the KB
+// blocks in sequence (the MT recurrence is serial); then warp w parses block
+// w for all six possible entry offsets at once (lane segment maps composed by
+// a warp scan -> the block's entry->exit map), one thread chains the KB block
+// maps from the known entry, and every warp emits its block's moves at its
+// resolved entry and move index (KB x fewer serial parse steps than parsing
+// one block at a time).
 constexpr int KB = 8;
 
 __device__ __forceinline__ uint32_t compose6(uint32_t g, uint32_t h) {  // (g o h)(x) = g(h(x))
@@ -459,9 +309,7 @@ gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n
   if (n == 0) return GCMC_OK;
   GenArgs a{mt, out, n, c.params.displace_percent, c.box.l,
             c.params.max_displacement > 0.0 ? 1 : 0};
-  static const bool v1 = std::getenv("GCMC_GEN_V1") != nullptr;
-  if (v1) k_gen<<<1, kThreads, 0, s>>>(a);
-  else k_gen2<<<1, kThreads, 0, s>>>(a);
+  k_gen2<<<1, kThreads, 0, s>>>(a);
   const unsigned blocks = (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
   k_annotate<<<blocks, 256, 0, s>>>(out, n, c.mirror, c.box, c.grid, a.raw_disp);
   cudaError_t e = cudaGetLastError();

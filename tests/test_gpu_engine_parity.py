@@ -182,11 +182,16 @@ CUT_BOX = 13.23  # T/acceptance.cpp:114-128: 0.23 sigma boundary microcell
 @pytest.mark.parametrize("strategy", ["microcell", "cell_list"])
 @pytest.mark.parametrize("rc", [2.75, 3.0, 3.75, 4.25])
 def test_other_cutoffs(strategy, rc):
-    n0 = int(0.6 * CUT_BOX ** 3)
+    """validate.hpp:164-172 (the C5 coverage check): n = max(64, 0.4 V) at
+    L = 13.23, seed 17. At r_c >= 3.75 the cell list has 3^3 cells of 4.41
+    sigma side (~34 particles each at rho = 0.4, default capacity 48), so the
+    chains run it with cell_capacity = 96 on both sides (config.hpp:60)."""
+    n0 = max(64, int(0.4 * CUT_BOX ** 3))
+    cap = 96 if strategy == "cell_list" else 0
     xyz, rng = E().random_initial_configuration(n0, CUT_BOX, 0.85, 17)
-    g = E().GpuNeighborStrategy(strategy, xyz, CUT_BOX, r_cut=rc)
-    o = O.RefStrategy(strategy, xyz, CUT_BOX, rc=rc) if use_ref() else \
-        O.PortGrid(strategy, xyz, CUT_BOX, rc=rc)
+    g = E().GpuNeighborStrategy(strategy, xyz, CUT_BOX, r_cut=rc, capacity=cap)
+    o = O.RefStrategy(strategy, xyz, CUT_BOX, rc=rc, capacity=cap) if use_ref() else \
+        O.PortGrid(strategy, xyz, CUT_BOX, rc=rc, capacity=cap)
     occ, slots = g.grid()
     roc, rsl = o.grid()
     assert np.array_equal(occ, roc) and np.array_equal(slots, rsl)
@@ -196,15 +201,17 @@ def test_other_cutoffs(strategy, rc):
     assert rel(du, ref[:, 0]).max() <= TOL
     assert rel(dw, ref[:, 1]).max() <= TOL
     # 10^4-move trace through the engine
-    cfg = RC()(temperature=2.0, chemical_potential=0.0, box_length=CUT_BOX, strategy=strategy,
-               r_cut=rc, seed=17)
+    kw = {"cell_capacity": cap} if cap else {}
+    cfg = RC()(temperature=2.0, chemical_potential=-1.0, box_length=CUT_BOX, strategy=strategy,
+               r_cut=rc, seed=17, **kw)
     sim = E().Simulation(cfg, xyz, rng)
     st = sim.dev.get_state()
     os_ = oracle_sim(strategy, CUT_BOX, xyz, rng.serialize_hex(), st.energy, st.virial,
-                     temperature=2.0, chemical_potential=0.0, r_cut=rc)
+                     temperature=2.0, chemical_potential=-1.0, r_cut=rc, **kw)
     tr = sim.run(10000, trace=True)
     _, tp = os_.run(10000, trace=True)
     assert_trace_parity(tr, tp)
+    assert tr["accepted"].sum() > 200
     assert np.array_equal(sim.particles(), os_.positions())
     assert_same_grid(sim, os_, f"rc={rc}")
 
@@ -226,7 +233,9 @@ def test_overlap_clamp_on_device(strategy):
         assert abs(a.u - b[0]) <= TOL * max(1.0, abs(b[0])), (a.u, b[0])
         assert abs(a.w - b[1]) <= TOL * max(1.0, abs(b[1]))
     assert g.delta_insert(pts[1]).u >= 1e30
-    assert g.delta_insert(pts[3]).u < 1e30  # just above the floor: huge but finite
+    # just above the floor: the unclamped LJ term (~1e72 here), not the clamp value
+    big = g.delta_insert(pts[3]).u
+    assert math.isfinite(big) and big != 1e30 and big > 1e60
     # a displacement onto another particle
     a = g.delta_displace(3, pts[2])
     b = o.delta_displace(3, pts[2])
