@@ -55,6 +55,11 @@ def parse_args(argv=None):
                     help="timed steps of the CPU baseline (the first timed GPU steps; "
                          "bounded to ~20 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--chains-per-gpu", type=int, default=1,
+                    help="independent chains sharing each GPU (gcmc_run_chains); "
+                         "value = moves/s summed over all chains")
+    ap.add_argument("--no-energy", action="store_true",
+                    help="skip the full-system energy timing (full_system_energy block)")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE configs[4]: mu isotherm sweep, one 64k chain per GPU "
                          "(rank g runs mu = -3 + g, seed 1 + g)")
@@ -65,13 +70,15 @@ def parse_args(argv=None):
     return a
 
 
-def state_point(a, rank):
-    """(mu, seed) of this rank's chain: replicas of the same state point, or
-    the isotherm sweep mu_g = -3 + g. No collective is needed
-    on the hot path: chains are independent."""
+def state_point(a, rank, chain=0):
+    """(mu, seed) of chain c of rank g: replicas of the same state point, or
+    the isotherm sweep mu = -3 + g + c / K (K = 1: mu_g = -3 + g).
+    No collective is needed on the hot path: chains are independent."""
+    k = a.chains_per_gpu
+    seed = 1 + rank * k + chain
     if a.sweep:
-        return -3.0 + rank, 1 + rank
-    return a.mu, 1 + rank
+        return -3.0 + rank + chain / k, seed
+    return a.mu, seed
 
 
 def reduce_max(pg, values, device):
@@ -157,15 +164,94 @@ def config_dict(a, world):
         wl = "LJ fluid GCMC ~1M particles on 1 B200 (BASELINE configs[3])"
     else:
         wl = f"LJ fluid GCMC N0={a.n0}"
+    if a.chains_per_gpu > 1:
+        wl += f", {a.chains_per_gpu} concurrent chains per GPU (gcmc_run_chains)"
+    k = a.chains_per_gpu
+    mus = ([-3.0 + g + c / k for g in range(world) for c in range(k)] if a.sweep else a.mu)
     return {"workload": wl,
             "n0": a.n0, "density": a.density, "temperature": a.temperature,
-            "mu": [-3.0 + g for g in range(world)] if a.sweep else a.mu,
+            "mu": mus,
             "r_cut": 2.5, "strategy": a.strategy, "move_mix": "30/35/35",
-            "moves_per_step": a.moves_per_step, "chains": world,
+            "moves_per_step": a.moves_per_step, "chains": world * k,
             "start": "random sequential insertion, 0.85 sigma (init_config.hpp:19-64)",
             "l2": "state (~70 MB at 1M) stays L2/HBM resident; inputs > L2 flush not needed: "
                   "each step reads a fresh 12 MB proposal stream and random cells",
-            "parallelism": f"replicas x{world} (independent chains, seed 1+rank)"}
+            "parallelism": f"replicas x{world * k} ({k} independent chain(s) per GPU, "
+                           f"seed 1 + rank * {k} + chain)"}
+
+
+PROFILE_DIR = os.path.join(ROOT, "profiles")
+
+
+def _load_json(name):
+    try:
+        with open(os.path.join(PROFILE_DIR, name)) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def engine_profile():
+    """ncu figures of one k_engine2 launch captured in the bench window
+    (profiles/engine_ncu.json, written by tools/ncu_engine.py from
+    `ncu --set full` of `bench.py` after its warm-up steps)."""
+    return _load_json("engine_ncu.json")
+
+
+def latency_block(eprof, ns_round, moves_round):
+    """The roof that binds a serial chain: ns per round against a floor built
+    from the round's dependent steps, each at its measured latency
+    (profiles/ubench.json, tools/ubench/ubench.cu on the same B200 type):
+    decision store -> evaluators see it (one-way cross-SM visibility), window
+    positions + x_pid / e_pid (one L2 hop, issued together), the window's pair
+    terms and a 128-thread reduction (dependent FP64 chain), slot result ->
+    sequencer sees it (one-way), read / write sets (one L2 hop), then the
+    next decision. Everything else in a round (walk, verify, commits) is
+    overhead above this floor."""
+    ub = _load_json("ubench.json")
+    out = {"ns_per_round": ns_round, "moves_per_round": moves_round,
+           "ns_per_move": ns_round / max(moves_round, 1e-9)}
+    if eprof:
+        for k in ("issue_active_pct", "fp64_pipe_pct", "warps_active_pct", "l2_hit_pct",
+                  "dram_bytes_per_move"):
+            if k in eprof:
+                out[k] = eprof[k]
+        out["ncu_source"] = eprof.get("source")
+    if ub:
+        ghz = ub["sm_ghz"]
+        oneway = ub["pingpong_cycles"] / 2.0
+        hop = ub["l2_chase_cycles"]
+        pair = ub["pair_term_cycles"]
+        floor_cyc = 2 * oneway + 2 * hop + pair + 7 * ub.get("shfl_dadd_cycles", 40)
+        floor_ns = floor_cyc / ghz
+        out.update({"floor_ns_per_round": floor_ns, "floor_frac": floor_ns / ns_round,
+                    "floor_model": "2 x one-way cross-SM visibility + 2 x dependent L2 hop + "
+                                   "one pair term + 7-level shuffle reduction, "
+                                   f"{ub['source']}"})
+    return out
+
+
+def energy_block(sim, peak):
+    """Full-system energy (SURVEY §8a row c, gcmc_total_energy) on the chain's
+    final state: device time of the pass and of the pair kernel (CUDA events),
+    achieved HBM bytes (N x 24 B of coordinates: the pass's algorithmic
+    input) per second against the HBM peak, and pair evaluations per second."""
+    n = sim.dev.get_state().n
+    passes, kern = [], []
+    for _ in range(6):
+        sim.dev.total_energy()
+        p_ms, k_ms = sim.dev.energy_timing()
+        passes.append(p_ms)
+        kern.append(k_ms)
+    p_ms = statistics.median(passes[1:])
+    k_ms = statistics.median(kern[1:])
+    rho = n / sim.cfg.volume()
+    pairs = 0.5 * n * rho * 4.0 / 3.0 * math.pi * sim.cfg.r_cut ** 3  # within r_c
+    ach = 24.0 * n / (p_ms * 1e-3) / 1e9
+    return {"n": n, "pass_us": 1e3 * p_ms, "kernel_us": 1e3 * k_ms,
+            "alg_bytes": 24 * n, "achieved_gbs": ach, "hbm_frac": ach / peak,
+            "pairs_in_cutoff": pairs, "pairs_per_s": pairs / (p_ms * 1e-3),
+            "kernel": "k_energy (energy.cu)"}
 
 
 def host_cpu():
@@ -281,6 +367,21 @@ def run_reference(a, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def make_chains(a, rank, local, E, RunConfig):
+    """This rank's chains: K = --chains-per-gpu sharing the device
+    (engine_share = K); chain c is state point j = rank * K + c."""
+    box = (a.n0 / a.density) ** (1.0 / 3.0)
+    sims = []
+    for c in range(a.chains_per_gpu):
+        mu, seed = state_point(a, rank, c)
+        xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed)
+        cfg = RunConfig(temperature=a.temperature, chemical_potential=mu, box_length=box,
+                        strategy=a.strategy, seed=seed)
+        kw = {"engine_share": a.chains_per_gpu} if a.chains_per_gpu > 1 else {}
+        sims.append(E.Simulation(cfg, xyz, rng, device=local, **kw))
+    return sims, box
+
+
 def main():
     a = parse_args()
     rank, world, local = dist_env()
@@ -301,20 +402,32 @@ def main():
     from paper_1408_3764_b200 import engine as E
     from paper_1408_3764_b200.config import RunConfig
 
-    box = (a.n0 / a.density) ** (1.0 / 3.0)
-    mu, seed = state_point(a, rank)
-    xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed)
-    cfg = RunConfig(temperature=a.temperature, chemical_potential=mu, box_length=box,
-                    strategy=a.strategy, seed=seed)
-    sim = E.Simulation(cfg, xyz, rng, device=local)
-    st0 = sim.dev.get_state()
-    u0, w0 = st0.energy, st0.virial
+    sims, box = make_chains(a, rank, local, E, RunConfig)
+    sim = sims[0]
+    K = len(sims)
+
+    def step():
+        """One step: --moves-per-step moves on every chain of this rank.
+        Returns (device ms of the step, engine ms, rounds). One chain: the
+        library's CUDA events (proposal generation + engine). K chains:
+        CUDA events bracketing gcmc_run_chains (all K chains, concurrent)."""
+        if K == 1:
+            sim.run(a.moves_per_step)
+            r = sim.last_run
+            return r.device_ms + r.gen_ms, r.device_ms, r.rounds
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = E.run_chains(sims, a.moves_per_step)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        return ms, max(r.device_ms for r in res), sum(r.rounds for r in res)
 
     for _ in range(a.warmup):
-        sim.run(a.moves_per_step)
+        step()
 
-    # CPU baseline (rank 0, N=1 only): the reference resumed from this exact
-    # state, timed on the same moves after the GPU's timed region
+    # CPU baseline (rank 0, N=1 only): the reference resumed from chain 0's
+    # exact state, timed on the same moves after the GPU's timed region
     if not a.cpu_steps or a.cpu_steps > a.steps:
         a.cpu_steps = a.steps
     want_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
@@ -326,31 +439,37 @@ def main():
         if pg:
             pg.barrier()
 
-    # ---- device-resident timing (value): CUDA events inside the library
+    def accepted():
+        return sum(sum(s.dev.get_state().accepted) for s in sims)
+
+    # ---- device-resident timing (value)
     barrier()
     dev_ms = eng_ms = 0.0
     rounds = 0
-    acc0 = sum(sim.dev.get_state().accepted)
+    acc0 = accepted()
     with ClockSampler(local) as clk:
         for k in range(a.steps):
-            sim.run(a.moves_per_step)
-            r = sim.last_run
-            dev_ms += r.device_ms + r.gen_ms
-            eng_ms += r.device_ms
-            rounds += r.rounds
+            d, e, r = step()
+            dev_ms += d
+            eng_ms += e
+            rounds += r
             if want_cpu and k + 1 == a.cpu_steps:
                 s1 = snapshot(sim)  # host read-back between steps: not in the device timing
     barrier()
-    acc1 = sum(sim.dev.get_state().accepted)
+    acc1 = accepted()
     # ---- end-to-end through the C ABI (run + checkpoint read-back of state,
     #      RNG and positions to host memory), wall clock
     barrier()
     t0 = time.perf_counter()
     for _ in range(a.steps):
-        sim.run(a.moves_per_step)
-        sim.dev.get_state()
-        sim.dev.get_rng()
-        sim.dev.positions()
+        if K == 1:
+            sim.run(a.moves_per_step)
+        else:
+            E.run_chains(sims, a.moves_per_step)
+        for s_ in sims:
+            s_.dev.get_state()
+            s_.dev.get_rng()
+            s_.dev.positions()
     barrier()
     e2e_s = time.perf_counter() - t0
 
@@ -362,26 +481,22 @@ def main():
             cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}
 
-    moves_rank = a.moves_per_step * a.steps
+    moves_rank = a.moves_per_step * a.steps * K
     t_dev = dev_ms / 1e3
     t_dev, e2e_s = reduce_max(pg, [t_dev, e2e_s], "cuda")
     value = moves_rank * world / t_dev
     e2e = moves_rank * world / e2e_s
     peak, peak_kind = hbm_peak()
-    launches = (a.moves_per_step + (1 << 21) - 1) >> 21  # engine launches per step
+    launches = (a.moves_per_step + (1 << 21) - 1) >> 21  # engine launches per step and chain
     moves_per_launch = a.moves_per_step / launches
     eng_launch_s = eng_ms / 1e3 / (a.steps * launches)
     achieved = ALG_BYTES_PER_MOVE * moves_per_launch / eng_launch_s / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "engine_traffic.json")
-    if os.path.exists(tf):
-        try:
-            with open(tf) as f:
-                tj = json.load(f)
-            traffic = tj.get("bytes_per_move") * moves_per_launch  # ncu dram bytes, per launch
-        except Exception:
-            traffic = None
-    n_final = sim.dev.get_state().n
+    eprof = engine_profile()
+    traffic = eprof["dram_bytes_per_move"] * moves_per_launch if eprof else None
+    n_final = [s_.dev.get_state().n for s_ in sims]
+    ns_round = 1e9 * (eng_ms / 1e3) / max(rounds / K, 1)
+    latency = latency_block(eprof, ns_round, a.moves_per_step * a.steps * K / max(rounds, 1))
+    energy = energy_block(sim, peak) if rank == 0 and not a.no_energy else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world,
@@ -389,24 +504,27 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_dict(a, world),
             "e2e": {"value": e2e, "unit": "moves/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 256 + 314 * 8 + 24 * n_final},
+                    "d2h_bytes_per_step": sum(256 + 314 * 8 + 24 * x for x in n_final)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
                          "kernel": "k_engine2 (persistent whole-GPU Metropolis loop, maintained per-particle energies)",
                          "alg_bytes_per_move": ALG_BYTES_PER_MOVE,
-                         "note": "serial Markov chain: latency-bound, not HBM-bound; see "
-                                 "ns_per_round and DESIGN.md"},
+                         "traffic_source": eprof["source"] if eprof else None,
+                         "note": "serial Markov chain: latency-bound, not HBM-bound; the "
+                                 "latency block is the roof that binds"},
+            "latency": latency,
+            "full_system_energy": energy,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            # per step and 2^21-move chunk (gcmc_run_moves): the engine plus the
-            # look-ahead proposal generation (k_gen, k_annotate)
-            "gpu_launches": 3 * a.steps * ((a.moves_per_step + (1 << 21) - 1) >> 21),
+            # per step, chain and 2^21-move chunk (gcmc_run_moves): the engine
+            # plus the look-ahead proposal generation (k_gen2, k_annotate)
+            "gpu_launches": 3 * a.steps * K * launches,
             "ns_per_move": 1e9 * t_dev / moves_rank,
-            "ns_per_round": 1e9 * (eng_ms / 1e3) / max(rounds, 1),
-            "moves_per_round": moves_rank / max(rounds, 1),
+            "ns_per_round": ns_round,
+            "moves_per_round": a.moves_per_step * a.steps * K / max(rounds, 1),
             "acceptance": (acc1 - acc0) / moves_rank,
-            "n_final": n_final,
+            "n_final": n_final[0] if K == 1 else n_final,
         }
         if cpu and cpu.get("value"):
             line["speedup_vs_cpu_e2e"] = e2e / cpu["value"]
@@ -415,7 +533,8 @@ def main():
             # the CPU reference ran the identical moves: the full state agrees
             line["cpu_gpu_same_trajectory"] = same
         print(json.dumps(line), flush=True)
-    sim.close()
+    for s_ in sims:
+        s_.close()
     if pg:
         pg.destroy_process_group()
 

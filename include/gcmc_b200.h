@@ -28,6 +28,9 @@
  *   gcmc_set/get_state              SystemState / RunStatistics / step_      engine.hpp:112-140, 244-252
  *   gcmc_run_moves                  Simulation::step() x n  (run_to loop)    engine.hpp:293-325
  *   gcmc_random_initial_configuration  random_initial_configuration()        init_config.hpp:19-64
+ *   gcmc_run_chains                 (no reference counterpart: K independent Simulations, e.g. the
+ *                                   points of a mu/T sweep, advanced concurrently on one device;
+ *                                   PAPER.md:632 future work)
  */
 #ifndef GCMC_B200_H
 #define GCMC_B200_H
@@ -74,7 +77,9 @@ typedef struct gcmc_params {
   int32_t engine_bias;        /* initial variant order: -1 N expected to fall, +1 rise (0 = -1) */
   int32_t engine_mode;        /* 0 = maintained-energy engine where supported (brick strategies,
                                  max_displacement = 0), 1 = per-window engine always */
-  int32_t engine_pad;
+  int32_t engine_share;       /* chains that share the device (gcmc_run_chains): with engine_ctas
+                                 = 0 this chain's engine takes (SMs - share) / share CTAs
+                                 (0 or 1 = the whole device) */
 } gcmc_params;
 
 /* SystemState + RunStatistics + step counter (engine.hpp:112-140, 436). */
@@ -148,6 +153,11 @@ gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w);
  * across moves, against a from-scratch evaluation (0, 0 when not in use). */
 gcmc_status gcmc_energy_drift(gcmc_dev* h, double* max_du, double* max_dw);
 
+/* Diagnostic (no reference counterpart): device time of the last
+ * gcmc_total_energy (CUDA events on the chain's stream): the whole pass
+ * (binning, sort, pair sums, reduction) and the pair-sum kernel alone. */
+gcmc_status gcmc_energy_timing(gcmc_dev* h, double* pass_ms, double* kernel_ms);
+
 /* std::mt19937_64 state in libstdc++ order: 312 words + position (_M_p),
  * plus RngStream's draw counter. */
 gcmc_status gcmc_seed_rng(gcmc_dev* h, uint64_t seed);
@@ -164,6 +174,15 @@ gcmc_status gcmc_get_state(gcmc_dev* h, gcmc_state* s);
  * statistics. `trace` (host, nullable) receives one record per move. */
 gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace,
                            gcmc_run_result* out);
+
+/* K chains (distinct handles, any devices) each run n[i] moves concurrently,
+ * exactly as K gcmc_run_moves calls would; out (nullable) receives K results.
+ * Create each chain with gcmc_params.engine_share = K (or an explicit
+ * engine_ctas) so that the K engines and their K proposal generators fit the
+ * device together. Returns the first failing chain's status;
+ * the message names the chain. */
+gcmc_status gcmc_run_chains(gcmc_dev* const* hs, int32_t k, const uint64_t* n,
+                            gcmc_run_result* out);
 
 /* Host-side initial configuration (init_config.hpp:19-64) consuming the
  * identical MT stream; returns the RNG state left for the MC stream. */

@@ -31,7 +31,7 @@ class GcmcParams(C.Structure):
                 ("strategy", _i32), ("cell_capacity", _i32), ("microcell_capacity", _i32),
                 ("tail_corrections", _i32), ("max_particles", _u64), ("engine_ctas", _i32),
                 ("engine_group", _i32), ("engine_variants", _i32), ("engine_bias", _i32),
-                ("engine_mode", _i32), ("engine_pad", _i32)]
+                ("engine_mode", _i32), ("engine_share", _i32)]
 
 
 class GcmcState(C.Structure):
@@ -56,7 +56,7 @@ EXPORTS = [
     "gcmc_delta_delete", "gcmc_delta_batch", "gcmc_commit_displace", "gcmc_commit_insert",
     "gcmc_commit_delete", "gcmc_total_energy", "gcmc_energy_drift", "gcmc_seed_rng", "gcmc_set_rng_state",
     "gcmc_get_rng_state", "gcmc_set_state", "gcmc_get_state", "gcmc_run_moves",
-    "gcmc_random_initial_configuration",
+    "gcmc_random_initial_configuration", "gcmc_run_chains", "gcmc_energy_timing",
 ]
 
 _lib = None
@@ -110,6 +110,8 @@ def load(path: str = SO):
         "gcmc_get_state": [_p, P(GcmcState)],
         "gcmc_run_moves": [_p, _u64, _p, P(GcmcRunResult)],
         "gcmc_random_initial_configuration": [_u64, _d, _d, _u64, _dp, P(_u64), P(_u64), P(_u64)],
+        "gcmc_run_chains": [P(_p), _i32, P(_u64), P(GcmcRunResult)],
+        "gcmc_energy_timing": [_p, _dp, _dp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

@@ -10,6 +10,7 @@
 #include <random>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -412,6 +413,13 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   }
   // one SM is left to generate the next batch of proposals concurrently
   c->engine_ctas = P.engine_ctas > 1 && P.engine_ctas <= c->sm_count ? P.engine_ctas : c->sm_count - 1;
+  if (P.engine_ctas <= 1 && P.engine_share > 1) {  // K chains on one device: 1/K of the SMs each
+    c->engine_ctas = (c->sm_count - P.engine_share) / P.engine_share;
+    if (c->engine_ctas < 2) {
+      delete c;
+      return set_error(GCMC_ARG, "engine_share: too many chains for this device");
+    }
+  }
   {
     const int mg = 512 / c->engine_group;
     const int max_ctas = 1 + engine_max_slots() / mg;
@@ -467,6 +475,7 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
   CK(cudaStreamCreateWithFlags(&c->gen_stream, cudaStreamNonBlocking), "stream");
   for (auto& ev : c->ev) CK(cudaEventCreate(&ev), "event");
+  for (auto& ev : c->ev_e) CK(cudaEventCreate(&ev), "event");
   CK(cudaEventCreateWithFlags(&c->ev_mt, cudaEventDisableTiming), "event");
   CK(cudaEventCreateWithFlags(&c->ev_ahead, cudaEventDisableTiming), "event");
   if ((s = arena_alloc(*c, c->mirror.cap, c->capn, false))) return s;
@@ -523,6 +532,7 @@ gcmc_status gcmc_destroy(gcmc_dev* h) {
   cudaFree(c->iscratch);
   cudaFree(c->egrid);
   for (auto& ev : c->ev) cudaEventDestroy(ev);
+  for (auto& ev : c->ev_e) cudaEventDestroy(ev);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->gen_stream);
   delete c;
@@ -731,6 +741,13 @@ extern "C" gcmc_status gcmc_debug_energies(gcmc_dev* h, double* maint, double* f
   gcmc_status s = pull_state(c);
   if (s) return s;
   return epart_dump(c, maint, fresh);
+}
+
+gcmc_status gcmc_energy_timing(gcmc_dev* h, double* pass_ms, double* kernel_ms) {
+  Chain& c = *H(h);
+  if (pass_ms) *pass_ms = c.energy_ms[0];
+  if (kernel_ms) *kernel_ms = c.energy_ms[1];
+  return GCMC_OK;
 }
 
 gcmc_status gcmc_energy_drift(gcmc_dev* h, double* max_du, double* max_dw) {
@@ -944,6 +961,36 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     out->device_ms = eng_ms;
     out->gen_ms = gen_ms;
   }
+  return GCMC_OK;
+}
+
+// K independent chains advanced concurrently ("multiple
+// large-scale simulations on a single GPU simultaneously"). Each chain owns
+// its streams and its engine's CTAs (gcmc_params.engine_ctas), so K engines
+// share the SMs of one device; one host thread per chain drives its
+// gcmc_run_moves (the host waits on a chain's stream between its batches, not
+// on the other chains). Every chain follows exactly the trajectory it would
+// follow alone.
+gcmc_status gcmc_run_chains(gcmc_dev* const* hs, int32_t k, const uint64_t* n, gcmc_run_result* out) {
+  if (k < 0 || (k > 0 && (!hs || !n))) return set_error(GCMC_ARG, "null argument");
+  for (int32_t i = 0; i < k; ++i) {
+    if (!hs[i]) return set_error(GCMC_ARG, "null chain handle");
+    for (int32_t j = 0; j < i; ++j)
+      if (hs[j] == hs[i]) return set_error(GCMC_ARG, "a chain appears twice");
+  }
+  if (k == 1) return gcmc_run_moves(hs[0], n[0], nullptr, out);
+  std::vector<gcmc_status> st(k, GCMC_OK);
+  std::vector<std::string> msg(k);
+  std::vector<std::thread> th;
+  th.reserve(k);
+  for (int32_t i = 0; i < k; ++i)
+    th.emplace_back([&, i]() {
+      st[i] = gcmc_run_moves(hs[i], n[i], nullptr, out ? out + i : nullptr);
+      if (st[i]) msg[i] = g_last_error;  // thread-local: carried to the caller's thread
+    });
+  for (auto& t : th) t.join();
+  for (int32_t i = 0; i < k; ++i)
+    if (st[i]) return set_error(st[i], "chain " + std::to_string(i) + ": " + msg[i]);
   return GCMC_OK;
 }
 

@@ -286,6 +286,7 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   unsigned long long* overlap = (unsigned long long*)small;
   double* out = (double*)(small + 16);
   cudaStream_t s = c.stream;
+  cudaEventRecord(c.ev_e[0], s);
   cudaMemsetAsync(count, 0, nc * 4, s);
   cudaMemsetAsync(fill, 0, nc * 4, s);
   cudaMemsetAsync(overlap, 0xff, 8, s);
@@ -307,14 +308,19 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
     pf.cut2 = (float)(cut2 * (1.0 + 1e-5) + 1e-6);
     pf.on = l > 2.0 * rc + 0.5 ? 1 : 0;
   }
+  cudaEventRecord(c.ev_e[1], s);
   k_energy<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
                                                          pu, pw, overlap);
+  cudaEventRecord(c.ev_e[2], s);
   k_ereduce<<<1, 1024, 0, s>>>(nc, pu, pw, out);
+  cudaEventRecord(c.ev_e[3], s);
   double h[2];
   unsigned long long ov = 0;
   cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(&ov, overlap, 8, cudaMemcpyDeviceToHost, s);
   if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "total_energy");
+  cudaEventElapsedTime(&c.energy_ms[0], c.ev_e[0], c.ev_e[3]);
+  cudaEventElapsedTime(&c.energy_ms[1], c.ev_e[1], c.ev_e[2]);
   if (ov != ~0ull) {
     std::ostringstream os;
     os << "total_energy: particles " << (ov >> 32) << " and " << (ov & 0xffffffffu) << " overlap";

@@ -46,6 +46,8 @@ struct Chain {
   cudaStream_t stream = nullptr;
   cudaStream_t gen_stream = nullptr;
   cudaEvent_t ev[4] = {};
+  cudaEvent_t ev_e[4] = {};      // total_energy: pass start, k_energy start / end, pass end
+  float energy_ms[2] = {0.f, 0.f};  // last total_energy: whole pass, k_energy alone
   int sm_count = 0;
   int engine_ctas = 0;        // sequencer + evaluator CTAs
   int engine2_ctas = 0;       // ... of engine2 (fewer in small boxes)

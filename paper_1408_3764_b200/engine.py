@@ -181,7 +181,7 @@ def random_initial_configuration(n: int, box_length: float, min_sep: float, seed
 
 
 def _params(cfg: RunConfig, engine_ctas=0, engine_group=0, engine_variants=0, engine_bias=0,
-            max_particles=0, engine_mode=0) -> L.GcmcParams:
+            max_particles=0, engine_mode=0, engine_share=0) -> L.GcmcParams:
     return L.GcmcParams(
         box_length=cfg.box_length, epsilon=cfg.epsilon, sigma=cfg.sigma, r_cut=cfg.r_cut,
         temperature=cfg.temperature, chemical_potential=cfg.chemical_potential,
@@ -191,7 +191,7 @@ def _params(cfg: RunConfig, engine_ctas=0, engine_group=0, engine_variants=0, en
         cell_capacity=cfg.cell_capacity, microcell_capacity=cfg.microcell_capacity,
         tail_corrections=int(cfg.tail_corrections), max_particles=max_particles,
         engine_ctas=engine_ctas, engine_group=engine_group, engine_variants=engine_variants,
-        engine_bias=engine_bias, engine_mode=engine_mode)
+        engine_bias=engine_bias, engine_mode=engine_mode, engine_share=engine_share)
 
 
 class _Device:
@@ -260,6 +260,12 @@ class _Device:
         u, w = C.c_double(), C.c_double()
         L.check(self.lib.gcmc_total_energy(self.h, C.byref(u), C.byref(w)))
         return u.value, w.value
+
+    def energy_timing(self):
+        """Device ms of the last total_energy(): (whole pass, pair kernel)."""
+        a, b = C.c_double(), C.c_double()
+        L.check(self.lib.gcmc_energy_timing(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def energy_drift(self):
         """Largest |maintained - fresh| per-particle pair energy / virial
@@ -504,3 +510,22 @@ class Simulation:
 
     def close(self):
         self.dev.close()
+
+
+def run_chains(sims, n):
+    """Advance independent Simulations concurrently (gcmc_run_chains): the
+    points of a mu/T sweep as K chains on one device (create each with
+    ``engine_share=K``). ``n`` is one move count for all or one per chain.
+    Every chain ends exactly where ``sim.run(n)`` alone would leave it."""
+    sims = list(sims)
+    k = len(sims)
+    counts = [int(n)] * k if np.isscalar(n) else [int(x) for x in n]
+    if len(counts) != k:
+        raise ValueError("one move count per chain")
+    hs = (C.c_void_p * k)(*[s.dev.h for s in sims])
+    ns = (C.c_uint64 * k)(*counts)
+    res = (L.GcmcRunResult * k)()
+    L.check(L.load().gcmc_run_chains(hs, k, ns, res))
+    for s, r in zip(sims, res):
+        s.last_run = r
+    return list(res)

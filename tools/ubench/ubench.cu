@@ -1,4 +1,8 @@
 // Latency microbenchmarks for the engine's critical path (single thread).
+// Build and run (writes the JSON line bench.py's latency floor reads):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -std=c++17 \
+//        -I paper_1408_3764_b200/csrc -I include -o /tmp/ubench tools/ubench/ubench.cu
+//   /tmp/ubench --json 2> profiles/ubench.json
 #include <cstdio>
 #include <cstring>
 #include <cstdint>
@@ -81,6 +85,18 @@ __global__ void k_lat(const int* chase, int steps, const double4* recs, Box b, u
   sink[0] = x + y + acc + p + q + pid;
 }
 
+// Dependent warp reduction step: one shuffle + one DADD.
+__global__ void k_shfl(int steps, double seed, unsigned long long* out, double* sink) {
+  double x = seed + threadIdx.x;
+  const unsigned long long t0 = clock64();
+  for (int i = 0; i < steps; ++i) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, 1 + (i & 15)));
+  const unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) {
+    out[0] = (t1 - t0) / steps;
+    sink[0] = x;
+  }
+}
+
 __device__ __forceinline__ unsigned long long ldr(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -120,7 +136,9 @@ __global__ void k_relaxed_chase(const unsigned long long* chase, int steps, unsi
   out[1] = (clock64() - t0) / steps + (p == 12345678 ? 1 : 0);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const bool json = argc > 1 && !strcmp(argv[1], "--json");
+  if (json) freopen("/dev/null", "w", stdout);
   const int N = 1 << 16;
   int* h = new int[N];
   // random cyclic permutation
@@ -143,6 +161,7 @@ int main() {
   cudaMemcpy(ho, o, 16 * 8, cudaMemcpyDeviceToHost);
   const char* names[] = {"ld.cg chase", "ld chase", "dadd", "rint+dadd", "ddiv+dadd", "pair_term", "exp", "8x ld.cg batch", "double4 ld.cg chase"};
   for (int i = 0; i < 9; ++i) printf("%-22s %6llu cycles\n", names[i], ho[i]);
+  unsigned long long pp_max = 0, chase_relaxed = 0, shfl = 0;
   {
     unsigned long long *flag, *ack, *po, *ch;
     cudaMalloc(&flag, 4096); cudaMalloc(&ack, 4096); cudaMalloc(&po, 64); cudaMalloc(&ch, N * 8);
@@ -156,12 +175,34 @@ int main() {
       unsigned long long hp[4];
       cudaMemcpy(hp, po, 32, cudaMemcpyDeviceToHost);
       printf("pingpong grid %3d (sm %llu <-> sm %llu): %llu cycles per round trip\n", grid, hp[2], hp[3], hp[0]);
+      if (hp[0] > pp_max) pp_max = hp[0];
     }
     k_relaxed_chase<<<1, 32>>>(ch, 4096, po);
     cudaDeviceSynchronize();
     unsigned long long hp[2];
     cudaMemcpy(hp, po, 16, cudaMemcpyDeviceToHost);
     printf("ld.relaxed.gpu chase: %llu cycles\n", hp[1]);
+    chase_relaxed = hp[1];
+  }
+  {
+    unsigned long long* so;
+    double* ss;
+    cudaMalloc(&so, 8);
+    cudaMalloc(&ss, 8);
+    k_shfl<<<1, 32>>>(4096, 1.0, so, ss);
+    cudaMemcpy(&shfl, so, 8, cudaMemcpyDeviceToHost);
+    printf("shfl+dadd chain: %llu cycles\n", shfl);
+  }
+  if (json) {
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, 0);
+    fprintf(stderr,
+            "{\"source\": \"tools/ubench/ubench.cu on %s\", \"sm_ghz\": %.4f, \"l2_chase_cycles\": %llu, "
+            "\"l2_relaxed_chase_cycles\": %llu, \"pingpong_cycles\": %llu, \"pair_term_cycles\": %llu, "
+            "\"shfl_dadd_cycles\": %llu, \"double4_chase_cycles\": %llu}\n",
+            prop.name, khz / 1e6, ho[0], chase_relaxed, pp_max, ho[5], shfl, ho[8]);
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
