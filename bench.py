@@ -220,12 +220,12 @@ def latency_block(eprof, ns_round, moves_round):
     if ub:
         ghz = ub["sm_ghz"]
         oneway = ub["pingpong_cycles"] / 2.0
-        hop = ub["l2_chase_cycles"]
+        hop = ub["l2_relaxed_chase_cycles"]
         pair = ub["pair_term_cycles"]
         floor_cyc = 2 * oneway + 2 * hop + pair + 7 * ub.get("shfl_dadd_cycles", 40)
         floor_ns = floor_cyc / ghz
         out.update({"floor_ns_per_round": floor_ns, "floor_frac": floor_ns / ns_round,
-                    "floor_model": "2 x one-way cross-SM visibility + 2 x dependent L2 hop + "
+                    "floor_model": "2 x one-way cross-SM visibility (half the measured ping-pong) + 2 x dependent L2 hop (ld.relaxed.gpu chase) + "
                                    "one pair term + 7-level shuffle reduction, "
                                    f"{ub['source']}"})
     return out
@@ -276,7 +276,7 @@ def snapshot(sim):
             "attempted": list(st.attempted), "accepted": list(st.accepted)}
 
 
-def cpu_baseline(s0, s1, a, box):
+def cpu_baseline(s0, s1, a, box, mu):
     """The reference's own Simulation::step loop (oracle/_ref, g++ -O3 with the
     reference's Release flags, 1 core) resumed (engine.hpp:244-252) from the
     GPU chain's state s0 at the start of the timed steps and timed on exactly
@@ -293,7 +293,7 @@ def cpu_baseline(s0, s1, a, box):
     same = None
     if os.path.exists(O.REF_SO):
         kind = "reference"
-        cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+        cfg = O.ref_config(temperature=a.temperature, chemical_potential=mu, box_length=box,
                            strategy=a.strategy)
         sim = O.RefSim(cfg, mode=2, xyz=s0["xyz"], rng_hex=s0["rng"], step=s0["step"],
                        energy=s0["u"], virial=s0["w"])
@@ -313,7 +313,7 @@ def cpu_baseline(s0, s1, a, box):
             same = {"all": all(checks.values()), **checks}
     else:
         kind = "port"
-        p = O.port_params(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+        p = O.port_params(temperature=a.temperature, chemical_potential=mu, box_length=box,
                           strategy=a.strategy)
         sim = O.PortSim(p, s0["xyz"], O.rng_from_hex(s0["rng"]), energy=s0["u"], virial=s0["w"])
         t0 = time.perf_counter()
@@ -333,8 +333,9 @@ def run_reference(a, rank, world):
     import oracle as O
 
     box = (a.n0 / a.density) ** (1.0 / 3.0)
-    xyz, hexs = O.ref_initial_configuration(a.n0, box, 1)  # the reference's own init
-    cfg = O.ref_config(temperature=a.temperature, chemical_potential=a.mu, box_length=box,
+    mu, seed = state_point(a, 0)  # the GPU arm's chain 0 of rank 0
+    xyz, hexs = O.ref_initial_configuration(a.n0, box, seed)  # the reference's own init
+    cfg = O.ref_config(temperature=a.temperature, chemical_potential=mu, box_length=box,
                        strategy=a.strategy)
     # U/W only matter for reported observables, not for the trajectory; the
     # resume ctor avoids the O(N^2) total energy (hours at 1M on one core).
@@ -476,7 +477,7 @@ def main():
     cpu, same = None, None
     if want_cpu:
         try:
-            cpu, same = cpu_baseline(s0, s1, a, box)
+            cpu, same = cpu_baseline(s0, s1, a, box, sim.cfg.chemical_potential)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}

@@ -153,6 +153,11 @@ gcmc_status gcmc_total_energy(gcmc_dev* h, double* u, double* w);
  * across moves, against a from-scratch evaluation (0, 0 when not in use). */
 gcmc_status gcmc_energy_drift(gcmc_dev* h, double* max_du, double* max_dw);
 
+/* Diagnostic: total_energy() as the reference computes it — every pair i < j,
+ * no cell structure (engine.hpp:74-94's O(N^2) loop) — on the device. A
+ * cross-check of gcmc_total_energy's cell-based pass (~1 s at 1M). */
+gcmc_status gcmc_total_energy_bruteforce(gcmc_dev* h, double* u, double* w);
+
 /* Diagnostic (no reference counterpart): device time of the last
  * gcmc_total_energy (CUDA events on the chain's stream): the whole pass
  * (binning, sort, pair sums, reduction) and the pair-sum kernel alone. */

@@ -743,6 +743,14 @@ extern "C" gcmc_status gcmc_debug_energies(gcmc_dev* h, double* maint, double* f
   return epart_dump(c, maint, fresh);
 }
 
+gcmc_status gcmc_total_energy_bruteforce(gcmc_dev* h, double* u, double* w) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  gcmc_status s = pull_state(c);
+  if (s) return s;
+  return total_energy_bruteforce(c, u, w);
+}
+
 gcmc_status gcmc_energy_timing(gcmc_dev* h, double* pass_ms, double* kernel_ms) {
   Chain& c = *H(h);
   if (pass_ms) *pass_ms = c.energy_ms[0];

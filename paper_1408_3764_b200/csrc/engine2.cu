@@ -1643,6 +1643,13 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       pc.mark(2);
+#ifdef GCMC_PHASE_TIMERS
+      if (a.walk_reps == 3) {  // diagnostics: the same walk again, warm (bucket 8)
+        if (warp == 0) walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+        group_sync(1, kPollThreads);
+        pc.mark(8);
+      }
+#endif
 #pragma unroll 1
       for (int vrep = 0; vrep < (a.walk_reps == 2 ? 2 : 1); ++vrep) {
       if (vrep == 1) pc.mark(7);

@@ -43,6 +43,7 @@ struct Chain {
   // energy grid scratch (counting sort)
   void* egrid = nullptr;
   size_t egrid_bytes = 0;
+  bool egrid_fresh = false;      // egrid (re)allocated: k_energy2's block counter needs a reset
   cudaStream_t stream = nullptr;
   cudaStream_t gen_stream = nullptr;
   cudaEvent_t ev[4] = {};
@@ -85,6 +86,7 @@ gcmc_status delta_batch(Chain& c, uint64_t n, const int32_t* kinds_d, const uint
 
 // energy.cu
 gcmc_status total_energy(Chain& c, double* u, double* w);
+gcmc_status total_energy_bruteforce(Chain& c, double* u, double* w);
 
 // gen.cu: parse the next `n` moves of the MT stream into c.props[0..n).
 gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s);

@@ -261,6 +261,12 @@ class _Device:
         L.check(self.lib.gcmc_total_energy(self.h, C.byref(u), C.byref(w)))
         return u.value, w.value
 
+    def total_energy_bruteforce(self):
+        """O(N^2) device cross-check of total_energy() (no cell structure)."""
+        u, w = C.c_double(), C.c_double()
+        L.check(self.lib.gcmc_total_energy_bruteforce(self.h, C.byref(u), C.byref(w)))
+        return u.value, w.value
+
     def energy_timing(self):
         """Device ms of the last total_energy(): (whole pass, pair kernel)."""
         a, b = C.c_double(), C.c_double()

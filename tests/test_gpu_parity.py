@@ -299,6 +299,49 @@ def test_total_energy_1m_against_pair_sum_identity():
     assert abs(w - (-0.5 * dw.sum())) <= 1e-9 * abs(w)
 
 
+def test_total_energy_1m_against_device_bruteforce():
+    """the 1M total energy against an independent O(N^2) device
+    pass (every pair i < j, no cell structure, engine.hpp:74-94's loop), at
+    the bench's start configuration and after 2^22 moves; the cell pass is
+    bitwise reproducible."""
+    from paper_1408_3764_b200.config import RunConfig
+
+    box, xyz, rng = config(1 << 20)
+    sim = E().Simulation(RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box),
+                         xyz, rng)
+    for rep in range(2):
+        u, w = sim.dev.total_energy()
+        bu, bw = sim.dev.total_energy_bruteforce()
+        assert abs(u - bu) <= TOL * abs(bu), (u, bu)
+        assert abs(w - bw) <= TOL * abs(bw), (w, bw)
+        assert sim.dev.total_energy() == (u, w)
+        pass_ms, kern_ms = sim.dev.energy_timing()
+        assert 0.0 < kern_ms <= pass_ms
+        sim.run(1 << 22)
+    sim.close()
+
+
+@pytest.mark.parametrize("box,rc,n0", [(6.0, 2.5, 120), (9.0, 2.5, 400), (13.23, 4.25, 1389),
+                                       (13.23, 2.75, 1389)])
+def test_total_energy_grid_shapes(box, rc, n0):
+    """Both cell passes (27-cell stencil below 5 half-width cells per axis, the
+    5^3 sub-cell stencil from there on) against the reference's O(N^2) loop
+    and the device brute force, at several cutoffs."""
+    xyz, _ = E().random_initial_configuration(n0, box, 0.85, 3)
+    g = E().GpuNeighborStrategy("microcell", xyz, box, r_cut=rc)
+    u, w = g.total_energy()
+    bu, bw = g.total_energy_bruteforce()
+    ru, rw = C.c_double(), C.c_double()
+    if use_ref():
+        O.ref_lib().ref_total_energy(O.dptr(xyz), n0, box, 1.0, 1.0, rc, C.byref(ru), C.byref(rw))
+    else:
+        O.port_lib().orc_total_energy(O.dptr(xyz), n0, box, 1.0, 1.0, rc, C.byref(ru), C.byref(rw))
+    for a in (u, bu):
+        assert abs(a - ru.value) <= TOL * max(1.0, abs(ru.value)), (a, ru.value)
+    for a in (w, bw):
+        assert abs(a - rw.value) <= TOL * max(1.0, abs(rw.value)), (a, rw.value)
+
+
 # --------------------------------------------------------------------- (d) engine
 def run_pair(strategy, n0, moves, mu, seed=1, **kw):
     box, xyz, rng = config(n0, seed=seed)
