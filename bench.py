@@ -251,7 +251,7 @@ def energy_block(sim, peak):
     return {"n": n, "pass_us": 1e3 * p_ms, "kernel_us": 1e3 * k_ms,
             "alg_bytes": 24 * n, "achieved_gbs": ach, "hbm_frac": ach / peak,
             "pairs_in_cutoff": pairs, "pairs_per_s": pairs / (p_ms * 1e-3),
-            "kernel": "k_energy (energy.cu)"}
+            "kernel": "k_energy (energy.cu: warp per cell >= r_cut, 14-cell half shell, FP32 prefilter, compensated sums)"}
 
 
 def host_cpu():

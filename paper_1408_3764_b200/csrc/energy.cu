@@ -236,81 +236,6 @@ __global__ void k_ereduce(uint64_t ncells, const double* pu, const double* pw, d
   }
 }
 
-
-// ---------------------------------------------------------------- sub-cells
-// The default pass (boxes of at least 5 sub-cells per axis): cells of side
-// >= r_cut / 2, so the half-shell stencil (62 of the 5^3 - 1 offsets, plus
-// the own cell) covers 15.6 r_c^3 instead of the 27-cell stencil's 27 r_c^3:
-// ~75 candidates per particle for ~21 inside r_cut at rho = 0.62.
-//
-// One thread per particle, in cell order (neighbouring threads share most
-// neighbour cells, so the candidate records come from L1). Each neighbour
-// cell's periodic image shift is known from its stencil offset, so the FP32
-// prefilter is dx = q.x + (shift - p.x): one add per axis, no minimum-image
-// rounding (same error bound as the 27-cell pass, Prefilter). Survivors are
-// buffered per thread in shared memory and evaluated with the reference's
-// exact FP64 minimum image and LJ pair (common.cuh), Kahan per thread. A pair
-// is visited once: forward stencil offsets, and later records of the own cell
-// (records are id-ordered within a cell, so the result is deterministic).
-constexpr int kE2Threads = 256;
-constexpr int kE2List = 32;   // survivors buffered per thread (evaluated when full)
-constexpr int kE2Off = 62;
-
-__constant__ int c_half5[kE2Off];  // packed (ox + 2) | (oy + 2) << 4 | (oz + 2) << 8
-
-__global__ void k_esort2(uint64_t ncells, const int* __restrict__ start, const int* __restrict__ count,
-                         int* ids, int2* cs) {
-  const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (c >= ncells) return;
-  const int s0 = start[c], m = count[c];
-  cs[c] = make_int2(s0, m);
-  int* a = ids + s0;
-  for (int i = 1; i < m; ++i) {  // a few ids per sub-cell: insertion sort
-    const int v = a[i];
-    int j = i - 1;
-    while (j >= 0 && a[j] > v) {
-      a[j + 1] = a[j];
-      --j;
-    }
-    a[j + 1] = v;
-  }
-}
-
-__global__ void k_egather(uint64_t n, const int* __restrict__ ids, const double4* __restrict__ pos,
-                          double4* rec, float4* recf) {
-  const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int id = ids[r];
-  const double4 p = pos[id];
-  rec[r] = make_double4(p.x, p.y, p.z, pid_bits((uint64_t)id));
-  recf[r] = make_float4((float)p.x, (float)p.y, (float)p.z, 0.0f);
-}
-
-__device__ __forceinline__ void e2_flush(const Box& b, double px, double py, double pz, long long iid,
-                                         const double4* __restrict__ rec, const int* list, int nl,
-                                         Kahan& ku, Kahan& kw, unsigned long long* overlap) {
-  for (int k = 0; k < nl; ++k) {
-    const double4 q = rec[list[k * kE2Threads]];
-    const double r2 = min_image_dist2(px, py, pz, q.x, q.y, q.z, b);
-    if (r2 <= b.rc2) {
-      if (r2 < __dmul_rn(1e-12, b.sigma2)) {
-        long long a = iid, c = bits_pid(q.w);
-        if (a > c) {
-          const long long t = a;
-          a = c;
-          c = t;
-        }
-        atomicMin(overlap, ((unsigned long long)a << 32) | (unsigned long long)c);
-      } else {
-        double u, w;
-        lj_pair_clamped(r2, b, u, w);
-        ku.add(u);
-        kw.add(w);
-      }
-    }
-  }
-}
-
 // Deterministic compensated sum of one block's per-thread accumulators.
 __device__ __forceinline__ void block_sum_comp(Kahan ku, Kahan kw, double* su, double* sw,
                                                double& ou, double& ow) {
@@ -329,83 +254,6 @@ __device__ __forceinline__ void block_sum_comp(Kahan ku, Kahan kw, double* su, d
     ow = warp_sum_comp(k2);
   }
 }
-
-__global__ void __launch_bounds__(kE2Threads)
-    k_energy2(EGrid eg, Box b, Prefilter pf, uint64_t n, const int2* __restrict__ cs,
-              const double4* __restrict__ rec, const float4* __restrict__ recf, double* part,
-              unsigned* done, double* out, unsigned long long* overlap) {
-  __shared__ int list_s[kE2List * kE2Threads];
-  __shared__ double su[kE2Threads / 32], sw[kE2Threads / 32];
-  __shared__ bool last;
-  const uint64_t t = blockIdx.x * (uint64_t)kE2Threads + threadIdx.x;
-  int* list = list_s + threadIdx.x;
-  Kahan ku = {0, 0}, kw = {0, 0};
-  if (t < n) {
-    const double4 p = rec[t];
-    const float4 pf4 = recf[t];
-    const long long iid = bits_pid(p.w);
-    const int d = eg.dims;
-    const int cx = ecoord(eg, p.x), cy = ecoord(eg, p.y), cz = ecoord(eg, p.z);
-    const float L = pf.l;
-    int nl = 0;
-    auto test = [&](int r, float ox, float oy, float oz) {
-      const float4 q = recf[r];
-      const float dx = q.x + ox, dy = q.y + oy, dz = q.z + oz;
-      if (!pf.on || dx * dx + dy * dy + dz * dz <= pf.cut2) {
-        list[nl * kE2Threads] = r;
-        if (++nl == kE2List) {
-          e2_flush(b, p.x, p.y, p.z, iid, rec, list, nl, ku, kw, overlap);
-          nl = 0;
-        }
-      }
-    };
-    {  // own cell: later records
-      const int2 c0 = cs[cx + d * (cy + d * cz)];
-      for (int r = (int)t + 1; r < c0.x + c0.y; ++r) test(r, -pf4.x, -pf4.y, -pf4.z);
-    }
-#pragma unroll 1
-    for (int o = 0; o < kE2Off; ++o) {
-      const int code = c_half5[o];
-      int nx = cx + (code & 15) - 2, ny = cy + ((code >> 4) & 15) - 2, nz = cz + (code >> 8) - 2;
-      // image of the neighbour cell adjacent to the own cell: shift by -L / +L
-      const float sx = nx < 0 ? -L : (nx >= d ? L : 0.0f);
-      const float sy = ny < 0 ? -L : (ny >= d ? L : 0.0f);
-      const float sz = nz < 0 ? -L : (nz >= d ? L : 0.0f);
-      nx += nx < 0 ? d : (nx >= d ? -d : 0);
-      ny += ny < 0 ? d : (ny >= d ? -d : 0);
-      nz += nz < 0 ? d : (nz >= d ? -d : 0);
-      const int2 c2 = cs[nx + d * (ny + d * nz)];
-      const float ox = sx - pf4.x, oy = sy - pf4.y, oz = sz - pf4.z;
-      for (int r = c2.x; r < c2.x + c2.y; ++r) test(r, ox, oy, oz);
-    }
-    e2_flush(b, p.x, p.y, p.z, iid, rec, list, nl, ku, kw, overlap);
-  }
-  double bu, bw;
-  block_sum_comp(ku, kw, su, sw, bu, bw);
-  // the last block to finish sums the block partials in block order
-  if (threadIdx.x == 0) {
-    part[2 * blockIdx.x] = bu;
-    part[2 * blockIdx.x + 1] = bw;
-    __threadfence();
-    last = atomicAdd(done, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  Kahan k1 = {0, 0}, k2 = {0, 0};
-  for (unsigned i = threadIdx.x; i < gridDim.x; i += kE2Threads) {
-    k1.add(__ldcg(part + 2 * i));
-    k2.add(__ldcg(part + 2 * i + 1));
-  }
-  __syncthreads();
-  block_sum_comp(k1, k2, su, sw, bu, bw);
-  if (threadIdx.x == 0) {
-    out[0] = bu;
-    out[1] = bw;
-    *done = 0u;  // ready for the next pass
-  }
-}
-
 
 // O(N^2) cross-check (gcmc_total_energy_bruteforce): every pair i < j with
 // the FP32 minimum image as a prefilter and the reference's FP64 minimum
@@ -482,6 +330,7 @@ __global__ void __launch_bounds__(kBfThreads)
   }
 }
 
+
 inline unsigned blocks(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -491,34 +340,26 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   *u = 0.0;
   *w = 0.0;
   if (n < 2) return GCMC_OK;
-  // compute_cell_dims (cell_grid.hpp:27-33) for a side of at least `side`
+  // coarse grid: compute_cell_dims (cell_grid.hpp:27-33)
   const double l = c.box.l, rc = c.box.rc;
-  auto dims_for = [l](double side) {
-    int t = (int)(l / side);
-    while ((double)(t + 1) * side <= l) ++t;
-    while (t > 1 && (double)t * side > l) --t;
-    return t;
-  };
-  const int t2 = dims_for(0.5 * rc);
-  const bool sub = t2 >= 5;  // half-width sub-cells, 5^3 stencil (distinct cells)
-  int t = sub ? t2 : dims_for(rc);
+  int t = (int)(l / rc);
+  while ((double)(t + 1) * rc <= l) ++t;
+  while (t > 1 && (double)t * rc > l) --t;
   if (t < 3) t = 3;
   EGrid eg{t, 1.0 / (l / t), (uint64_t)t * t * t};
   const uint64_t nc = eg.ncells;
-  const unsigned nblk = blocks(n, kE2Threads);
   // scratch layout
   size_t scan_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, (int)nc);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t need = al(n * 4) * 2 + al(nc * 4) * 3 + al(nc * 8) + al(n * 32) + al(n * 16) +
-                      al(nc * 8) * 2 + al(nblk * 16) + al(64) + al(scan_bytes);
+  const size_t need = al(n * 4) * 2 + al(nc * 4) * 3 + al(n * 32) + al(n * 16) + al(nc * 8) * 2 +
+                      al(64) + al(scan_bytes);
   cudaError_t e;
   if (need > c.egrid_bytes) {
     if (c.egrid) cudaFree(c.egrid);
     c.egrid = nullptr;
     if ((e = cudaMalloc(&c.egrid, need))) return cuda_error(e, "total_energy alloc");
     c.egrid_bytes = need;
-    c.egrid_fresh = true;
   }
   char* p = static_cast<char*>(c.egrid);
   auto take = [&](size_t bytes) {
@@ -531,37 +372,30 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   int* count = (int*)take(nc * 4);
   int* start = (int*)take(nc * 4);
   int* fill = (int*)take(nc * 4);
-  int2* cs = (int2*)take(nc * 8);
   double4* rec = (double4*)take(n * 32);
   float4* recf = (float4*)take(n * 16);
   double* pu = (double*)take(nc * 8);
   double* pw = (double*)take(nc * 8);
-  double* part = (double*)take(nblk * 16);
   char* small = take(64);
   void* scan_tmp = take(scan_bytes);
   unsigned long long* overlap = (unsigned long long*)small;
   double* out = (double*)(small + 16);
-  unsigned* done = (unsigned*)(small + 32);
   cudaStream_t s = c.stream;
   cudaEventRecord(c.ev_e[0], s);
-  if (c.egrid_fresh) {
-    cudaMemsetAsync(done, 0, 4, s);  // k_energy2 leaves it at 0 after every pass
-    c.egrid_fresh = false;
-  }
   cudaMemsetAsync(count, 0, nc * 4, s);
   cudaMemsetAsync(fill, 0, nc * 4, s);
   cudaMemsetAsync(overlap, 0xff, 8, s);
   k_ecount<<<blocks(n, 256), 256, 0, s>>>(eg, c.pos, n, cid, count);
   cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, count, start, (int)nc, s);
   k_escatter<<<blocks(n, 256), 256, 0, s>>>(n, cid, start, fill, ids);
+  k_esort<<<blocks(nc * 32, 256), 256, 0, s>>>(nc, start, count, ids, c.pos, rec, recf);
   // FP32 prefilter: the bound adds 2 sqrt(3) r_cut delta + 3 delta^2 (plus
   // float rounding of the sum) to r_cut^2. Off when the minimum-image choice
   // itself could differ between FP32 and FP64 (L close to 2 r_cut).
   Prefilter pf;
   {
-    // per-axis error of the FP32 displacement: inputs, difference, and the
-    // L * rint product (or the image shift) each contribute at most L 2^-24
-    // -> delta = 3 * (3 L 2^-24)
+    // per-axis error of the FP32 minimum image: inputs, difference, and the
+    // L * rint product each contribute at most L 2^-24 -> delta = 3 * (3 L 2^-24)
     const double delta = 9.0 * l * std::ldexp(1.0, -24);
     const double cut2 = c.box.rc2 + 2.0 * rc * std::sqrt(3.0) * delta + 3.0 * delta * delta;
     pf.l = (float)l;
@@ -569,38 +403,17 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
     pf.cut2 = (float)(cut2 * (1.0 + 1e-5) + 1e-6);
     pf.on = l > 2.0 * rc + 0.5 ? 1 : 0;
   }
-  if (sub) {
-    static bool stencil_set[256] = {};  // the constant table is per device
-    if (!stencil_set[c.device & 255]) {
-      int h[kE2Off], k = 0;
-      for (int oz = -2; oz <= 2; ++oz)
-        for (int oy = -2; oy <= 2; ++oy)
-          for (int ox = -2; ox <= 2; ++ox)
-            if (oz > 0 || (oz == 0 && (oy > 0 || (oy == 0 && ox > 0))))
-              h[k++] = (ox + 2) | ((oy + 2) << 4) | ((oz + 2) << 8);
-      if ((e = cudaMemcpyToSymbol(c_half5, h, sizeof h))) return cuda_error(e, "total_energy stencil");
-      stencil_set[c.device & 255] = true;
-    }
-    k_esort2<<<blocks(nc, 256), 256, 0, s>>>(nc, start, count, ids, cs);
-    k_egather<<<blocks(n, 256), 256, 0, s>>>(n, ids, c.pos, rec, recf);
-    cudaEventRecord(c.ev_e[1], s);
-    k_energy2<<<nblk, kE2Threads, 0, s>>>(eg, c.box, pf, n, cs, rec, recf, part, done, out, overlap);
-    cudaEventRecord(c.ev_e[2], s);
-  } else {
-    k_esort<<<blocks(nc * 32, 256), 256, 0, s>>>(nc, start, count, ids, c.pos, rec, recf);
-    cudaEventRecord(c.ev_e[1], s);
-    k_energy<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
-                                                           pu, pw, overlap);
-    cudaEventRecord(c.ev_e[2], s);
-    k_ereduce<<<1, 1024, 0, s>>>(nc, pu, pw, out);
-  }
+  cudaEventRecord(c.ev_e[1], s);
+  k_energy<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
+                                                         pu, pw, overlap);
+  cudaEventRecord(c.ev_e[2], s);
+  k_ereduce<<<1, 1024, 0, s>>>(nc, pu, pw, out);
   cudaEventRecord(c.ev_e[3], s);
   double h[2];
   unsigned long long ov = 0;
   cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(&ov, overlap, 8, cudaMemcpyDeviceToHost, s);
   if ((e = cudaStreamSynchronize(s))) return cuda_error(e, "total_energy");
-  if ((e = cudaGetLastError())) return cuda_error(e, "total_energy");
   cudaEventElapsedTime(&c.energy_ms[0], c.ev_e[0], c.ev_e[3]);
   cudaEventElapsedTime(&c.energy_ms[1], c.ev_e[1], c.ev_e[2]);
   if (ov != ~0ull) {

@@ -70,7 +70,6 @@ constexpr int kResWords = 3;
 constexpr int kPollWarps = 12;
 constexpr int kMaxSlots = 768;            // buffer sizing: evaluator groups
 constexpr double kHugeTerm = 1e4;
-constexpr int kBitWords = 4096;
 constexpr int kEBuf = 384;              // buffered energy updates per group in shared memory
 constexpr int kEBig = 4096;             // ... and in global memory beyond that          // verify bitmap: up to 131072 bricks         // |pair(n, x_pid)| above this: re-sum without pid
 
@@ -1219,7 +1218,6 @@ struct SeqShared {
   uint64_t st_n[kMaxAcc + 1];
   double st_v[kMaxAcc + 1][4];
   unsigned long long stops[kNStop];
-  uint32_t nbits[kBitWords];  // verify: bricks near a changed point of the round
   unsigned smp[kMH];          // statistics: sampled steps of the round
   int8_t acck[kMaxMoves];     // accepted index of a consumed move (-1: rejected)
   uint8_t nbef[kMaxMoves];    // accepted moves before a consumed move
@@ -1551,7 +1549,6 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool grid = a.g.kind != GCMC_ALL_PAIRS;
   constexpr int kPollThreads = kPollWarps * 32;
-  for (int q = tid; q < kBitWords; q += kThreads) sh.nbits[q] = 0u;
   if (tid == 0) {
     sh.ks = *a.st;
     sh.done.len = 0;
@@ -1617,8 +1614,12 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       }
       group_sync(1, kPollThreads);
       // every evaluation of round r has read its state: the previous round's
-      // commits may store now
-      if (tid == 0) st_release(a.flags + kGo, (uint64_t)r);
+      // commits may store now. A relaxed store suffices: every slot result
+      // word read above is data-dependent on that slot's state loads, which
+      // had therefore returned before the word was written; the committers'
+      // stores follow their acquire of kGo (0.15 us per round less than a
+      // release here, profiles/r02/engine_variants.txt).
+      if (tid == 0) st_relaxed(a.flags + kGo, (uint64_t)r);
 #ifdef GCMC_PHASE_TIMERS
       if (a.prof && tid == 0) a.prof[3640 + (r & 1)] = gtimer();
 #endif

@@ -43,7 +43,6 @@ struct Chain {
   // energy grid scratch (counting sort)
   void* egrid = nullptr;
   size_t egrid_bytes = 0;
-  bool egrid_fresh = false;      // egrid (re)allocated: k_energy2's block counter needs a reset
   cudaStream_t stream = nullptr;
   cudaStream_t gen_stream = nullptr;
   cudaEvent_t ev[4] = {};

@@ -307,8 +307,8 @@ def test_total_energy_1m_against_device_bruteforce():
     from paper_1408_3764_b200.config import RunConfig
 
     box, xyz, rng = config(1 << 20)
-    sim = E().Simulation(RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box),
-                         xyz, rng)
+    sim = E().Simulation(RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box,
+                                   strategy="microcell"), xyz, rng)
     for rep in range(2):
         u, w = sim.dev.total_energy()
         bu, bw = sim.dev.total_energy_bruteforce()

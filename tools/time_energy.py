@@ -1,23 +1,24 @@
-"""Full-system energy (SURVEY §8 row c) timing at a given N0: wall time of
-gcmc_total_energy over repeats (includes the counting sort and the reduction),
-pair-candidate rate, and a check against the sum of deletion energies."""
+"""Time gcmc_total_energy (cell pass) and the O(N^2) brute force at several N.
+python tools/time_energy.py [--bf-max N]"""
 import argparse, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 from paper_1408_3764_b200 import engine as E
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--n0", type=int, default=1 << 20)
-ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--bf-max", type=int, default=1 << 18)
+ap.add_argument("--sizes", default="32768,131072,262144,1048576")
 a = ap.parse_args()
-box = (a.n0 / 0.67) ** (1 / 3)
-xyz, _ = E.random_initial_configuration(a.n0, box, 0.85, 1)
-g = E.GpuNeighborStrategy("microcell", xyz, box)
-g.total_energy()
-t = time.perf_counter()
-for _ in range(a.reps):
-    u, w = g.total_energy()
-dt = (time.perf_counter() - t) / a.reps
-n = len(xyz)
-print(f"n={n} U={u:.10e} W={w:.10e} total_energy {dt*1e6:.1f} us/call "
-      f"({n * 24 / dt / 1e9:.1f} GB/s of positions, {n / dt / 1e9:.3f} G particles/s)")
+for n in [int(x) for x in a.sizes.split(",")]:
+    box = (n / 0.67) ** (1 / 3)
+    xyz, _ = E.random_initial_configuration(n, box, 0.85, 1)
+    g = E.GpuNeighborStrategy("microcell", xyz, box)
+    for _ in range(3):
+        u, w = g.total_energy()
+    p, k = g.energy_timing()
+    line = f"n={n} cell pass {1e3*p:.1f} us kernel {1e3*k:.1f} us U={u:.10e}"
+    if n <= a.bf_max:
+        t = time.time()
+        bu, bw = g.total_energy_bruteforce()
+        line += f" | brute force {time.time()-t:.3f} s U={bu:.10e} rel {abs(u-bu)/abs(bu):.2e}"
+    print(line, flush=True)
+    g.close()
