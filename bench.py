@@ -375,7 +375,7 @@ def make_chains(a, rank, local, E, RunConfig):
     sims = []
     for c in range(a.chains_per_gpu):
         mu, seed = state_point(a, rank, c)
-        xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed)
+        xyz, rng = E.random_initial_configuration(a.n0, box, 0.85, seed, device=local)
         cfg = RunConfig(temperature=a.temperature, chemical_potential=mu, box_length=box,
                         strategy=a.strategy, seed=seed)
         kw = {"engine_share": a.chains_per_gpu} if a.chains_per_gpu > 1 else {}

@@ -28,6 +28,7 @@
  *   gcmc_set/get_state              SystemState / RunStatistics / step_      engine.hpp:112-140, 244-252
  *   gcmc_run_moves                  Simulation::step() x n  (run_to loop)    engine.hpp:293-325
  *   gcmc_random_initial_configuration  random_initial_configuration()        init_config.hpp:19-64
+ *   gcmc_device_initial_configuration  (the same, on the device)              init_config.hpp:19-64
  *   gcmc_run_chains                 (no reference counterpart: K independent Simulations, e.g. the
  *                                   points of a mu/T sweep, advanced concurrently on one device;
  *                                   PAPER.md:632 future work)
@@ -188,6 +189,15 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace,
  * the message names the chain. */
 gcmc_status gcmc_run_chains(gcmc_dev* const* hs, int32_t k, const uint64_t* n,
                             gcmc_run_result* out);
+
+/* random_initial_configuration (init_config.hpp:19-64) on the device: the
+ * same MT19937-64 stream, bit-identical positions in the same order, the same
+ * RNG state afterwards and the same error after 10^6 consecutive rejections;
+ * candidates are tested in parallel blocks against the particles placed so
+ * far, and within a block in candidate order. */
+gcmc_status gcmc_device_initial_configuration(int device, uint64_t n, double box_length,
+                                              double min_sep, uint64_t seed, double* out_xyz,
+                                              uint64_t words[312], uint64_t* index, uint64_t* draws);
 
 /* Host-side initial configuration (init_config.hpp:19-64) consuming the
  * identical MT stream; returns the RNG state left for the MC stream. */

@@ -57,7 +57,7 @@ EXPORTS = [
     "gcmc_commit_delete", "gcmc_total_energy", "gcmc_energy_drift", "gcmc_seed_rng", "gcmc_set_rng_state",
     "gcmc_get_rng_state", "gcmc_set_state", "gcmc_get_state", "gcmc_run_moves",
     "gcmc_random_initial_configuration", "gcmc_run_chains", "gcmc_energy_timing",
-    "gcmc_total_energy_bruteforce",
+    "gcmc_total_energy_bruteforce", "gcmc_device_initial_configuration",
 ]
 
 _lib = None
@@ -114,6 +114,8 @@ def load(path: str = SO):
         "gcmc_run_chains": [P(_p), _i32, P(_u64), P(GcmcRunResult)],
         "gcmc_energy_timing": [_p, _dp, _dp],
         "gcmc_total_energy_bruteforce": [_p, _dp, _dp],
+        "gcmc_device_initial_configuration": [C.c_int, _u64, _d, _d, _u64, _dp, P(_u64), P(_u64),
+                                              P(_u64)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

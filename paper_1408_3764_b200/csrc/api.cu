@@ -1002,6 +1002,17 @@ gcmc_status gcmc_run_chains(gcmc_dev* const* hs, int32_t k, const uint64_t* n, g
   return GCMC_OK;
 }
 
+gcmc_status gcmc_device_initial_configuration(int device, uint64_t n, double box_length, double min_sep,
+                                              uint64_t seed, double* out_xyz, uint64_t words[312],
+                                              uint64_t* index, uint64_t* draws) {
+  if (n && !out_xyz) return set_error(GCMC_ARG, "null positions");
+  if (!words || !index) return set_error(GCMC_ARG, "null argument");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev), "device count");
+  if (device < 0 || device >= ndev) return set_error(GCMC_ARG, "invalid device ordinal");
+  return device_initial_configuration(device, n, box_length, min_sep, seed, out_xyz, words, index, draws);
+}
+
 gcmc_status gcmc_random_initial_configuration(uint64_t n, double l, double min_sep, uint64_t seed,
                                               double* out_xyz, uint64_t words[312],
                                               uint64_t* index, uint64_t* draws) {

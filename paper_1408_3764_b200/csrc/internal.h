@@ -103,6 +103,11 @@ gcmc_status epart_build(Chain& c, double2* out);
 gcmc_status epart_drift(Chain& c, double* du, double* dw);
 gcmc_status epart_dump(Chain& c, double* maint, double* fresh);
 
+// initcfg.cu: random_initial_configuration on the device (same stream and result)
+gcmc_status device_initial_configuration(int device, uint64_t n, double l, double min_sep, uint64_t seed,
+                                         double* out_xyz, uint64_t words[312], uint64_t* index,
+                                         uint64_t* draws);
+
 // Error text in the reference's wording.
 std::string overflow_message(const Chain& c, int64_t cell, int64_t occ);
 std::string strategy_name(int kind);

@@ -168,14 +168,21 @@ def tail_corrections(rho, epsilon, sigma, r_cut):
     return u, pr
 
 
-def random_initial_configuration(n: int, box_length: float, min_sep: float, seed: int):
-    """init_config.hpp:19-64 on the host (same MT draws). Returns
-    (positions (n,3), RngState left for the MC stream)."""
+def random_initial_configuration(n: int, box_length: float, min_sep: float, seed: int,
+                                 device: Optional[int] = 0):
+    """init_config.hpp:19-64 (same MT draws, bit-identical result) on the
+    given device (gcmc_device_initial_configuration), or on the host with
+    device=None. Returns (positions (n,3), RngState left for the MC stream)."""
     out = np.zeros((max(n, 1), 3))
     words = (C.c_uint64 * 312)()
     idx, draws = C.c_uint64(), C.c_uint64()
-    L.check(L.load().gcmc_random_initial_configuration(n, box_length, min_sep, seed, L.dptr(out),
-                                                       words, C.byref(idx), C.byref(draws)))
+    if device is None:
+        L.check(L.load().gcmc_random_initial_configuration(n, box_length, min_sep, seed, L.dptr(out),
+                                                           words, C.byref(idx), C.byref(draws)))
+    else:
+        L.check(L.load().gcmc_device_initial_configuration(device, n, box_length, min_sep, seed,
+                                                           L.dptr(out), words, C.byref(idx),
+                                                           C.byref(draws)))
     return out[:n].copy(), RngState(np.frombuffer(words, dtype=np.uint64).copy(), idx.value,
                                     draws.value)
 
@@ -415,7 +422,7 @@ class Simulation:
             if cfg.initial_particles > 0:
                 positions, rng = random_initial_configuration(cfg.initial_particles,
                                                               cfg.box_length, 0.85 * cfg.sigma,
-                                                              cfg.seed)
+                                                              cfg.seed, device=device)
             else:
                 positions, rng = np.zeros((0, 3)), RngState.from_seed(cfg.seed)
         if rng is None:

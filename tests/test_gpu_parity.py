@@ -546,3 +546,34 @@ def test_drop_in_strategy_against_reference(strategy, n0):
                        timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "fails=0" in r.stdout, r.stdout
+
+
+# --------------------------------------------------------------------- (f4) initial configuration
+@pytest.mark.parametrize("n,density,seed", [(2048, 0.67, 1), (32768, 0.67, 3), (262144, 0.67, 5),
+                                            (1 << 20, 0.67, 1), (300, 0.75, 9), (5, 0.6, 2),
+                                            (4000, 0.9, 11)])
+def test_device_initial_configuration_bitwise(n, density, seed):
+    """gcmc_device_initial_configuration == the host restatement (itself pinned
+    to the reference, test_host_cpu) bit for bit: positions in order, MT state,
+    position and draw count (init_config.hpp:19-64)."""
+    box = (n / density) ** (1.0 / 3.0)
+    hx, hr = E().random_initial_configuration(n, box, 0.85, seed, device=None)
+    dx, dr = E().random_initial_configuration(n, box, 0.85, seed, device=0)
+    assert np.array_equal(hx, dx)
+    assert hr.serialize_hex() == dr.serialize_hex()
+    if use_ref() and n <= 4096:
+        rx, rh = O.ref_initial_configuration(n, box, seed)
+        assert np.array_equal(dx, rx) and dr.serialize_hex() == rh
+
+
+def test_device_initial_configuration_rejection_limit():
+    """The reference's error after 10^6 consecutive rejections (a density the
+    separation cannot reach), with the same text."""
+    from paper_1408_3764_b200 import _lib
+
+    with pytest.raises(_lib.GcmcError) as e1:
+        E().random_initial_configuration(400, 5.0, 0.85, 1, device=0)
+    with pytest.raises(_lib.GcmcError) as e2:
+        E().random_initial_configuration(400, 5.0, 0.85, 1, device=None)
+    assert str(e1.value) == str(e2.value)
+    assert "consecutive rejections" in str(e1.value)

@@ -45,7 +45,7 @@ def test_random_initial_configuration_matches_reference():
 
     for n, seed in ((300, 3), (2048, 1)):
         box = (n / 0.67) ** (1 / 3)
-        xyz, rng = E.random_initial_configuration(n, box, 0.85, seed)
+        xyz, rng = E.random_initial_configuration(n, box, 0.85, seed, device=None)  # host form
         if O.ref_available():
             rx, rh = O.ref_initial_configuration(n, box, seed)
             assert np.array_equal(xyz, rx)
@@ -126,7 +126,7 @@ def test_checkpoint_text_roundtrip_and_reference_format():
 
     n = 64
     box = (n / 0.5) ** (1 / 3)
-    xyz, rng = E.random_initial_configuration(n, box, 0.85, 4)
+    xyz, rng = E.random_initial_configuration(n, box, 0.85, 4, device=None)
     cfg = CFG.RunConfig(temperature=2.0, chemical_potential=-2.0, box_length=box,
                         strategy="microcell", seed=4)
     c = CK.Checkpoint(cfg, 17, -12.5, 3.25, rng.serialize_hex(), xyz)
