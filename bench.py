@@ -415,14 +415,15 @@ def main():
         if K == 1:
             sim.run(a.moves_per_step)
             r = sim.last_run
-            return r.device_ms + r.gen_ms, r.device_ms, r.rounds
+            return r.device_ms + r.gen_ms, r.device_ms, r.rounds, r.pair_evals
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         res = E.run_chains(sims, a.moves_per_step)
         e1.record()
         e1.synchronize()
         ms = e0.elapsed_time(e1)
-        return ms, max(r.device_ms for r in res), sum(r.rounds for r in res)
+        return (ms, max(r.device_ms for r in res), sum(r.rounds for r in res),
+                sum(r.pair_evals for r in res))
 
     for _ in range(a.warmup):
         step()
@@ -446,14 +447,15 @@ def main():
     # ---- device-resident timing (value)
     barrier()
     dev_ms = eng_ms = 0.0
-    rounds = 0
+    rounds = pairs = 0
     acc0 = accepted()
     with ClockSampler(local) as clk:
         for k in range(a.steps):
-            d, e, r = step()
+            d, e, r, pe = step()
             dev_ms += d
             eng_ms += e
             rounds += r
+            pairs += pe
             if want_cpu and k + 1 == a.cpu_steps:
                 s1 = snapshot(sim)  # host read-back between steps: not in the device timing
     barrier()
@@ -521,6 +523,12 @@ def main():
             # per step, chain and 2^21-move chunk (gcmc_run_moves): the engine
             # plus the look-ahead proposal generation (k_gen2, k_annotate)
             "gpu_launches": 3 * a.steps * K * launches,
+            "pair_evals_per_s": pairs * world / t_dev,
+            "pair_evals_per_move": pairs / moves_rank,
+            "pair_evals_note": "counted on the device (gcmc_run_result.pair_evals): FP64 "
+                               "minimum-image + cutoff evaluations in move windows and "
+                               "neighbour-energy updates; the engine scans one window per "
+                               "move (maintained per-particle energies)",
             "ns_per_move": 1e9 * t_dev / moves_rank,
             "ns_per_round": ns_round,
             "moves_per_round": a.moves_per_step * a.steps * K / max(rounds, 1),

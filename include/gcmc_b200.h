@@ -109,6 +109,8 @@ typedef struct gcmc_run_result {
   uint64_t rounds;    /* speculative evaluation rounds the device used */
   double device_ms;   /* device time of the move loop (CUDA events) */
   double gen_ms;      /* device time of proposal generation */
+  uint64_t pair_evals; /* FP64 pair evaluations (minimum image + cutoff test) the device
+                          performed for this call: windows, energy updates, all-pairs scans */
 } gcmc_run_result;
 
 typedef struct gcmc_dev gcmc_dev;

@@ -876,6 +876,11 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
   }
   float gen_ms = 0.f, eng_ms = 0.f;
   uint64_t done = 0, rounds = 0;
+  if (out) {  // the device counter before the call
+    gcmc_status ps = pull_state(c);
+    if (ps) return ps;
+  }
+  const unsigned long long pairs0 = c.st_host->pair_evals;
   gcmc_status s = GCMC_OK;
   while (done < n) {
     const uint64_t m = std::min(chunk_cap, n - done);
@@ -968,6 +973,7 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     out->rounds = rounds;
     out->device_ms = eng_ms;
     out->gen_ms = gen_ms;
+    out->pair_evals = c.st_host->pair_evals - pairs0;
   }
   return GCMC_OK;
 }

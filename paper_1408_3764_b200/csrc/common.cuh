@@ -74,7 +74,8 @@ struct ChainState {
   int64_t err_a, err_b, err_c;  // failure detail (cell, occupancy, particle)
   uint64_t moves_done;      // moves completed by the last engine call
   uint64_t rounds;          // speculative rounds of the last engine call
-  uint64_t pad[11];
+  unsigned long long pair_evals;  // FP64 pair evaluations the engines performed (cumulative)
+  uint64_t pad[10];
 };
 static_assert(sizeof(ChainState) == 256, "ChainState layout");
 

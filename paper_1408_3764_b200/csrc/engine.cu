@@ -619,6 +619,9 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
           allpairs_sums<T>(a.b, a.s.pos, d.n, ws, G.kind == 1 ? -1 : (long long)G.pid, gt, du, dw);
         else
           win_sums<T>(a.m, a.b, ws, gt, du, dw);
+        if (gt == 0)
+          atomicAdd(&a.st->pair_evals,
+                    (unsigned long long)(all_pairs ? d.n * (uint64_t)ws.nwin : (uint64_t)ws.total));
       }
       group_reduce<T>(ws, du, dw, bar_id, gt, 32 * lw);
       pc.mark(4);  // sums + reduce

@@ -634,6 +634,7 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
   group_sync(bar_id, T);
   ec.mark(1);
   const int total = ws.total;
+  if (gt == 0) atomicAdd(&a.st->pair_evals, (unsigned long long)total);
   const double c0x = G.nx, c0y = G.ny, c0z = G.nz, c1x = G.ox, c1y = G.oy, c1z = G.oz;
   const double s0 = (double)G.sgn0, s1 = (double)G.sgn1;
   const bool has_old = G.kind != 1;
@@ -1033,6 +1034,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       // ---- S(n): the whole group
       double su = 0.0, sw = 0.0;
       if (kind != 2) win_sums<T>(a.m, a.b, ws, gt, su, sw);
+      if (gt == 0 && kind != 2) atomicAdd(&a.st->pair_evals, (unsigned long long)ws.total);
       group_reduce<T>(ws, su, sw, bar_id, gt, 32 * lw);
       pc.mark(3);
       if (gw == lw) {
@@ -1200,11 +1202,15 @@ struct SeqShared {
   alignas(16) uint32_t mcf[kMaxMoves];
   alignas(16) uint32_t movf[kMaxMoves];
   alignas(16) uint8_t mkind[kMaxMoves];
-  int len, nacc, err, cmin, why, dend, arrived;
+  int len, nacc, err, cmin, why, dend, arrived, plen;
   unsigned long long vmax, vsum;  // diagnostics
   unsigned viters, vcalls;
   int wscr_i[kMaxAcc], wscr_d[kMaxAcc];  // walk dry runs (discarded)
   int8_t wscr_k[kMaxMoves];
+  // the previous round's masks, the dry walk's input (the live masks are
+  // being written by the poll while it runs)
+  uint32_t pacc[kMaxMoves], pcf[kMaxMoves], povf[kMaxMoves];
+  uint8_t pkind[kMaxMoves];
   int acc_i[kMaxAcc], acc_d[kMaxAcc];
   int res_d[kMaxMoves];
   // read / write sets of the consumed moves (verify)
@@ -1551,6 +1557,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
   constexpr int kPollThreads = kPollWarps * 32;
   if (tid == 0) {
     sh.ks = *a.st;
+    sh.plen = 0;
     sh.done.len = 0;
     sh.done.nacc = 0;
     sh.arrived = 0;
@@ -1589,7 +1596,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // discarded) so that the walk's code is in the instruction cache when
       // the last slot lands.
       if (warp == 0) {  // one dry run (the walk's code into the instruction cache), then wait
-        walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+        walk_warp(sh.pacc, sh.pcf, sh.povf, sh.pkind, sh.plen, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
         while (*(volatile int*)&sh.arrived < fit) __nanosleep(32);
       }
       for (int sl = tid - 32; sl >= 0 && sl < fit; sl += kPollThreads - 32) {
@@ -1859,6 +1866,13 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
         D.res_d[i] = sh.res_d[i];
         D.kind[i] = sh.mkind[i];
       }
+      if (i < fit) {  // the next round's dry walk input
+        sh.pacc[i] = sh.macc[i];
+        sh.pcf[i] = sh.mcf[i];
+        sh.povf[i] = sh.movf[i];
+        sh.pkind[i] = sh.mkind[i];
+      }
+      if (i == 0) sh.plen = fit;
       if (i < nacc) {
         const int m = sh.acc_i[i];
         const Proposal& pr = sh.ring[(base + m) % kRing];

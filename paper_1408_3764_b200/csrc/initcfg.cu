@@ -196,13 +196,40 @@ struct IcState {  // device-resident progress of the placement
   int error, pad;
 };
 
-// 4. candidates in order. The block's flags and list lengths are staged in
-// shared memory by all threads; one thread decides (a survivor is placed
-// unless an earlier survivor it lists was placed; lists that overflowed, or
-// all of them when the block's survivor grid overflowed, are replaced by a
-// scan of the earlier placed survivors); then the ids by a block scan.
+// 4. candidates in order, decided in parallel where the order cannot matter:
+// a blocked candidate is rejected, a survivor without an earlier survivor
+// within min_sep is placed; only the survivors that have one (rare: blocks
+// are sized to the box) are decided one by one, in order, from their lists
+// (or by a scan of the block's earlier placed candidates when a list or the
+// block's survivor grid overflowed). Then block scans give the ids, the stop
+// at the n-th placement, and the consecutive-rejection limit (only the run
+// before the block's first placement can reach it: later gaps are shorter
+// than a block).
 constexpr int kResolveThreads = 1024;
 constexpr int kMaxBlock = 32768;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < kResolveThreads / 32 ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    if (lane < kResolveThreads / 32) wsum[lane] = w;
+  }
+  __syncthreads();
+  total = wsum[kResolveThreads / 32 - 1];
+  return incl - v + (warp ? wsum[warp - 1] : 0);
+}
 
 __global__ void __launch_bounds__(kResolveThreads)
     k_ic_resolve(IcGrid g, const double* __restrict__ uni, uint64_t ubase, int nc, uint64_t n,
@@ -210,88 +237,98 @@ __global__ void __launch_bounds__(kResolveThreads)
                  const int* __restrict__ ncount, const int* __restrict__ nlist,
                  const int* __restrict__ local_full, int* placed_id, IcState* st) {
   extern __shared__ uint8_t sm[];
-  uint8_t* bl = sm;              // [kMaxBlock] blocked
-  uint8_t* cnt8 = sm + kMaxBlock;  // [kMaxBlock] list length (255: scan)
-  uint8_t* acc = sm + 2 * kMaxBlock;  // [kMaxBlock] placed
-  __shared__ unsigned long long s_placed0, s_qend;
+  uint8_t* cnt8 = sm;                                        // [kMaxBlock] 0 blocked / no list, 1..8, 255 scan
+  uint8_t* acc = sm + kMaxBlock;                             // [kMaxBlock] placed
+  uint16_t* dl = reinterpret_cast<uint16_t*>(sm + 2 * kMaxBlock);  // [kMaxBlock] dependent survivors
   __shared__ int wsum[kResolveThreads / 32];
+  __shared__ int s_first, s_cut;
   const bool scan_all = *local_full != 0;
-  for (int q = threadIdx.x; q < nc; q += kResolveThreads) {
-    bl[q] = blocked[q];
-    const int c = bl[q] ? 0 : ncount[q];
-    cnt8[q] = (uint8_t)(scan_all ? 255 : (c > 255 ? 255 : c));
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long placed = st->placed, run = st->run;
-    s_placed0 = placed;
-    int q = 0;
-    for (; q < nc && placed < n; ++q) {
-      bool ok = !bl[q];
-      if (ok) {
-        const int m = cnt8[q];
-        if (m == 255) {  // scan the block's earlier placed candidates
-          double x, y, z;
-          ic_cand(g, uni, ubase + 3ull * q, x, y, z);
-          for (int p = 0; p < q && ok; ++p) {
-            if (!acc[p]) continue;
-            double px, py, pz;
-            ic_cand(g, uni, ubase + 3ull * p, px, py, pz);
-            if (ic_dist2(g, x, y, z, px, py, pz) < g.min_sep2) ok = false;
-          }
-        } else {
-          for (int k = 0; k < m; ++k)
-            if (acc[nlist[(size_t)q * kNbr + k]]) {
-              ok = false;
-              break;
-            }
-        }
-      }
-      acc[q] = ok ? 1 : 0;
-      if (!ok) {
-        if (++run >= max_rej) {
-          st->error = 1;
-          ++q;
-          break;
-        }
-        continue;
-      }
-      run = 0;
-      ++placed;
-    }
-    for (int r = q; r < nc; ++r) acc[r] = 0;  // not consumed
-    st->placed = placed;
-    st->run = run;
-    st->consumed += (unsigned long long)q;
-    s_qend = (unsigned long long)q;
-  }
-  __syncthreads();
-  // ids: placed0 + rank among the placed candidates (block-wide scan)
   const int per = (nc + kResolveThreads - 1) / kResolveThreads;
   const int lo = threadIdx.x * per, hi = min(nc, lo + per);
+  int ndep = 0;
+  for (int q = lo; q < hi; ++q) {
+    const bool surv = !blocked[q];
+    const int c = surv ? ncount[q] : 0;
+    const uint8_t m = !surv ? 0 : (scan_all ? 255 : (uint8_t)(c > 255 ? 255 : c));
+    cnt8[q] = m;
+    acc[q] = surv && m == 0 ? 1 : 0;
+    ndep += surv && m != 0 ? 1 : 0;
+  }
+  int total_dep;
+  int pos = block_excl_scan(ndep, wsum, total_dep);
+  for (int q = lo; q < hi; ++q)
+    if (!blocked[q] && cnt8[q] != 0) dl[pos++] = (uint16_t)q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < total_dep; ++t) {
+      const int q = dl[t];
+      const int m = cnt8[q];
+      bool ok = true;
+      if (m == 255) {
+        double x, y, z;
+        ic_cand(g, uni, ubase + 3ull * q, x, y, z);
+        for (int p = 0; p < q && ok; ++p) {
+          if (!acc[p]) continue;
+          double px, py, pz;
+          ic_cand(g, uni, ubase + 3ull * p, px, py, pz);
+          if (ic_dist2(g, x, y, z, px, py, pz) < g.min_sep2) ok = false;
+        }
+      } else {
+        for (int k = 0; k < m && ok; ++k)
+          if (acc[nlist[(size_t)q * kNbr + k]]) ok = false;
+      }
+      acc[q] = ok ? 1 : 0;
+    }
+    s_first = nc;
+    s_cut = nc;
+  }
+  __syncthreads();
+  // ranks of the placed candidates; the first placement; the n-th placement
   int local = 0;
   for (int q = lo; q < hi; ++q) local += acc[q];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = local;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int v = lane < kResolveThreads / 32 ? wsum[lane] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += t;
-    }
-    if (lane < kResolveThreads / 32) wsum[lane] = v;  // inclusive over warps
+  int total_acc;
+  int rank = block_excl_scan(local, wsum, total_acc);
+  const unsigned long long placed0 = st->placed, run0 = st->run;
+  const long long need = (long long)n - (long long)placed0;  // >= 1
+  {
+    int r = rank;
+    for (int q = lo; q < hi; ++q)
+      if (acc[q]) {
+        if (r == 0) s_first = q;  // one thread holds rank 0
+        if (r == need - 1) s_cut = q + 1;
+        ++r;
+      }
   }
   __syncthreads();
-  int rank = incl - local + (warp ? wsum[warp - 1] : 0);
+  int consumed = s_cut;
+  bool error = false;
+  // the run before the first placement (with the carried one) is the only
+  // one that can reach max_rej inside a block
+  if (run0 + (unsigned long long)min(s_first, consumed) >= max_rej) {
+    consumed = (int)(max_rej - run0);  // the failing candidate included
+    error = true;
+  }
   for (int q = lo; q < hi; ++q) {
-    placed_id[q] = acc[q] ? (int)(s_placed0 + rank) : -1;
+    const bool placed = acc[q] && q < consumed && !error;
+    placed_id[q] = placed ? (int)(placed0 + rank) : -1;
     rank += acc[q];
+  }
+  if (threadIdx.x == 0) {
+    if (error) {
+      st->error = 1;
+      st->run = max_rej;
+    } else {
+      const long long nplaced = need <= (long long)total_acc ? need : (long long)total_acc;
+      st->placed = placed0 + (unsigned long long)nplaced;
+      // rejections since the last placement within the consumed candidates
+      if (nplaced == 0) st->run = run0 + (unsigned long long)consumed;
+      else {
+        int last = consumed - 1;
+        while (last >= 0 && !acc[last]) --last;
+        st->run = (unsigned long long)(consumed - 1 - last);
+      }
+    }
+    st->consumed += (unsigned long long)consumed;
   }
 }
 
@@ -373,7 +410,7 @@ gcmc_status device_initial_configuration(int device, uint64_t n, double l, doubl
   int *cnt = (int*)bcnt.p, *slots = (int*)bslots.p, *lcnt = (int*)blcnt.p, *lslots = (int*)blslots.p;
   int *ncount = (int*)bnc.p, *nlist = (int*)bnl.p, *pid = (int*)bpid.p, *ovf = (int*)bov.p;
   int* lfull = (int*)blf.p;
-  const size_t rsmem = 3 * (size_t)kMaxBlock;
+  const size_t rsmem = 4 * (size_t)kMaxBlock;
   if ((e = cudaFuncSetAttribute(k_ic_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem)))
     return cuda_error(e, "initial configuration");
   uint8_t* blocked = (uint8_t*)bblk.p;

@@ -320,3 +320,25 @@ def test_build_on_a_live_strategy_keeps_stale_slots_like_the_reference(strategy)
     O.ref_lib().ref_strat_build(o.h)
     a, b = g.grid(), o.grid()
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_pair_evaluations_are_counted():
+    """gcmc_run_result.pair_evals: the device's own count of FP64 pair
+    evaluations — about one window of candidates per non-deletion move at
+    rho ~ 0.67 (bricks >= r_c, pruned 27-brick window) plus the neighbour
+    updates of accepted moves; all-pairs scans N per window."""
+    from paper_1408_3764_b200.config import RunConfig
+
+    box, xyz, rng = config(32768)
+    sim = E().Simulation(RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box,
+                                   strategy="microcell"), xyz, rng)
+    sim.run(20000)
+    r = sim.last_run
+    per_move = r.pair_evals / r.moves
+    assert 50 < per_move < 1000, per_move
+    sim.close()
+    sim = E().Simulation(RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box,
+                                   strategy="all_pairs"), xyz, rng)
+    sim.run(2000)
+    assert sim.last_run.pair_evals >= 2000 * 0.6 * len(xyz) * 0.9
+    sim.close()
