@@ -276,54 +276,75 @@ def snapshot(sim):
             "attempted": list(st.attempted), "accepted": list(st.accepted)}
 
 
-def cpu_baseline(s0, s1, a, box, mu):
-    """The reference's own Simulation::step loop (oracle/_ref, g++ -O3 with the
-    reference's Release flags, 1 core) resumed (engine.hpp:244-252) from the
-    GPU chain's state s0 at the start of the timed steps and timed on exactly
-    the moves of the first --cpu-steps timed GPU steps. The run doubles as a
-    parity check against the GPU chain's state s1 after those steps:
-    positions and RNG state bitwise, step / N / per-kind attempted and
-    accepted counts exact, U and W within 1e-10 relative."""
+def cpu_chain(s0, s1, a, box, mu):
+    """One chain of the CPU baseline: the reference's own Simulation::step
+    loop (oracle/_ref, g++ -O3 with the reference's Release flags) resumed
+    (engine.hpp:244-252) from the GPU chain's state s0 at the start of the
+    timed steps and run on exactly the moves of the first --cpu-steps timed
+    GPU steps. The run doubles as a parity check against the GPU chain's
+    state s1 after those steps: positions and RNG state bitwise, step / N /
+    per-kind attempted and accepted counts exact, U and W within 1e-10
+    relative. Returns (seconds, checks or None, kind)."""
     import numpy as np
 
     import oracle as O
 
     timed = a.cpu_steps * a.moves_per_step
-    model, ncpu = host_cpu()
-    same = None
-    if os.path.exists(O.REF_SO):
-        kind = "reference"
-        cfg = O.ref_config(temperature=a.temperature, chemical_potential=mu, box_length=box,
-                           strategy=a.strategy)
-        sim = O.RefSim(cfg, mode=2, xyz=s0["xyz"], rng_hex=s0["rng"], step=s0["step"],
-                       energy=s0["u"], virial=s0["w"])
-        secs, _ = sim.run(timed)
-        if s1 is not None:
-            st = sim.state()
-            tol = lambda x, y: abs(x - y) <= 1e-10 * max(1.0, abs(y))  # noqa: E731
-            checks = {
-                "positions_bitwise": bool(np.array_equal(sim.positions(), s1["xyz"])),
-                "rng_bitwise": sim.rng_hex() == s1["rng"],
-                "step_n": st.step == s1["step"] and st.n == s1["n"],
-                "counts": all(st.attempted[k] == s1["attempted"][k] - s0["attempted"][k] and
-                              st.accepted[k] == s1["accepted"][k] - s0["accepted"][k]
-                              for k in range(3)),
-                "energy_1e-10": tol(s1["u"], st.energy) and tol(s1["w"], st.virial),
-            }
-            same = {"all": all(checks.values()), **checks}
-    else:
-        kind = "port"
+    if not os.path.exists(O.REF_SO):
         p = O.port_params(temperature=a.temperature, chemical_potential=mu, box_length=box,
                           strategy=a.strategy)
         sim = O.PortSim(p, s0["xyz"], O.rng_from_hex(s0["rng"]), energy=s0["u"], virial=s0["w"])
         t0 = time.perf_counter()
         sim.run(timed)
-        secs = time.perf_counter() - t0
-    return ({"value": timed / secs, "unit": "moves/s", "cores": 1, "kind": kind,
-             "sample": f"moves {s0['step']}..{s0['step'] + timed} of the same chain (the first "
-                       f"{a.cpu_steps} of the {a.steps} timed GPU steps), reference "
-                       f"Simulation::step loop resumed from the GPU chain's state there, "
-                       f"{secs:.2f} s, 1 thread on host '{model}' ({ncpu} logical cores)"}, same)
+        return time.perf_counter() - t0, None, "port"
+    cfg = O.ref_config(temperature=a.temperature, chemical_potential=mu, box_length=box,
+                       strategy=a.strategy)
+    sim = O.RefSim(cfg, mode=2, xyz=s0["xyz"], rng_hex=s0["rng"], step=s0["step"],
+                   energy=s0["u"], virial=s0["w"])
+    secs, _ = sim.run(timed)
+    same = None
+    if s1 is not None:
+        st = sim.state()
+        tol = lambda x, y: abs(x - y) <= 1e-10 * max(1.0, abs(y))  # noqa: E731
+        checks = {
+            "positions_bitwise": bool(np.array_equal(sim.positions(), s1["xyz"])),
+            "rng_bitwise": sim.rng_hex() == s1["rng"],
+            "step_n": st.step == s1["step"] and st.n == s1["n"],
+            "counts": all(st.attempted[k] == s1["attempted"][k] - s0["attempted"][k] and
+                          st.accepted[k] == s1["accepted"][k] - s0["accepted"][k]
+                          for k in range(3)),
+            "energy_1e-10": tol(s1["u"], st.energy) and tol(s1["w"], st.virial),
+        }
+        same = {"all": all(checks.values()), **checks}
+    return secs, same, "reference"
+
+
+def cpu_baseline(s0s, s1s, a, box, mus):
+    """The CPU baseline on this host: one reference chain per GPU chain of
+    rank 0 (sweep chains run one per core, concurrently), each
+    on its own chain's moves; value = all chains' moves / wall time."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    timed = a.cpu_steps * a.moves_per_step
+    model, ncpu = host_cpu()
+    k = len(s0s)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(k, ncpu or 1)) as ex:  # ctypes calls drop the GIL
+        res = list(ex.map(lambda c: cpu_chain(s0s[c], s1s[c], a, box, mus[c]), range(k)))
+    wall = time.perf_counter() - t0
+    kind = res[0][2]
+    same = None
+    if all(r[1] is not None for r in res):
+        same = dict(res[0][1]) if k == 1 else {"all": all(r[1]["all"] for r in res),
+                                               "chains": [r[1] for r in res]}
+    s0 = s0s[0]
+    return ({"value": k * timed / wall, "unit": "moves/s", "cores": min(k, ncpu or 1),
+             "kind": kind,
+             "sample": f"moves {s0['step']}..{s0['step'] + timed} of each of the {k} chain(s) (the "
+                       f"first {a.cpu_steps} of the {a.steps} timed GPU steps), reference "
+                       f"Simulation::step loop resumed from each GPU chain's state there, "
+                       f"{wall:.2f} s wall, {min(k, ncpu or 1)} thread(s) on host '{model}' "
+                       f"({ncpu} logical cores)"}, same)
 
 
 def run_reference(a, rank, world):
@@ -433,7 +454,7 @@ def main():
     if not a.cpu_steps or a.cpu_steps > a.steps:
         a.cpu_steps = a.steps
     want_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
-    s0 = snapshot(sim) if want_cpu else None
+    s0 = [snapshot(s_) for s_ in sims] if want_cpu else None
     s1 = None
 
     def barrier():
@@ -457,7 +478,7 @@ def main():
             rounds += r
             pairs += pe
             if want_cpu and k + 1 == a.cpu_steps:
-                s1 = snapshot(sim)  # host read-back between steps: not in the device timing
+                s1 = [snapshot(s_) for s_ in sims]  # host read-back: not in the device timing
     barrier()
     acc1 = accepted()
     # ---- end-to-end through the C ABI (run + checkpoint read-back of state,
@@ -479,7 +500,7 @@ def main():
     cpu, same = None, None
     if want_cpu:
         try:
-            cpu, same = cpu_baseline(s0, s1, a, box, sim.cfg.chemical_potential)
+            cpu, same = cpu_baseline(s0, s1, a, box, [s_.cfg.chemical_potential for s_ in sims])
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "moves/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}

@@ -324,9 +324,8 @@ def test_build_on_a_live_strategy_keeps_stale_slots_like_the_reference(strategy)
 
 def test_pair_evaluations_are_counted():
     """gcmc_run_result.pair_evals: the device's own count of FP64 pair
-    evaluations — about one window of candidates per non-deletion move at
-    rho ~ 0.67 (bricks >= r_c, pruned 27-brick window) plus the neighbour
-    updates of accepted moves; all-pairs scans N per window."""
+    evaluations: one pruned brick window per evaluated non-deletion slot plus
+    the neighbour updates of accepted moves; all-pairs scans N per window."""
     from paper_1408_3764_b200.config import RunConfig
 
     box, xyz, rng = config(32768)
@@ -334,8 +333,11 @@ def test_pair_evaluations_are_counted():
                                    strategy="microcell"), xyz, rng)
     sim.run(20000)
     r = sim.last_run
+    # every evaluated slot counts, consumed or discarded by its round (from
+    # the random start most rounds end early: ~1.1e3 per consumed move; in the
+    # bench regime ~140)
     per_move = r.pair_evals / r.moves
-    assert 50 < per_move < 1000, per_move
+    assert 50 < per_move < 5000, per_move
     sim.close()
     sim = E().Simulation(RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box,
                                    strategy="all_pairs"), xyz, rng)
