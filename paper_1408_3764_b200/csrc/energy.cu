@@ -13,6 +13,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <sstream>
 
 #include "internal.h"
@@ -83,6 +84,7 @@ struct Prefilter {
 // minimum image and LJ pair (common.cuh), Kahan per lane and a compensated
 // warp tree. Overlap (r^2 < 1e-12 sigma^2) is reported like total_energy's
 // runtime_error (engine.hpp:74-94).
+template <bool kShift>
 __global__ void __launch_bounds__(kEWarps * 32)
     k_energy(EGrid eg, Box b, Prefilter pf, const int* __restrict__ start,
              const int* __restrict__ count, const double4* __restrict__ rec,
@@ -99,12 +101,19 @@ __global__ void __launch_bounds__(kEWarps * 32)
   const int cx = (int)(c % d), cy = (int)((c / d) % d), cz = (int)(c / ((uint64_t)d * d));
   // half shell: offsets 0..13 of the 27-cube in x-fastest order starting at
   // (0,0,0): {self} + the 13 cells after it in lexicographic (z, y, x) order
-  int ncnt = 0, nstart = 0;
+  // kShift: each neighbour's periodic image shift (-L, 0, +L per axis, the
+  // image adjacent to this cell) rides in the low 6 bits of its candidate
+  // entries, so the FP32 prefilter needs no minimum-image rounding (valid
+  // for cells >= r_cut: a pair within r_cut has no other close image)
+  int ncnt = 0, nstart = 0, scode = 21;  // 21: no shift on any axis
   if (lane < 14) {
     const int t = 13 + lane;  // cube index: (ox, oy, oz) = (t % 3, t / 3 % 3, t / 9) - 1
     const int ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
-    const int nx = (cx + ox + d) % d, ny = (cy + oy + d) % d, nz = (cz + oz + d) % d;
+    const int rx = cx + ox, ry = cy + oy, rz = cz + oz;
+    const int nx = (rx + d) % d, ny = (ry + d) % d, nz = (rz + d) % d;
     const int nc = nx + d * (ny + d * nz);
+    scode = (rx < 0 ? 0 : (rx >= d ? 2 : 1)) | (ry < 0 ? 0 : (ry >= d ? 2 : 1)) << 2 |
+            (rz < 0 ? 0 : (rz >= d ? 2 : 1)) << 4;
     ncnt = count[nc];
     nstart = start[nc];
   }
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(kEWarps * 32)
         const int e0 = incl - ncnt;
         for (int k = 0; k < ncnt; ++k) {
           const int f = e0 + k - cb;
-          if (f >= 0 && f < kECand) cand_s[warp][f] = nstart + k;
+          if (f >= 0 && f < kECand) cand_s[warp][f] = kShift ? ((nstart + k) << 6) | scode : nstart + k;
         }
       }
       __syncwarp();
@@ -166,18 +175,33 @@ __global__ void __launch_bounds__(kEWarps * 32)
       for (int t0 = 0; t0 < ctot; t0 += 32) {
         const int t = t0 + lane;
         const bool have = t < ctot;
-        const int qi = have ? cand_s[warp][t] : 0;
-        const float4 qf = have ? recf[qi] : make_float4(0, 0, 0, 0);
-        const bool self = have && cb + t < own_n;
+        const int ce = have ? cand_s[warp][t] : 0;
+        const int qi = kShift ? ce >> 6 : ce;
+        float4 qf = have ? recf[qi] : make_float4(0, 0, 0, 0);
+        if (kShift) {
+          qf.x += (float)((ce & 3) - 1) * pf.l;
+          qf.y += (float)(((ce >> 2) & 3) - 1) * pf.l;
+          qf.z += (float)(((ce >> 4) & 3) - 1) * pf.l;
+        }
+        // own i < lim passes the i < j rule (self cell) / all own i (others)
+        const int lim = !have ? 0 : (cb + t < own_n ? cb + t - ob : on);
+        const float cut2 = pf.on ? pf.cut2 : __int_as_float(0x7f800000);
         for (int i = 0; i < on; ++i) {
-          bool pass = have && !(self && ob + i >= cb + t);  // i < j within the cell
-          if (pass && pf.on) {
+          bool pass;
+          if (kShift) {
             const float4 pff = ownf_s[warp][i];
-            float dx = pff.x - qf.x, dy = pff.y - qf.y, dz = pff.z - qf.z;
-            dx -= pf.l * rintf(dx * pf.inv_l);
-            dy -= pf.l * rintf(dy * pf.inv_l);
-            dz -= pf.l * rintf(dz * pf.inv_l);
-            pass = dx * dx + dy * dy + dz * dz <= pf.cut2;
+            const float dx = pff.x - qf.x, dy = pff.y - qf.y, dz = pff.z - qf.z;
+            pass = i < lim && __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))) <= cut2;
+          } else {
+            pass = i < lim;
+            if (pass && pf.on) {
+              const float4 pff = ownf_s[warp][i];
+              float dx = pff.x - qf.x, dy = pff.y - qf.y, dz = pff.z - qf.z;
+              dx -= pf.l * rintf(dx * pf.inv_l);
+              dy -= pf.l * rintf(dy * pf.inv_l);
+              dz -= pf.l * rintf(dz * pf.inv_l);
+              pass = dx * dx + dy * dy + dz * dz <= pf.cut2;
+            }
           }
           const unsigned m = __ballot_sync(0xffffffffu, pass);
           if (m) {
@@ -209,10 +233,18 @@ __global__ void __launch_bounds__(kEWarps * 32)
 }
 
 // Deterministic final reduction over the per-cell partials.
-__global__ void k_ereduce(uint64_t ncells, const double* pu, const double* pw, double* out) {
-  __shared__ double su[32], sw[32], cu[32], cw[32];
+// Deterministic reduction of n partials (u, w): block b sums its contiguous
+// chunk (Kahan per thread + compensated trees) into ou[b], ow[b]. Used twice:
+// 1024-value chunks over the per-cell partials, then one block over those.
+constexpr int kRedChunk = 4096;
+
+__global__ void __launch_bounds__(1024) k_ereduce(uint64_t n, const double* pu, const double* pw,
+                                                  double* ou, double* ow) {
+  __shared__ double su[32], sw[32];
   Kahan ku = {0, 0}, kw = {0, 0};
-  for (uint64_t i = threadIdx.x; i < ncells; i += blockDim.x) {
+  const uint64_t lo = (uint64_t)blockIdx.x * kRedChunk;
+  const uint64_t hi = lo + kRedChunk < n ? lo + kRedChunk : n;
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     ku.add(pu[i]);
     kw.add(pw[i]);
   }
@@ -228,11 +260,9 @@ __global__ void k_ereduce(uint64_t ncells, const double* pu, const double* pw, d
     Kahan k2 = {lane < (int)(blockDim.x / 32) ? sw[lane] : 0.0, 0.0};
     const double tu = warp_sum_comp(k1), tw = warp_sum_comp(k2);
     if (lane == 0) {
-      out[0] = tu;
-      out[1] = tw;
+      ou[blockIdx.x] = tu;
+      ow[blockIdx.x] = tw;
     }
-    (void)cu;
-    (void)cw;
   }
 }
 
@@ -353,7 +383,7 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, (int)nc);
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t need = al(n * 4) * 2 + al(nc * 4) * 3 + al(n * 32) + al(n * 16) + al(nc * 8) * 2 +
-                      al(64) + al(scan_bytes);
+                      al(64 + 16 * ((nc + kRedChunk - 1) / kRedChunk)) + al(scan_bytes);
   cudaError_t e;
   if (need > c.egrid_bytes) {
     if (c.egrid) cudaFree(c.egrid);
@@ -376,7 +406,8 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   float4* recf = (float4*)take(n * 16);
   double* pu = (double*)take(nc * 8);
   double* pw = (double*)take(nc * 8);
-  char* small = take(64);
+  const size_t nred = (nc + kRedChunk - 1) / kRedChunk;
+  char* small = take(64 + 16 * nred);  // overlap word, result, first-level partials
   void* scan_tmp = take(scan_bytes);
   unsigned long long* overlap = (unsigned long long*)small;
   double* out = (double*)(small + 16);
@@ -404,10 +435,21 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
     pf.on = l > 2.0 * rc + 0.5 ? 1 : 0;
   }
   cudaEventRecord(c.ev_e[1], s);
-  k_energy<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
-                                                         pu, pw, overlap);
+  // the image-shift prefilter needs cells >= r_cut (t >= 3 forced otherwise)
+  static const bool rint_form = std::getenv("GCMC_ENERGY_RINT") != nullptr;  // A/B
+  if (l / t >= rc && !rint_form)
+    k_energy<true><<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
+                                                               pu, pw, overlap);
+  else
+    k_energy<false><<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec,
+                                                                recf, pu, pw, overlap);
   cudaEventRecord(c.ev_e[2], s);
-  k_ereduce<<<1, 1024, 0, s>>>(nc, pu, pw, out);
+  {  // two deterministic levels: chunks of the per-cell partials, then the chunks
+    const unsigned nb = (unsigned)((nc + kRedChunk - 1) / kRedChunk);
+    double* r2 = out + 2;  // [2 * nb] after the result (small scratch)
+    k_ereduce<<<nb, 1024, 0, s>>>(nc, pu, pw, r2, r2 + nb);
+    k_ereduce<<<1, 1024, 0, s>>>(nb, r2, r2 + nb, out, out + 1);
+  }
   cudaEventRecord(c.ev_e[3], s);
   double h[2];
   unsigned long long ov = 0;

@@ -175,9 +175,10 @@ __device__ __forceinline__ void ring_fill(const EngineArgs& a, Proposal* ring, u
 __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d, int lane, bool need_s) {
   constexpr int PER = (kDecWords + 31) / 32;  // 5
   uint64_t w[PER];
+  const uint64_t* dec = a.dec;
   for (;;) {
-    w[0] = ld_relaxed(a.dec + lane);
-    w[1] = ld_relaxed(a.dec + 32 + lane);
+    w[0] = ld_relaxed(dec + lane);
+    w[1] = ld_relaxed(dec + 32 + lane);
     const uint64_t fl = lane < 2 ? ld_acquire(a.flags + (lane == 0 ? kECount : kSFlag)) : 0ull;
     const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2);
     const uint64_t h3 = __shfl_sync(0xffffffffu, w[0], 3);
@@ -190,7 +191,7 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
 #pragma unroll
     for (int j = 2; j < PER; ++j) {
       const int idx = lane + 32 * j;
-      w[j] = idx < need ? ld_relaxed(a.dec + idx) : 0;
+      w[j] = idx < need ? ld_relaxed(dec + idx) : 0;
     }
     bool ok = h2ok;
 #pragma unroll
@@ -2189,6 +2190,7 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
     a.epoll_ns = e2 ? (unsigned)std::atoi(e2) : 64u;
     const char* e3 = std::getenv("GCMC_WALK_REPS");
     a.walk_reps = e3 && std::atoi(e3) > 1 ? std::atoi(e3) : 1;
+
   }
   size_t eval_bytes = T == 128 ? sizeof(EvalShared<128>) : (T == 256 ? sizeof(EvalShared<256>) : sizeof(EvalShared<512>));
   eval_bytes = (eval_bytes + 15) & ~size_t(15);
