@@ -248,9 +248,12 @@ def energy_block(sim, peak):
     rho = n / sim.cfg.volume()
     pairs = 0.5 * n * rho * 4.0 / 3.0 * math.pi * sim.cfg.r_cut ** 3  # within r_c
     ach = 24.0 * n / (p_ms * 1e-3) / 1e9
+    ep = _load_json("energy_ncu.json") or {}
     return {"n": n, "pass_us": 1e3 * p_ms, "kernel_us": 1e3 * k_ms,
             "alg_bytes": 24 * n, "achieved_gbs": ach, "hbm_frac": ach / peak,
             "pairs_in_cutoff": pairs, "pairs_per_s": pairs / (p_ms * 1e-3),
+            "issue_active_pct": ep.get("issue_active_pct"), "fp64_pipe_pct": ep.get("fp64_pipe_pct"),
+            "dram_bytes_ncu": ep.get("dram_bytes"), "ncu_source": ep.get("source"),
             "kernel": "k_energy (energy.cu: warp per cell >= r_cut, 14-cell half shell, FP32 prefilter, compensated sums)"}
 
 

@@ -351,11 +351,15 @@ __device__ __forceinline__ void warp_rank_sort(int32_t* a, int m, int lane) {
   const int32_t v0 = lane < m ? a[lane] : 0x7fffffff;
   const int32_t v1 = lane + 32 < m ? a[lane + 32] : 0x7fffffff;
   int r0 = 0, r1 = 0;
-  for (int k = 0; k < 32; ++k) {
-    const int32_t w0 = __shfl_sync(0xffffffffu, v0, k);
-    const int32_t w1 = __shfl_sync(0xffffffffu, v1, k);
-    r0 += (w0 < v0) + (w1 < v0);
-    r1 += (w0 < v1) + (w1 < v1);
+  if (m <= 32) {  // (the usual case: one value per lane, m rounds)
+    for (int k = 0; k < m; ++k) r0 += __shfl_sync(0xffffffffu, v0, k) < v0;
+  } else {
+    for (int k = 0; k < 32; ++k) {
+      const int32_t w0 = __shfl_sync(0xffffffffu, v0, k);
+      const int32_t w1 = __shfl_sync(0xffffffffu, v1, k);
+      r0 += (w0 < v0) + (w1 < v0);
+      r1 += (w0 < v1) + (w1 < v1);
+    }
   }
   __syncwarp();
   if (lane < m) a[r0] = v0;

@@ -30,11 +30,5 @@ python tools/ncu_engine.py $O/engine2_full.ncu-rep 2097152 $O \
   > $O/engine_ncu.json 2> $O/engine_ncu.err
 timeout 900 ncu --set full --clock-control none -k regex:k_energy -c 1 -o $O/energy_full \
   python tools/time_energy.py --bf-max 0 --sizes 1048576 > $O/ncu_energy.log 2>&1
-ncu -i $O/energy_full.ncu-rep --page raw --csv 2>/dev/null | python -c "
-import csv,sys
-r=list(csv.reader(sys.stdin)); h=r[0]; u=r[1]; d=r[2]
-want=['gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum','smsp__issue_active.avg.pct_of_peak_sustained_active','sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active','sm__warps_active.avg.pct_of_peak_sustained_active','lts__t_sector_hit_rate.pct','launch__registers_per_thread']
-print('k_energy at 1M (random start, rho 0.67), ncu --set full --clock-control none'); print(); print('| metric | value | unit |'); print('|---|---|---|')
-[print('|',m,'|',d[h.index(m)],'|',u[h.index(m)],'|') for m in want if m in h]
-" > $O/energy_ncu.md
+python tools/ncu_energy.py $O/energy_full.ncu-rep $O > $O/energy_ncu.json 2> $O/energy_ncu.err
 echo done
