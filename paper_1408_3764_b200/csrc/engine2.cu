@@ -41,6 +41,7 @@
 // Supported: brick-window strategies (microcell, cell list) with whole-box
 // displacements (max_displacement = 0, the bench and paper configuration).
 // Otherwise engine.cu runs.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -115,6 +116,7 @@ struct EngineArgs {
   double beta, mu, lambda3, vol, temp;
   uint64_t equil, interval;
   int tail, nslots, fitmax;
+  int max_acc;      // accepted moves per round = reserved energy-update groups (<= kMaxAcc)
   double tail_cu, tail_cp, tail_s3, tail_bu, tail_bp;
   uint64_t* dec;    // [kDecStride]
   uint64_t* res;    // [2][kResWords][nslots]
@@ -823,7 +825,7 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
   const int g = tid / T, gt = tid % T, gw = gt >> 5;
   const int bar_id = 1 + g;
   const int slot = (blockIdx.x - 1) * MG + g;
-  const int eslot0 = a.nslots - kMaxAcc;  // groups reserved for energy updates
+  const int eslot0 = a.nslots - a.max_acc;  // groups reserved for energy updates
   WinWs<T>& ws = sh.ws[g];
   auto& G = sh.gs[g];
   const bool grid = a.g.kind != GCMC_ALL_PAIRS;
@@ -1267,7 +1269,7 @@ struct WalkOut {
 // changes only at accepted insertions / deletions.
 __device__ __noinline__ WalkOut walk_warp(const uint32_t* macc, const uint32_t* mcf, const uint32_t* movf,
                                           const uint8_t* mkind, int fit, int* acc_i, int* acc_d,
-                                          int8_t* acck, int lane) {
+                                          int8_t* acck, int lane, int max_acc) {
   int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kStopEnd;
   const int nh = (fit + 31) >> 5;
   // two blocks of 32 moves per ballot pair (independent ballots), so a block
@@ -1321,7 +1323,7 @@ __device__ __noinline__ WalkOut walk_warp(const uint32_t* macc, const uint32_t* 
       const int k = (int)(info >> 2);
       d += k == 1 ? 1 : (k == 2 ? -1 : 0);
       start = e + 1;
-      if (nacc == kMaxAcc) {
+      if (nacc == max_acc) {
         len = e + 1;
         why = kStopFull;
         done = true;
@@ -1597,7 +1599,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       // discarded) so that the walk's code is in the instruction cache when
       // the last slot lands.
       if (warp == 0) {  // one dry run (the walk's code into the instruction cache), then wait
-        walk_warp(sh.pacc, sh.pcf, sh.povf, sh.pkind, sh.plen, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+        walk_warp(sh.pacc, sh.pcf, sh.povf, sh.pkind, sh.plen, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane, a.max_acc);
         while (*(volatile int*)&sh.arrived < fit) __nanosleep(32);
       }
       for (int sl = tid - 32; sl >= 0 && sl < fit; sl += kPollThreads - 32) {
@@ -1641,7 +1643,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
 #endif
       pc.mark(1);
       if (warp == 0) {  // ---- walk (warm: warp 0 ran it on the partial masks while polling)
-        const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane);
+        const WalkOut wo = walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.acc_i, sh.acc_d, sh.acck, lane, a.max_acc);
         if (lane == 0) {
           sh.len = wo.len;
           sh.nacc = wo.nacc;
@@ -1654,7 +1656,7 @@ __device__ void sequencer(const EngineArgs& a, uint8_t* smem) {
       pc.mark(2);
 #ifdef GCMC_PHASE_TIMERS
       if (a.walk_reps == 3) {  // diagnostics: the same walk again, warm (bucket 8)
-        if (warp == 0) walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane);
+        if (warp == 0) walk_warp(sh.macc, sh.mcf, sh.movf, sh.mkind, fit, sh.wscr_i, sh.wscr_d, sh.wscr_k, lane, a.max_acc);
         group_sync(1, kPollThreads);
         pc.mark(8);
       }
@@ -2061,7 +2063,7 @@ bool engine2_supported(const Chain& c) {
   if (std::getenv("GCMC_ENGINE_V1")) return false;
   if (c.grid.kind == GCMC_ALL_PAIRS || c.params.max_displacement > 0.0) return false;
   const int mg = kThreads / c.engine2_group;
-  return (c.engine2_ctas - 1) * mg > kMaxAcc + 1 && (c.engine2_ctas - 1) * mg <= kMaxSlots;
+  return (c.engine2_ctas - 1) * mg > 8 + 1 + 8 && (c.engine2_ctas - 1) * mg <= kMaxSlots;
 }
 
 gcmc_status epart_build(Chain& c, double2* out) {
@@ -2159,7 +2161,13 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
     a.tail_bp = 2.0 / 3.0 * sr9 - sr3;
   }
   a.nslots = (G - 1) * MG;
-  a.fitmax = a.nslots - kMaxAcc - 1 < kMaxMoves ? a.nslots - kMaxAcc - 1 : kMaxMoves;  // + committer
+  // Accepted moves per round, each with its own energy-update group: 32 when
+  // the evaluator groups are plentiful; a smaller engine (a chain sharing the
+  // device, a small box) keeps about a quarter of its groups for them (at
+  // least 8), so more are left for moves: a round stops at max_acc accepts.
+  a.max_acc = a.nslots >= kMaxMoves + kMaxAcc + 1 ? kMaxAcc
+                                                   : std::max(8, std::min(kMaxAcc, a.nslots / 4));
+  a.fitmax = a.nslots - a.max_acc - 1 < kMaxMoves ? a.nslots - a.max_acc - 1 : kMaxMoves;  // + committer
   {
     const char* f = std::getenv("GCMC_FITMAX");
     if (f && std::atoi(f) > 0 && std::atoi(f) < a.fitmax) a.fitmax = std::atoi(f);
