@@ -292,6 +292,7 @@ struct EvalShared {
     int n;
   } eb[kThreads / T];
   int nprev;                      // the previous decision's accepted moves (replica update)
+  uint64_t nstore;                // particles in the store during this round (before the in-flight moves)
   uint32_t prev_pt0[kMaxAcc], prev_pt1[kMaxAcc];
   int prev_kind[kMaxAcc];
   WinWs<T> ws[kThreads / T];
@@ -876,6 +877,11 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
         sh.prev_pt0[lane] = (uint32_t)d.acc[lane].pt0;
         sh.prev_pt1[lane] = (uint32_t)d.acc[lane].pt1;
       }
+      {  // the store still holds the state before the in-flight moves (all-pairs scans it)
+        const int kd = lane < d.nacc ? d.acc[lane].kind : 0;
+        const int dn = __reduce_add_sync(0xffffffffu, kd == 1 ? 1 : (kd == 2 ? -1 : 0));
+        if (lane == 0) sh.nstore = (uint64_t)((int64_t)d.n - dn);
+      }
       if (lane == 0) sh.nprev = d.nacc;
       if (lane < MG) {
         const int s = slot - g + lane;
@@ -1036,8 +1042,15 @@ __device__ void evaluator(const EngineArgs& a, uint8_t* smem) {
       pc.mark(2);
       // ---- S(n): the whole group
       double su = 0.0, sw = 0.0;
-      if (kind != 2) win_sums<T>(a.m, a.b, ws, gt, su, sw);
-      if (gt == 0 && kind != 2) atomicAdd(&a.st->pair_evals, (unsigned long long)ws.total);
+      // all-pairs strategy (strategy.hpp:64-116): S(n) over the whole store,
+      // in-flight moves corrected below like the brick window's
+      const bool allp = a.g.kind == GCMC_ALL_PAIRS;
+      if (kind != 2) {
+        if (allp) allpairs_sums<T>(a.b, a.s.pos, sh.nstore, ws, -1, gt, su, sw);
+        else win_sums<T>(a.m, a.b, ws, gt, su, sw);
+      }
+      if (gt == 0 && kind != 2)
+        atomicAdd(&a.st->pair_evals, (unsigned long long)(allp ? sh.nstore : (uint64_t)ws.total));
       group_reduce<T>(ws, su, sw, bar_id, gt, 32 * lw);
       pc.mark(3);
       if (gw == lw) {
@@ -2061,7 +2074,7 @@ __global__ void k_ediff(const double2* a, const double2* b, uint64_t n, unsigned
 bool engine2_supported(const Chain& c) {
   if (c.params.engine_mode == 1) return false;
   if (std::getenv("GCMC_ENGINE_V1")) return false;
-  if (c.grid.kind == GCMC_ALL_PAIRS || c.params.max_displacement > 0.0) return false;
+  if (c.params.max_displacement > 0.0) return false;
   const int mg = kThreads / c.engine2_group;
   return (c.engine2_ctas - 1) * mg > 8 + 1 + 8 && (c.engine2_ctas - 1) * mg <= kMaxSlots;
 }

@@ -344,3 +344,29 @@ def test_pair_evaluations_are_counted():
     sim.run(2000)
     assert sim.last_run.pair_evals >= 2000 * 0.6 * len(xyz) * 0.9
     sim.close()
+
+
+def test_all_pairs_on_the_maintained_energy_engine_32k():
+    """BASELINE configs[1]'s all-pairs arm: the all-pairs strategy on the
+    maintained-energy engine (S(n) by a scan of the whole store, in-flight
+    moves corrected) is trace-identical to the reference's AllPairsStrategy
+    (strategy.hpp:64-116) and to the per-window engine (engine_mode = 1)."""
+    from paper_1408_3764_b200.config import RunConfig
+
+    box, xyz, rng = config(32768)
+    cfg = RunConfig(temperature=2.0, chemical_potential=1.0, box_length=box, strategy="all_pairs")
+    sim = E().Simulation(cfg, xyz, rng)
+    st0 = sim.dev.get_state()
+    o = oracle_sim("all_pairs", box, xyz, rng.serialize_hex(), st0.energy, st0.virial,
+                   temperature=2.0, chemical_potential=1.0)
+    tr = sim.run(20000, trace=True)
+    _, tp = o.run(20000, trace=True)
+    assert_trace_parity(tr, tp)
+    assert_full_state(sim, o, st0)
+    assert sim.last_run.pair_evals > 20000 * 0.5 * len(xyz)  # whole-store scans
+    old = E().Simulation(cfg, xyz, rng, engine_mode=1)
+    to = old.run(20000, trace=True)
+    assert np.array_equal(to["accepted"], tr["accepted"])
+    assert np.array_equal(old.particles(), sim.particles())
+    sim.close()
+    old.close()
