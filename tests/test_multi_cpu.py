@@ -83,3 +83,42 @@ def test_reference_arm_world2_prints_one_line():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 2
     assert d["cpu_baseline"]["kind"] == "reference"
+
+
+def test_chains_per_gpu_state_points():
+    """--chains-per-gpu K: chain c of rank g is state point g * K + c: sweep
+    mu = -3 + g + c / K, distinct seeds over the whole job."""
+    s = bench.parse_args(["--sweep", "--chains-per-gpu", "4"])
+    pts = [bench.state_point(s, g, c) for g in range(2) for c in range(4)]
+    assert [p[0] for p in pts] == [-3.0 + g + c / 4 for g in range(2) for c in range(4)]
+    assert len({p[1] for p in pts}) == 8
+    cfg = bench.config_dict(s, 2)
+    assert cfg["chains"] == 8 and len(cfg["mu"]) == 8 and "4 concurrent chains" in cfg["workload"]
+    r = bench.parse_args(["--chains-per-gpu", "3"])
+    assert {bench.state_point(r, 0, c)[0] for c in range(3)} == {1.0}
+
+
+def test_latency_floor_from_measured_latencies(tmp_path, monkeypatch):
+    """The latency block's floor: 2 one-way visibilities (half a ping-pong) +
+    2 L2 hops + one pair term + 7 shuffle-add levels, in ns at the SM clock."""
+    ub = {"source": "test", "sm_ghz": 2.0, "l2_relaxed_chase_cycles": 400, "pingpong_cycles": 1400,
+          "pair_term_cycles": 300, "shfl_dadd_cycles": 40}
+    (tmp_path / "ubench.json").write_text(json.dumps(ub))
+    monkeypatch.setattr(bench, "PROFILE_DIR", str(tmp_path))
+    lat = bench.latency_block({"issue_active_pct": 7.0, "source": "x"}, 20000.0, 350.0)
+    floor = (1400 + 2 * 400 + 300 + 7 * 40) / 2.0
+    assert abs(lat["floor_ns_per_round"] - floor) < 1e-9
+    assert abs(lat["floor_frac"] - floor / 20000.0) < 1e-12
+    assert lat["issue_active_pct"] == 7.0 and abs(lat["ns_per_move"] - 20000.0 / 350.0) < 1e-9
+
+
+def test_profiles_summaries_are_consistent():
+    """The committed bench-window ncu summaries bench.py reads exist and are
+    self-consistent (traffic per move = traffic per launch / moves)."""
+    e = json.load(open(os.path.join(ROOT, "profiles", "engine_ncu.json")))
+    assert abs(e["dram_bytes_per_move"] * e["moves_per_launch"] - e["dram_bytes_per_launch"]) < 1.0
+    assert 0 < e["issue_active_pct"] < 100 and 0 < e["fp64_pipe_pct"] < 100
+    en = json.load(open(os.path.join(ROOT, "profiles", "energy_ncu.json")))
+    assert en["duration_us"] > 0 and en["dram_bytes"] > 0
+    u = json.load(open(os.path.join(ROOT, "profiles", "ubench.json")))
+    assert u["pingpong_cycles"] > 0 and u["l2_relaxed_chase_cycles"] > 0
