@@ -267,6 +267,11 @@ void profile_report(Chain& c) {
       if (lt[12] && lt[14] && lt[17])
         std::fprintf(stderr, "\n[dbg] latency ns: publish->CTA sees D mean=%.0f max=%.0f; publish->slot result mean=%.0f; publish->last result (per round) mean=%.0f; publish->sequencer has all mean=%.0f",
                      (double)lt[10] / lt[12], (double)lt[11], (double)lt[13] / lt[14], (double)lt[16] / lt[17], (double)lt[15] / lt[17]);
+      unsigned long long pd[4];
+      cudaMemcpy(pd, c.prof + 3680, sizeof pd, cudaMemcpyDeviceToHost);
+      if (pd[2])
+        std::fprintf(stderr, "\n[dbg] decision poll (per CTA-round): header words seen %.0f ns after publish, then %.0f ns until the state flags allowed it; flags held it > 300 ns in %.1f %% of polls",
+                     (double)pd[0] / pd[2], (double)pd[1] / pd[2], 100.0 * pd[3] / pd[2]);
       unsigned long long gq[17];
       cudaMemcpy(gq, c.prof + 3640, sizeof gq, cudaMemcpyDeviceToHost);
       if (gq[7])

@@ -178,12 +178,18 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
   constexpr int PER = (kDecWords + 31) / 32;  // 5
   uint64_t w[PER];
   const uint64_t* dec = a.dec;
+#ifdef GCMC_PHASE_TIMERS
+  unsigned long long t_tag = 0;  // first poll that saw the header words of D_r
+#endif
   for (;;) {
     w[0] = ld_relaxed(dec + lane);
     w[1] = ld_relaxed(dec + 32 + lane);
     const uint64_t fl = lane < 2 ? ld_acquire(a.flags + (lane == 0 ? kECount : kSFlag)) : 0ull;
     const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2);
     const uint64_t h3 = __shfl_sync(0xffffffffu, w[0], 3);
+#ifdef GCMC_PHASE_TIMERS
+    if (!t_tag && tagged(h2, r) && tagged(h3, r)) t_tag = gtimer();
+#endif
     const uint64_t ecnt = __shfl_sync(0xffffffffu, fl, 0) & 0xffffffffull;
     const uint64_t sflg = __shfl_sync(0xffffffffu, fl, 1);
     const bool h2ok = tagged(h2, r) && tagged(h3, r) &&
@@ -204,6 +210,16 @@ __device__ __forceinline__ void poll_dec(const EngineArgs& a, uint32_t r, Dec& d
     if (__all_sync(0xffffffffu, ok)) break;
     __nanosleep(a.epoll_ns);
   }
+#ifdef GCMC_PHASE_TIMERS
+  if (a.prof && lane == 0 && r > 2 && t_tag) {  // decision visible vs state flags (ECount, SFlag) ready
+    const unsigned long long pub = ld_relaxed(reinterpret_cast<uint64_t*>(a.prof + 3600 + (r & 1)));
+    const unsigned long long now = gtimer();
+    atomicAdd(a.prof + 3680, t_tag - pub);
+    atomicAdd(a.prof + 3681, now - t_tag);
+    atomicAdd(a.prof + 3682, 1ull);
+    if (now - t_tag > 300) atomicAdd(a.prof + 3683, 1ull);
+  }
+#endif
   const uint64_t h2 = __shfl_sync(0xffffffffu, w[0], 2) & kPay;
   const int nacc = (int)(h2 & 0xff);
   const int need = kDecHdr + kDecEnt * nacc;
