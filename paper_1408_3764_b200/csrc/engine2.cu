@@ -305,7 +305,6 @@ struct EvalShared {
   struct EBuf {                   // buffered neighbour energy updates (energy_update)
     uint32_t id[kEBuf];            // particle | pass << 31
     double u[kEBuf], w[kEBuf];
-    int16_t link[kEBuf];           // pass 0: its pass-1 partner (same particle) or -1; pass 1: -2 partnered
     int n;
   } eb[kThreads / T];
   int nprev;                      // the previous decision's accepted moves (replica update)
@@ -699,45 +698,15 @@ __device__ __noinline__ void energy_update(const EngineArgs& a, EvalShared<T>& s
   }
   __threadfence();
   group_sync(bar_id, T);
-  if (gt == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + kETrav), 1ull);
-  // A particle near both the old and the new position gets two updates, old
-  // window first. Pair them (before the wait for kGo, off the critical path)
-  // so that one thread issues both: same-thread atomics to one address are
-  // performed in program order, so the two passes need no fence between them.
-  const int nb = B.n;
-  const bool linked = nb <= kEBuf;
-  if (linked) {
-    for (int q = gt; q < nb; q += T) B.link[q] = -1;
-    group_sync(bar_id, T);
-    for (int q = gt; q < nb; q += T) {
-      const uint32_t v = B.id[q];
-      if (!(v >> 31)) continue;  // pass-1 entries look for their pass-0 partner
-      const uint32_t want = v & 0x7fffffffu;
-      for (int q0 = 0; q0 < nb; ++q0)
-        if (B.id[q0] == want) {  // pass 0, same particle
-          B.link[q0] = (int16_t)q;
-          B.link[q] = -2;
-          break;
-        }
-    }
+  if (gt == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + kETrav), 1ull);
+    while (ld_acquire(a.flags + kGo) < (uint64_t)r) nap();
   }
-  if (gt == 0) while (ld_acquire(a.flags + kGo) < (uint64_t)r) nap();
   group_sync(bar_id, T);
   ec.mark(2);
-  if (linked) {
-    for (int q = gt; q < nb; q += T) {
-      const int lk = B.link[q];
-      if (lk == -2) continue;  // issued by its pass-0 partner's thread
-      const uint32_t id = B.id[q] & 0x7fffffffu;
-      atomicAdd(&a.ep[id].x, B.u[q]);
-      atomicAdd(&a.ep[id].y, B.w[q]);
-      if (lk >= 0) {  // then the same particle's new-window update
-        atomicAdd(&a.ep[id].x, B.u[lk]);
-        atomicAdd(&a.ep[id].y, B.w[lk]);
-      }
-    }
-  }
-  for (int pass = 0; pass < 2 && !linked; ++pass) {  // more updates than the buffer: two fenced passes
+  const int nb = B.n;
+  // old window first (a particle near both positions gets two updates)
+  for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
       __threadfence();
       group_sync(bar_id, T);
