@@ -77,7 +77,9 @@ typedef struct gcmc_params {
                                  after the first (0 = 11, at most 15) */
   int32_t engine_bias;        /* initial variant order: -1 N expected to fall, +1 rise (0 = -1) */
   int32_t engine_mode;        /* 0 = maintained-energy engine where supported (brick strategies,
-                                 max_displacement = 0), 1 = per-window engine always */
+                                 max_displacement = 0), 1 = per-window engine always,
+                                 2 = chain-per-SM engine (one CTA; brick strategies,
+                                 max_displacement = 0, else as 0) */
   int32_t engine_share;       /* chains that share the device (gcmc_run_chains): with engine_ctas
                                  = 0 this chain's engine takes (SMs - share) / share CTAs
                                  (0 or 1 = the whole device) */
@@ -111,6 +113,9 @@ typedef struct gcmc_run_result {
   double gen_ms;      /* device time of proposal generation */
   uint64_t pair_evals; /* FP64 pair evaluations (minimum image + cutoff test) the device
                           performed for this call: windows, energy updates, all-pairs scans */
+  int32_t engine;     /* engine that ran the moves: 1 per-window (engine.cu), 2 multi-SM
+                         maintained-energy (engine2.cu), 3 chain-per-SM (engine_sm.cu) */
+  int32_t pad;
 } gcmc_run_result;
 
 typedef struct gcmc_dev gcmc_dev;

@@ -43,7 +43,7 @@ class GcmcState(C.Structure):
 
 class GcmcRunResult(C.Structure):
     _fields_ = [("state", GcmcState), ("moves", _u64), ("rounds", _u64), ("device_ms", _d),
-                ("gen_ms", _d), ("pair_evals", _u64)]
+                ("gen_ms", _d), ("pair_evals", _u64), ("engine", _i32), ("pad", _i32)]
 
 
 TRACE_DTYPE = np.dtype([("kind", "<i4"), ("accepted", "<i4"), ("delta_u", "<f8"),

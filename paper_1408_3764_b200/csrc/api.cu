@@ -420,6 +420,7 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   c->engine_ctas = P.engine_ctas > 1 && P.engine_ctas <= c->sm_count ? P.engine_ctas : c->sm_count - 1;
   if (P.engine_ctas <= 1 && P.engine_share > 1) {  // K chains on one device: 1/K of the SMs each
     c->engine_ctas = (c->sm_count - P.engine_share) / P.engine_share;
+    if (c->engine_ctas < 2 && P.engine_mode == 2) c->engine_ctas = 2;  // (one CTA per chain)
     if (c->engine_ctas < 2) {
       delete c;
       return set_error(GCMC_ARG, "engine_share: too many chains for this device");
@@ -857,12 +858,8 @@ gcmc_status gcmc_get_state(gcmc_dev* h, gcmc_state* out) {
   return GCMC_OK;
 }
 
-gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_run_result* out) {
-  Chain& c = *H(h);
-  cudaSetDevice(c.device);
-  if (!c.built) return set_error(GCMC_STATE, "grid not built (upload positions first)");
-  const uint64_t kChunk = 1ull << 21;
-  const uint64_t chunk_cap = n < kChunk ? (n ? n : 1) : kChunk;
+// Proposal buffers for chunks of up to chunk_cap moves.
+gcmc_status props_reserve(Chain& c, uint64_t chunk_cap, bool trace) {
   if (chunk_cap > c.props_cap) {
     CK(cudaStreamSynchronize(c.gen_stream), "proposals");
     cudaFree(c.props);
@@ -879,6 +876,99 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     CK(cudaMalloc(&c.trace, chunk_cap * sizeof(gcmc_trace_rec)), "alloc trace");
     c.trace_cap = chunk_cap;
   }
+  return GCMC_OK;
+}
+
+// The proposals of the next m moves into c.props (generated during the
+// previous chunk when it had the same size), then the chunk after it (mn
+// moves) on the SM the engine leaves free.
+gcmc_status props_next_chunk(Chain& c, uint64_t m, uint64_t mn) {
+  gcmc_status s = GCMC_OK;
+  CK(cudaEventRecord(c.ev[0], c.stream), "event");
+  if (c.ahead_n == m) {  // generated during the previous batch
+    CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
+    std::swap(c.props, c.props_next);
+    std::swap(c.mt, c.mt_next);
+  } else {
+    // a look-ahead copy of c.mt may still be in flight on gen_stream
+    CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
+    if ((s = gen_proposals(c, m, c.stream))) return s;
+  }
+  c.ahead_n = 0;
+  CK(cudaEventRecord(c.ev_mt, c.stream), "ahead");
+  CK(cudaStreamWaitEvent(c.gen_stream, c.ev_mt, 0), "ahead");
+  CK(cudaMemcpyAsync(c.mt_next, c.mt, 314 * sizeof(uint64_t), cudaMemcpyDeviceToDevice, c.gen_stream),
+     "ahead");
+  if ((s = gen_proposals_into(c, c.mt_next, c.props_next, mn, c.gen_stream))) return s;
+  CK(cudaEventRecord(c.ev_ahead, c.gen_stream), "ahead");
+  c.ahead_n = mn;
+  return GCMC_OK;
+}
+
+// Moves [off, m) of the chunk in c.props on the chain's own engine. When the
+// evaluation mirror (not the reference grid) runs out of records in a brick,
+// the engine stops before the move that overflowed with everything before it
+// committed: the mirror's records per brick double and the chunk continues
+// there, so the mirror never fails a state the reference accepts (up to
+// kMaxCap).
+gcmc_status run_chunk_from(Chain& c, uint64_t m, uint64_t off, gcmc_trace_rec* trace_d, float& eng_ms,
+                           uint64_t& rounds) {
+  gcmc_status s = GCMC_OK;
+  for (;;) {
+    if ((s = ensure_store(c, m - off))) return s;
+    profile_arm(c);
+    Proposal* const p0 = c.props;
+    c.props += off;
+    CK(cudaEventRecord(c.ev[1], c.stream), "event");
+    s = engine_run(c, m - off, trace_d ? trace_d + off : nullptr, c.stream);
+    c.props = p0;
+    if (s) return s;
+    CK(cudaEventRecord(c.ev[2], c.stream), "event");
+    if ((s = pull_state(c))) return s;
+    float b = 0;
+    cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
+    eng_ms += b;
+    rounds += c.st_host->rounds;
+    profile_report(c);
+    ChainState& st = *c.st_host;
+    if (st.error == GCMC_CELL_OVERFLOW && st.err_c == 1 && c.mirror.cap < kMaxCap) {
+      off += st.moves_done;
+      st.error = 0;
+      sync_state_to_device(c);
+      if ((s = arena_alloc(c, std::min(kMaxCap, 2 * c.mirror.cap), c.capn, true))) return s;
+      continue;
+    }
+    return GCMC_OK;
+  }
+}
+
+// A failed chain's error in the reference's wording (clears the device flag).
+gcmc_status chain_error(Chain& c) {
+  const ChainState& st = *c.st_host;
+  const int err = st.error;
+  const int64_t ea = st.err_a, eb = st.err_b, ec = st.err_c;
+  c.st_host->error = 0;
+  sync_state_to_device(c);
+  if (err == GCMC_CELL_OVERFLOW && ec == 1) {
+    std::ostringstream os;
+    os << "mirror: brick " << ea << " exceeds capacity " << c.mirror.cap
+       << " (the evaluation mirror's limit; density too high)";
+    return set_error(GCMC_CELL_OVERFLOW, os.str());
+  }
+  if (err == GCMC_CELL_OVERFLOW) return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, ea, eb));
+  std::ostringstream os;
+  os << strategy_name(c.grid.kind) << ": particle " << ea << " not found in cell " << eb;
+  return set_error((gcmc_status)err, os.str());
+}
+
+gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_run_result* out) {
+  Chain& c = *H(h);
+  cudaSetDevice(c.device);
+  if (!c.built) return set_error(GCMC_STATE, "grid not built (upload positions first)");
+  const uint64_t kChunk = 1ull << 21;
+  const uint64_t chunk_cap = n < kChunk ? (n ? n : 1) : kChunk;
+  gcmc_status s = props_reserve(c, chunk_cap, trace != nullptr);
+  if (s) return s;
   float gen_ms = 0.f, eng_ms = 0.f;
   uint64_t done = 0, rounds = 0;
   if (out) {  // the device counter before the call
@@ -886,65 +976,15 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     if (ps) return ps;
   }
   const unsigned long long pairs0 = c.st_host->pair_evals;
-  gcmc_status s = GCMC_OK;
   while (done < n) {
     const uint64_t m = std::min(chunk_cap, n - done);
-    CK(cudaEventRecord(c.ev[0], c.stream), "event");
-    if (c.ahead_n == m) {  // generated during the previous batch
-      CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
-      std::swap(c.props, c.props_next);
-      std::swap(c.mt, c.mt_next);
-    } else {
-      // a look-ahead copy of c.mt may still be in flight on gen_stream
-      CK(cudaStreamWaitEvent(c.stream, c.ev_ahead, 0), "ahead");
-      if ((s = gen_proposals(c, m, c.stream))) return s;
-    }
-    c.ahead_n = 0;
-    {  // the next batch, on the SM the engine leaves free
-      const uint64_t left = n - done - m;
-      const uint64_t mn = left ? std::min(chunk_cap, left) : m;
-      CK(cudaEventRecord(c.ev_mt, c.stream), "ahead");
-      CK(cudaStreamWaitEvent(c.gen_stream, c.ev_mt, 0), "ahead");
-      CK(cudaMemcpyAsync(c.mt_next, c.mt, 314 * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
-                         c.gen_stream), "ahead");
-      if ((s = gen_proposals_into(c, c.mt_next, c.props_next, mn, c.gen_stream))) return s;
-      CK(cudaEventRecord(c.ev_ahead, c.gen_stream), "ahead");
-      c.ahead_n = mn;
-    }
-    // Moves [off, m) of the chunk. When the evaluation mirror (not the
-    // reference grid) runs out of records in a brick, the engine stops before
-    // the move that overflowed with everything before it committed: the
-    // mirror's records per brick double and the chunk continues there, so
-    // the mirror never fails a state the reference accepts (up to kMaxCap).
-    uint64_t off = 0;
-    for (;;) {
-      if ((s = ensure_store(c, m - off))) return s;
-      profile_arm(c);
-      Proposal* const p0 = c.props;
-      c.props += off;
-      CK(cudaEventRecord(c.ev[1], c.stream), "event");
-      s = engine_run(c, m - off, trace ? c.trace + off : nullptr, c.stream);
-      c.props = p0;
-      if (s) return s;
-      CK(cudaEventRecord(c.ev[2], c.stream), "event");
-      if ((s = pull_state(c))) return s;
-      float a = 0, b = 0;
-      cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
-      cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
-      gen_ms += off ? 0.f : a;
-      eng_ms += b;
-      rounds += c.st_host->rounds;
-      profile_report(c);
-      ChainState& st = *c.st_host;
-      if (st.error == GCMC_CELL_OVERFLOW && st.err_c == 1 && c.mirror.cap < kMaxCap) {
-        off += st.moves_done;
-        st.error = 0;
-        sync_state_to_device(c);
-        if ((s = arena_alloc(c, std::min(kMaxCap, 2 * c.mirror.cap), c.capn, true))) return s;
-        continue;
-      }
-      break;
-    }
+    const uint64_t left = n - done - m;
+    if ((s = props_next_chunk(c, m, left ? std::min(chunk_cap, left) : m))) return s;
+    CK(cudaEventRecord(c.ev[3], c.stream), "event");
+    if ((s = run_chunk_from(c, m, 0, trace ? c.trace : nullptr, eng_ms, rounds))) return s;
+    float a = 0;
+    cudaEventElapsedTime(&a, c.ev[0], c.ev[3]);
+    gen_ms += a;
     if (trace)
       CK(cudaMemcpyAsync(trace + done, c.trace, m * sizeof(gcmc_trace_rec), cudaMemcpyDeviceToHost,
                          c.stream),
@@ -956,22 +996,7 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     }
     done += m;
   }
-  const ChainState& st = *c.st_host;
-  if (st.error) {
-    const int err = st.error;
-    c.st_host->error = 0;
-    sync_state_to_device(c);
-    if (err == GCMC_CELL_OVERFLOW && st.err_c == 1) {
-      std::ostringstream os;
-      os << "mirror: brick " << st.err_a << " exceeds capacity " << c.mirror.cap
-         << " (the evaluation mirror's limit; density too high)";
-      return set_error(GCMC_CELL_OVERFLOW, os.str());
-    }
-    if (err == GCMC_CELL_OVERFLOW) return set_error(GCMC_CELL_OVERFLOW, overflow_message(c, st.err_a, st.err_b));
-    std::ostringstream os;
-    os << strategy_name(c.grid.kind) << ": particle " << st.err_a << " not found in cell " << st.err_b;
-    return set_error((gcmc_status)err, os.str());
-  }
+  if (c.st_host->error) return chain_error(c);
   if (out) {
     gcmc_get_state(h, &out->state);
     out->moves = done;
@@ -979,7 +1004,100 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
     out->device_ms = eng_ms;
     out->gen_ms = gen_ms;
     out->pair_evals = c.st_host->pair_evals - pairs0;
+    out->engine = c.last_engine;
+    out->pad = 0;
   }
+  return GCMC_OK;
+}
+
+// K chain-per-SM chains on one device in ONE launch per chunk (one CTA per
+// chain): separate launches from separate streams serialise once the streams
+// outnumber the device's hardware queues. Proposals are generated per chain
+// (the next chunk's during this one's engine launch); a chain whose mirror
+// overflows mid-chunk finishes that chunk on its own launches.
+gcmc_status run_chains_sm(const std::vector<Chain*>& cs, const uint64_t* n, gcmc_run_result* out) {
+  const int k = (int)cs.size();
+  const uint64_t kChunk = 1ull << 21;
+  gcmc_status s = GCMC_OK;
+  std::vector<uint64_t> cap(k), done(k, 0), rounds(k, 0), m(k, 0);
+  std::vector<float> eng_ms(k, 0.f), gen_ms(k, 0.f);
+  std::vector<unsigned long long> pairs0(k);
+  for (int i = 0; i < k; ++i) {
+    Chain& c = *cs[i];
+    if (!c.built) return set_error(GCMC_STATE, "grid not built (upload positions first)");
+    cap[i] = n[i] < kChunk ? (n[i] ? n[i] : 1) : kChunk;
+    if ((s = props_reserve(c, cap[i], false))) return s;
+    if ((s = pull_state(c))) return s;
+    pairs0[i] = c.st_host->pair_evals;
+  }
+  Chain& c0 = *cs[0];
+  for (;;) {
+    std::vector<Chain*> run;
+    std::vector<uint64_t> rm;
+    std::vector<int> idx;
+    for (int i = 0; i < k; ++i) {
+      if (done[i] >= n[i]) continue;
+      Chain& c = *cs[i];
+      m[i] = std::min(cap[i], n[i] - done[i]);
+      const uint64_t left = n[i] - done[i] - m[i];
+      if ((s = props_next_chunk(c, m[i], left ? std::min(cap[i], left) : m[i]))) return s;
+      if ((s = ensure_store(c, m[i]))) return s;
+      if (!c.e_valid) {
+        if ((s = epart_build(c, c.ep))) return s;
+        c.e_valid = true;
+      }
+      CK(cudaEventRecord(c.ev[1], c.stream), "event");
+      CK(cudaStreamWaitEvent(c0.stream, c.ev[1], 0), "event");
+      run.push_back(&c);
+      rm.push_back(m[i]);
+      idx.push_back(i);
+    }
+    if (run.empty()) break;
+    CK(cudaEventRecord(c0.ev[3], c0.stream), "event");
+    if ((s = engine_sm_run_many(run.data(), (int)run.size(), rm.data(), c0.stream))) return s;
+    CK(cudaEventRecord(c0.ev[2], c0.stream), "event");
+    float ems = 0.f;
+    CK(cudaEventSynchronize(c0.ev[2]), "engine");
+    cudaEventElapsedTime(&ems, c0.ev[3], c0.ev[2]);
+    for (size_t q = 0; q < run.size(); ++q) {
+      const int i = idx[q];
+      Chain& c = *run[q];
+      CK(cudaStreamWaitEvent(c.stream, c0.ev[2], 0), "event");
+      float a = 0.f;
+      cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+      gen_ms[i] += a;
+      eng_ms[i] += ems;
+      if ((s = pull_state(c))) return s;
+      rounds[i] += c.st_host->rounds;
+      c.last_engine = 3;
+      ChainState& st = *c.st_host;
+      if (st.error == GCMC_CELL_OVERFLOW && st.err_c == 1 && c.mirror.cap < kMaxCap) {
+        const uint64_t off = st.moves_done;  // finish this chunk on the chain's own launches
+        st.error = 0;
+        sync_state_to_device(c);
+        if ((s = arena_alloc(c, std::min(kMaxCap, 2 * c.mirror.cap), c.capn, true))) return s;
+        if ((s = run_chunk_from(c, m[i], off, nullptr, eng_ms[i], rounds[i]))) return s;
+      }
+      if (c.st_host->error) {
+        c.ahead_n = 0;
+        const gcmc_status e = chain_error(c);
+        return set_error(e, "chain " + std::to_string(i) + ": " + g_last_error);
+      }
+      done[i] += m[i];
+    }
+  }
+  if (out)
+    for (int i = 0; i < k; ++i) {
+      Chain& c = *cs[i];
+      gcmc_get_state(reinterpret_cast<gcmc_dev*>(cs[i]), &out[i].state);
+      out[i].moves = done[i];
+      out[i].rounds = rounds[i];
+      out[i].device_ms = eng_ms[i];
+      out[i].gen_ms = gen_ms[i];
+      out[i].pair_evals = c.st_host->pair_evals - pairs0[i];
+      out[i].engine = 3;
+      out[i].pad = 0;
+    }
   return GCMC_OK;
 }
 
@@ -998,6 +1116,19 @@ gcmc_status gcmc_run_chains(gcmc_dev* const* hs, int32_t k, const uint64_t* n, g
       if (hs[j] == hs[i]) return set_error(GCMC_ARG, "a chain appears twice");
   }
   if (k == 1) return gcmc_run_moves(hs[0], n[0], nullptr, out);
+  {  // chain-per-SM chains on one device: one launch for all of them
+    std::vector<Chain*> cs;
+    bool batch = true;
+    for (int32_t i = 0; i < k; ++i) {
+      Chain* c = H(hs[i]);
+      batch = batch && c->device == H(hs[0])->device && engine_sm_supported(*c);
+      cs.push_back(c);
+    }
+    if (batch) {
+      cudaSetDevice(cs[0]->device);
+      return run_chains_sm(cs, n, out);
+    }
+  }
   std::vector<gcmc_status> st(k, GCMC_OK);
   std::vector<std::string> msg(k);
   std::vector<std::thread> th;

@@ -1416,7 +1416,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_engine(EngineArgs a) {
 
 gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaStream_t s) {
   if (nmoves == 0) return GCMC_OK;
-  if (engine2_supported(c)) return engine2_run(c, nmoves, trace_d, s);
+  if (engine_sm_supported(c)) {
+    c.last_engine = 3;
+    return engine_sm_run(c, nmoves, trace_d, s);
+  }
+  if (engine2_supported(c)) {
+    c.last_engine = 2;
+    return engine2_run(c, nmoves, trace_d, s);
+  }
+  c.last_engine = 1;
   c.e_valid = false;  // this engine does not maintain the per-particle energies
   const gcmc_params& P = c.params;
   EngineArgs a{};

@@ -65,6 +65,7 @@ struct Chain {
   bool e_valid = false;
   void* eng2_buf = nullptr;
   size_t eng2_bytes = 0;
+  int last_engine = 0;           // gcmc_run_result.engine of the last engine_run
   unsigned long long* prof = nullptr;
   unsigned long long* stamp = nullptr;  // per-round global timestamps (GCMC_ENGINE_LATENCY=1)
 };
@@ -102,6 +103,12 @@ gcmc_status engine2_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStrea
 gcmc_status epart_build(Chain& c, double2* out);
 gcmc_status epart_drift(Chain& c, double* du, double* dw);
 gcmc_status epart_dump(Chain& c, double* maint, double* fresh);
+
+// engine_sm.cu: the chain-per-SM engine (one CTA; engine_mode = 2)
+bool engine_sm_supported(const Chain& c);
+gcmc_status engine_sm_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
+// k chains (one CTA each) in one launch on stream s; proposals in each c.props
+gcmc_status engine_sm_run_many(Chain* const* cs, int k, const uint64_t* n, cudaStream_t s);
 
 // initcfg.cu: random_initial_configuration on the device (same stream and result)
 gcmc_status device_initial_configuration(int device, uint64_t n, double l, double min_sep, uint64_t seed,
