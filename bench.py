@@ -48,7 +48,8 @@ def parse_args(argv=None):
     ap.add_argument("--mu", type=float, default=1.0)
     ap.add_argument("--temperature", type=float, default=2.0)
     ap.add_argument("--strategy", default="microcell")
-    ap.add_argument("--moves-per-step", type=int, default=1 << 22)
+    ap.add_argument("--moves-per-step", type=int, default=None,
+                    help="moves per chain per step (default 2^22; 2^20 with >= 12 chains per GPU)")
     ap.add_argument("--cpu-moves", type=int, default=100000,
                     help="(--impl reference) unused; kept for compatibility")
     ap.add_argument("--cpu-steps", type=int, default=1,
@@ -64,6 +65,8 @@ def parse_args(argv=None):
                     help="BASELINE configs[4]: mu isotherm sweep, one 64k chain per GPU "
                          "(rank g runs mu = -3 + g, seed 1 + g)")
     a = ap.parse_args(argv)
+    if a.moves_per_step is None:
+        a.moves_per_step = 1 << 20 if a.chains_per_gpu >= 12 else 1 << 22
     if a.sweep:
         if a.n0 == 1 << 20:
             a.n0 = 1 << 16
@@ -165,7 +168,8 @@ def config_dict(a, world):
     else:
         wl = f"LJ fluid GCMC N0={a.n0}"
     if a.chains_per_gpu > 1:
-        wl += f", {a.chains_per_gpu} concurrent chains per GPU (gcmc_run_chains)"
+        wl += f", {a.chains_per_gpu} concurrent chains per GPU (gcmc_run_chains"
+        wl += ", chain-per-SM engine: one CTA per chain, one launch)" if a.chains_per_gpu >= 12 else ")"
     k = a.chains_per_gpu
     mus = ([-3.0 + g + c / k for g in range(world) for c in range(k)] if a.sweep else a.mu)
     return {"workload": wl,
@@ -431,6 +435,8 @@ def main():
     sim = sims[0]
     K = len(sims)
 
+    engine_used = [0]
+
     def step():
         """One step: --moves-per-step moves on every chain of this rank.
         Returns (device ms of the step, engine ms, rounds). One chain: the
@@ -439,10 +445,12 @@ def main():
         if K == 1:
             sim.run(a.moves_per_step)
             r = sim.last_run
+            engine_used[0] = r.engine
             return r.device_ms + r.gen_ms, r.device_ms, r.rounds, r.pair_evals
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         res = E.run_chains(sims, a.moves_per_step)
+        engine_used[0] = res[0].engine
         e1.record()
         e1.synchronize()
         ms = e0.elapsed_time(e1)
@@ -518,11 +526,16 @@ def main():
     moves_per_launch = a.moves_per_step / launches
     eng_launch_s = eng_ms / 1e3 / (a.steps * launches)
     achieved = ALG_BYTES_PER_MOVE * moves_per_launch / eng_launch_s / 1e9
-    eprof = engine_profile()
+    sm_engine = engine_used[0] == 3
+    eprof = None if sm_engine else engine_profile()
     traffic = eprof["dram_bytes_per_move"] * moves_per_launch if eprof else None
     n_final = [s_.dev.get_state().n for s_ in sims]
     ns_round = 1e9 * (eng_ms / 1e3) / max(rounds / K, 1)
-    latency = latency_block(eprof, ns_round, a.moves_per_step * a.steps * K / max(rounds, 1))
+    latency = (latency_block(eprof, ns_round, a.moves_per_step * a.steps * K / max(rounds, 1))
+               if not sm_engine else
+               {"ns_per_round": ns_round, "moves_per_round": a.moves_per_step * a.steps * K / max(rounds, 1),
+                "note": "chain-per-SM engine: every hand-off of a round is a CTA barrier; "
+                        "per-phase cycles in profiles/r02sm (GCMC_SM_PHASES=1)"})
     energy = energy_block(sim, peak) if rank == 0 and not a.no_energy else None
     if rank == 0:
         line = {
@@ -535,7 +548,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind,
-                         "kernel": "k_engine2 (persistent whole-GPU Metropolis loop, maintained per-particle energies)",
+                         "kernel": ("k_engine_sm (one CTA per chain, all chains of the GPU in one launch)"
+                                    if sm_engine else
+                                    "k_engine2 (persistent whole-GPU Metropolis loop, maintained per-particle energies)"),
                          "alg_bytes_per_move": ALG_BYTES_PER_MOVE,
                          "traffic_source": eprof["source"] if eprof else None,
                          "note": "serial Markov chain: latency-bound, not HBM-bound; the "
@@ -546,7 +561,10 @@ def main():
             "clocks": clk.summary(),
             # per step, chain and 2^21-move chunk (gcmc_run_moves): the engine
             # plus the look-ahead proposal generation (k_gen2, k_annotate)
-            "gpu_launches": 3 * a.steps * K * launches,
+            "gpu_launches": (a.steps * launches * (1 + 2 * K) if sm_engine and K > 1
+                             else 3 * a.steps * K * launches),
+            "engine": {1: "per-window (engine.cu)", 2: "multi-SM maintained-energy (engine2.cu)",
+                       3: "chain-per-SM (engine_sm.cu)"}.get(engine_used[0], "?"),
             "pair_evals_per_s": pairs * world / t_dev,
             "pair_evals_per_move": pairs / moves_rank,
             "pair_evals_note": "counted on the device (gcmc_run_result.pair_evals): FP64 "

@@ -77,9 +77,10 @@ typedef struct gcmc_params {
                                  after the first (0 = 11, at most 15) */
   int32_t engine_bias;        /* initial variant order: -1 N expected to fall, +1 rise (0 = -1) */
   int32_t engine_mode;        /* 0 = maintained-energy engine where supported (brick strategies,
-                                 max_displacement = 0), 1 = per-window engine always,
-                                 2 = chain-per-SM engine (one CTA; brick strategies,
-                                 max_displacement = 0, else as 0) */
+                                 max_displacement = 0; the chain-per-SM engine when
+                                 engine_share >= 12), 1 = per-window engine always,
+                                 2 = chain-per-SM engine (one CTA per chain; brick
+                                 strategies, max_displacement = 0, else as 0) */
   int32_t engine_share;       /* chains that share the device (gcmc_run_chains): with engine_ctas
                                  = 0 this chain's engine takes (SMs - share) / share CTAs
                                  (0 or 1 = the whole device) */

@@ -420,7 +420,8 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   c->engine_ctas = P.engine_ctas > 1 && P.engine_ctas <= c->sm_count ? P.engine_ctas : c->sm_count - 1;
   if (P.engine_ctas <= 1 && P.engine_share > 1) {  // K chains on one device: 1/K of the SMs each
     c->engine_ctas = (c->sm_count - P.engine_share) / P.engine_share;
-    if (c->engine_ctas < 2 && P.engine_mode == 2) c->engine_ctas = 2;  // (one CTA per chain)
+    if (c->engine_ctas < 2 && (P.engine_mode == 2 || (P.engine_mode == 0 && P.engine_share >= 12)))
+      c->engine_ctas = 2;  // (the chain-per-SM engine runs instead: one CTA per chain)
     if (c->engine_ctas < 2) {
       delete c;
       return set_error(GCMC_ARG, "engine_share: too many chains for this device");

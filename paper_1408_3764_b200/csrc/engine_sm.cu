@@ -1183,8 +1183,14 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
 
 }  // namespace
 
+// engine_mode 2, or 0 (auto) when at least kSmShare chains share the device:
+// from there a CTA per chain beats 1/K of the device per chain (64k sweep:
+// K = 8 engine2 10.2 M moves/s vs 9.2 M here, K = 16+ this engine,
+// profiles/r02sm).
+constexpr int kSmShare = 12;
 bool engine_sm_supported(const Chain& c) {
-  if (c.params.engine_mode != 2) return false;
+  if (c.params.engine_mode != 2 && !(c.params.engine_mode == 0 && c.params.engine_share >= kSmShare))
+    return false;
   if (c.params.max_displacement > 0.0) return false;
   if (c.grid.kind == GCMC_ALL_PAIRS) return false;
   return c.capn < (1ull << 31);
