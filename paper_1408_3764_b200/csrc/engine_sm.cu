@@ -17,8 +17,7 @@
 //             e[pid], ΔU, the acceptance test and the overflow test (the
 //             maintained-energy form of engine2.cu: displace ΔU = S(n) -
 //             pair(n, x_pid) - e[pid], insert ΔU = S(n), delete ΔU = -e[pid]);
-//   walk      every warp walks the slots in move order tracking d (ballots;
-//             the same result in every warp, so no barrier follows);
+//   walk      one warp walks the slots in move order tracking d (ballots);
 //   verify    each warp checks its slots against the earlier accepted moves:
 //             a consumed move that read anything an earlier accepted move of
 //             the round changes (its particle index, its target brick / cell,
@@ -85,6 +84,7 @@ struct SmArgs {
   double tail_cu, tail_cp, tail_s3, tail_bu, tail_bp;
   int smem_occ;  // mirror occupancy replica in shared memory
   int max_acc;
+  unsigned long long* diag;  // GCMC_SM_PHASES: per-role cycles per round (max over warps)
 };
 
 // A window workspace: bricks, exclusive occupancy prefix and the expanded
@@ -92,6 +92,7 @@ struct SmArgs {
 // shared memory left to L1 keeps the call frames cached).
 struct SWs {
   uint32_t brick[kMaxEnt];
+  uint8_t sc[kMaxEnt];  // periodic image of each brick: 2 bits per axis (0: none, 1: +L, 2: -L)
   int pre[kMaxEnt + 1];
   uint16_t cand[kSCand];
   int nent0, nent, total;
@@ -108,13 +109,15 @@ struct SmShared {
   Proposal ring[kSRing];
   // evaluation results per slot and N offset
   double off_du[kSM][kSOff], off_dw[kSM][kSOff], off_mu[kSM][kSOff], off_mw[kSM][kSOff];
-  double off_pe[kSM][kSOff];
-  double off_x[kSM][kSOff][3];  // position of the offset's particle
+  float off_x[kSM][kSOff][3];   // position of the offset's particle (conflict tests; exact: the store)
+  int32_t off_ia[kSM][kSOff];   // the offset's particle (insert: the new index), -1: none
+  uint32_t off_po[kSM][kSOff];  // brick point of its position (kNoPoint: none)
+  int32_t off_co[kSM][kSOff];   // reference cell of its position
   uint32_t macc[kSM], movf[kSM];
   uint32_t ptn[kSM];            // brick point of the new position (kNoPoint: deletion)
   int32_t cn[kSM];              // reference cell of the new position
   uint8_t mkind[kSM];
-  WalkRes wr[kSW];
+  WalkRes wr[1];
   int cmin;
   // structural commits
   MoveData md[kSAcc];
@@ -136,6 +139,7 @@ struct SmShared {
   unsigned long long stops[6];
   uint64_t base, n;  // the round's first move and N
   uint64_t nprev;    // N at the start of the previous round (error report)
+  unsigned long long rmax[16], racc[16];  // diagnostics: role cycles (round max, sum)
 };
 
 enum SStop { kSEnd, kSRange, kSVerify, kSFull, kSOverflow };
@@ -219,6 +223,50 @@ __device__ __forceinline__ int cand_record(const Mirror& m, const SWs& ws, int f
   return (int)ws.brick[e] * m.cap + k;
 }
 
+// Image code of the brick at window offset o (0..26) around brick point
+// (cx, cy, cz): per axis whether the neighbour wraps (+L: beyond the upper
+// face, -L: below 0). With dims >= 5 the minimum-image shift of every record
+// in that brick relative to any point of the centre brick is exactly that
+// (|dx| <= 2 L / dims < L / 2 inside, >= L - 2 L / dims > L / 2 wrapped), so
+// rint(dx / L) of box.hpp:45-55 is known without computing it.
+__device__ __forceinline__ uint8_t image_code(int cx, int cy, int cz, int o, int d) {
+  const int x = cx + o % 3 - 1, y = cy + (o / 3) % 3 - 1, z = cz + o / 9 - 1;
+  return (uint8_t)((x < 0 ? 2 : (x >= d ? 1 : 0)) | ((y < 0 ? 2 : (y >= d ? 1 : 0)) << 2) |
+                   ((z < 0 ? 2 : (z >= d ? 1 : 0)) << 4));
+}
+__device__ __forceinline__ double image_shift(unsigned c, double l) {
+  return c == 0u ? 0.0 : (c == 1u ? l : -l);
+}
+// min_image_dist2 (common.cuh) with the image known: the same operations and
+// roundings (dx - L * rint(dx / L) with rint = 0 / +1 / -1 is dx - 0 / L / -L).
+__device__ __forceinline__ double image_dist2(double ax, double ay, double az, double bx, double by,
+                                              double bz, unsigned code, double l) {
+  const double dx = __dsub_rn(__dsub_rn(ax, bx), image_shift(code & 3u, l));
+  const double dy = __dsub_rn(__dsub_rn(ay, by), image_shift((code >> 2) & 3u, l));
+  const double dz = __dsub_rn(__dsub_rn(az, bz), image_shift((code >> 4) & 3u, l));
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+// The pair distance of a window candidate: known image when dims >= 5.
+__device__ __forceinline__ double cand_dist2(const Mirror& m, const Box& b, const SWs& ws, int e, double px,
+                                             double py, double pz, double rx, double ry, double rz) {
+  return m.dims >= 5 ? image_dist2(px, py, pz, rx, ry, rz, ws.sc[e], b.l)
+                     : min_image_dist2(px, py, pz, rx, ry, rz, b);
+}
+
+// engine.hpp:28-59 with one exponential (same operation order): the exchange
+// ratio's prefactor for N = nd, then the acceptance probability of ΔU.
+__device__ __forceinline__ double exchange_prefactor(const SmArgs& a, int kind, int64_t nd) {
+  const double nn = (double)nd;
+  return kind == 1 ? __ddiv_rn(a.vol, __dmul_rn(a.lambda3, __dadd_rn(nn, 1.0)))
+                   : (kind == 2 ? __ddiv_rn(__dmul_rn(a.lambda3, nn), a.vol) : 1.0);
+}
+__device__ __forceinline__ double accept_prob(const SmArgs& a, int kind, double du, double fpre) {
+  const double x = kind == 0 ? __dmul_rn(-a.beta, du)
+                 : (kind == 1 ? __dmul_rn(a.beta, __dsub_rn(a.mu, du)) : __dmul_rn(-a.beta, __dadd_rn(a.mu, du)));
+  const double ex = exp(x);
+  return metropolis(kind == 0 ? ex : __dmul_rn(fpre, ex));
+}
+
 // ------------------------------------------------------------- evaluation
 // Half-warp window of point (x, y, z): the pruned 3x3x3 brick window (from
 // the proposal's precomputed offset mask when present), occupancies and the
@@ -265,8 +313,9 @@ __device__ __forceinline__ void half_window(const SmArgs& a, SWs& ws, const uint
         cy -= cy >= d ? d : 0;
         cz += cz < 0 ? d : 0;
         cz -= cz >= d ? d : 0;
-        ws.brick[__popc(wm & ((1u << o) - 1u))] =
-            (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
+        const int at = __popc(wm & ((1u << o) - 1u));
+        ws.brick[at] = (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
+        ws.sc[at] = image_code(pt_x(bpt), pt_y(bpt), pt_z(bpt), o, d);
       }
     }
   }
@@ -308,11 +357,9 @@ __device__ __forceinline__ void half_window(const SmArgs& a, SWs& ws, const uint
   __syncwarp();
 }
 
-// Half-warp Σ pair(p, record) over the workspace's candidates except record
-// `excl`: four candidates per lane in flight, lane sums then an xor tree
-// inside the half (fixed order: every lane of the half gets the same bits).
-__device__ __forceinline__ void half_sum(const Mirror& m, const Box& b, const SWs& ws, double px, double py,
-                                         double pz, int excl, bool on, int hl, double& su, double& sw) {
+template <bool kImg>
+__device__ __forceinline__ void half_sum_t(const Mirror& m, const Box& b, const SWs& ws, double px, double py,
+                                           double pz, int excl, bool on, int hl, double& su, double& sw) {
   su = 0.0;
   sw = 0.0;
   const int total = on ? ws.total : 0;
@@ -321,13 +368,15 @@ __device__ __forceinline__ void half_sum(const Mirror& m, const Box& b, const SW
   for (int base = 0; base < tmax; base += 64) {
     double rx[4], ry[4], rz[4];
     bool ok[4];
+    int ent[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int f = base + 16 * u + hl;
       ok[u] = f < total;
       rx[u] = ry[u] = rz[u] = 0.0;
+      ent[u] = 0;
       if (ok[u]) {
-        const int idx = cand_record(m, ws, f);
+        const int idx = cand_record(m, ws, f, &ent[u]);
         if (idx == excl) {
           ok[u] = false;
         } else {
@@ -337,12 +386,23 @@ __device__ __forceinline__ void half_sum(const Mirror& m, const Box& b, const SW
         }
       }
     }
+    // branch-free: the four pair chains interleave (a term outside r_c adds
+    // +0.0, which leaves the sum's bits unchanged)
+    double pu[4], pw[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (ok[u]) {
-        const double r2 = min_image_dist2(px, py, pz, rx[u], ry[u], rz[u], b);
-        if (r2 <= b.rc2) lj_accum(b, r2, 1.0, su, sw);
-      }
+      const double r2 = kImg ? image_dist2(px, py, pz, rx[u], ry[u], rz[u], ws.sc[ent[u]], b.l)
+                             : min_image_dist2(px, py, pz, rx[u], ry[u], rz[u], b);
+      const bool in = ok[u] && r2 <= b.rc2;
+      double tu, tw;
+      lj_pair_clamped(in ? r2 : b.rc2, b, tu, tw);
+      pu[u] = in ? tu : 0.0;
+      pw[u] = in ? tw : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      su = __dadd_rn(su, pu[u]);
+      sw = __dadd_rn(sw, pw[u]);
     }
   }
 #pragma unroll
@@ -352,9 +412,31 @@ __device__ __forceinline__ void half_sum(const Mirror& m, const Box& b, const SW
   }
 }
 
+// Half-warp Σ pair(p, record) over the workspace's candidates except record
+// `excl`: four candidates per lane in flight, lane sums then an xor tree
+// inside the half (fixed order: every lane of the half gets the same bits).
+__device__ __forceinline__ void half_sum(const Mirror& m, const Box& b, const SWs& ws, double px, double py,
+                                         double pz, int excl, bool on, int hl, double& su, double& sw) {
+  if (m.dims >= 5)
+    half_sum_t<true>(m, b, ws, px, py, pz, excl, on, hl, su, sw);
+  else
+    half_sum_t<false>(m, b, ws, px, py, pz, excl, on, hl, su, sw);
+}
+
 // Two slots per warp call: half hw evaluates slot s0 + kSW * hw.
 __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const uint8_t* occ_s, int s0,
                                           int fit, uint64_t base, uint64_t n, int warp, int lane) {
+  // diagnostics build (-DGCMC_SM_STEPS): cycles of the steps, max over warps
+  unsigned long long tq = clock64();
+  auto step = [&](int k) {
+#ifdef GCMC_SM_STEPS
+    const unsigned long long t = clock64();
+    if (lane == 0) atomicMax(&sh.rmax[k], t - tq);
+    tq = t;
+#else
+    (void)k;
+#endif
+  };
   const int hw = lane >> 4, hl = lane & 15;
   const int s = s0 + kSW * hw;
   const bool on = s < fit;
@@ -381,9 +463,8 @@ __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const u
       ew = e2.y;
     }
   }
-  const double nn = (double)nd;
-  const double fpre = kind == 1 ? __ddiv_rn(a.vol, __dmul_rn(a.lambda3, __dadd_rn(nn, 1.0)))
-                                : (kind == 2 ? __ddiv_rn(__dmul_rn(a.lambda3, nn), a.vol) : 1.0);
+  const double fpre = exchange_prefactor(a, kind, nd);
+  step(9);
   SWs& ws = sh.ws[warp][hw];
   const bool win = on && kind != 2;
   uint32_t pn = (uint32_t)kNoPoint;
@@ -395,8 +476,10 @@ __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const u
     if (grid) ocb = __ldcg(a.g.occ + cb);
   }
   half_window(a, ws, occ_s, pr, win, hl, hw);
+  step(10);
   double su = 0.0, sw = 0.0;
   half_sum(a.m, a.b, ws, pr.x, pr.y, pr.z, -1, win, hl, su, sw);
+  step(11);
   if (win && hl == 0) atomicAdd(&sh.pairs, (unsigned long long)ws.total);
   double du = 0.0, dw = 0.0, mu_ = 0.0, mw = 0.0, p = 0.0;
   bool slow = false;
@@ -436,14 +519,12 @@ __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const u
     du = __dsub_rn(mu_, eu);
     dw = __dsub_rn(mw, ew);
   }
-  {  // engine.hpp:28-59 with one exponential (same operation order)
-    const double x = kind == 0 ? __dmul_rn(-a.beta, du)
-                   : (kind == 1 ? __dmul_rn(a.beta, __dsub_rn(a.mu, du))
-                                : __dmul_rn(-a.beta, __dadd_rn(a.mu, du)));
-    const double ex = exp(x);
-    if (valid) p = metropolis(kind == 0 ? ex : __dmul_rn(fpre, ex));
+  {
+    const double pp = accept_prob(a, kind, du, fpre);
+    if (valid) p = pp;
   }
   const bool acc = valid && pr.acc < p;
+  step(12);
   // overflow of the commit (exact: occupancies before the round)
   bool ovf = false;
   if (valid && kind != 2) {
@@ -461,10 +542,13 @@ __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const u
     sh.off_dw[s][hl] = dw;
     sh.off_mu[s][hl] = mu_;
     sh.off_mw[s][hl] = mw;
-    sh.off_pe[s][hl] = valid ? p : 0.0;
-    sh.off_x[s][hl][0] = xox;
-    sh.off_x[s][hl][1] = xoy;
-    sh.off_x[s][hl][2] = xoz;
+    sh.off_x[s][hl][0] = (float)xox;
+    sh.off_x[s][hl][1] = (float)xoy;
+    sh.off_x[s][hl][2] = (float)xoz;
+    const bool has_x = kind != 1 && nd >= 1 && pid < a.capn;
+    sh.off_ia[s][hl] = kind == 1 ? (int32_t)nd : (nd >= 1 ? (int32_t)pid : -1);
+    sh.off_po[s][hl] = has_x ? (uint32_t)mpoint(a.m, xox, xoy, xoz) : (uint32_t)kNoPoint;
+    sh.off_co[s][hl] = has_x && grid ? cell_of(a.g, xox, xoy, xoz) : -1;
     if (hl == 0) {
       sh.macc[s] = accm;
       sh.movf[s] = ovm;
@@ -473,14 +557,15 @@ __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const u
       sh.cn[s] = cb;
     }
   }
+  step(13);
   __syncwarp();
 }
 
 // ------------------------------------------------------------- walk
 // Moves in order tracking the N offset d; stops at a move whose d is outside
 // the evaluated range, at an accepted move whose commit would overflow, or
-// after max_acc accepts. Two ballots per 64 moves plus two per event. Every
-// warp runs it (same inputs, same result) into its own WalkRes.
+// after max_acc accepts. Two ballots per 64 moves plus two per event (one
+// warp; the others wait at the barrier after it).
 __device__ __forceinline__ void walk(const SmArgs& a, const SmShared& sh, WalkRes& W, int fit, int lane) {
   int d = 0, start = 0, nacc = 0, len = fit, err = 0, why = kSEnd;
   const int i0 = lane, i1 = lane + 32;
@@ -566,26 +651,15 @@ __device__ __forceinline__ RW rw_of(const SmArgs& a, const SmShared& sh, uint64_
   r.nx = pr.x;
   r.ny = pr.y;
   r.nz = pr.z;
-  r.ia = r.ib = -1;
-  r.po = (uint32_t)kNoPoint;
-  r.co = -1;
-  r.ox = r.oy = r.oz = 0.0;
+  const int o = d + kSHalf;
   const int64_t nd = (int64_t)n + d;
-  if (r.kind == 1) {
-    r.ia = (int32_t)nd;
-  } else if (nd >= 1) {
-    const uint64_t pid = index_from(pr.pick, (uint64_t)nd);
-    r.ia = (int32_t)pid;
-    r.ib = r.kind == 2 ? (int32_t)(nd - 1) : -1;
-    if (pid < a.capn) {
-      const double* x = sh.off_x[i][d + kSHalf];
-      r.ox = x[0];
-      r.oy = x[1];
-      r.oz = x[2];
-      r.po = (uint32_t)mpoint(a.m, r.ox, r.oy, r.oz);
-      r.co = grid_on(a) ? cell_of(a.g, r.ox, r.oy, r.oz) : -1;
-    }
-  }
+  r.ia = sh.off_ia[i][o];
+  r.ib = r.kind == 2 && nd >= 1 ? (int32_t)(nd - 1) : -1;
+  r.po = sh.off_po[i][o];
+  r.co = sh.off_co[i][o];
+  r.ox = sh.off_x[i][o][0];
+  r.oy = sh.off_x[i][o][1];
+  r.oz = sh.off_x[i][o][2];
   return r;
 }
 
@@ -595,8 +669,8 @@ __device__ __forceinline__ bool near_rc(const Box& b, double ax, double ay, doub
 }
 
 // Does consumed slot i read anything accepted slot j (< i) changed, or (i
-// accepted) lie within 2 r_c of it? Brick filters first, exact distances
-// decide (1e-9 relative margin).
+// accepted) lie within 2 r_c of it? Brick filters first, then distances with
+// a margin (conservative: a false conflict only ends the round early).
 __device__ __forceinline__ bool conflicts(const SmArgs& a, const RW& I, const RW& J, bool i_acc) {
   const bool grid = grid_on(a);
   if (I.kind != 1 && I.ia >= 0 && (I.ia == J.ia || I.ia == J.ib)) return true;
@@ -607,7 +681,10 @@ __device__ __forceinline__ bool conflicts(const SmArgs& a, const RW& I, const RW
     if (ao != kNP && (lb == mbrick(a.m, ao) || (grid && I.cn == J.co))) return true;
     if (an != kNP && (lb == mbrick(a.m, an) || (grid && I.cn == J.cn))) return true;
   }
-  const double lim1 = a.b.rc2 * (1.0 + 1e-9);
+  // the particles' positions are single-precision copies here: every
+  // distance gets a margin of 4e-7 L (two roundings of <= 6e-8 L per axis)
+  const double eps = 4e-7 * a.b.l;
+  const double lim1 = (a.b.rc + eps) * (a.b.rc + eps);
   if (ln != kNP) {
     if (ao != kNP && mnear(a.m, ln, ao) && near_rc(a.b, I.nx, I.ny, I.nz, J.ox, J.oy, J.oz, lim1)) return true;
     if (an != kNP && mnear(a.m, ln, an) && near_rc(a.b, I.nx, I.ny, I.nz, J.nx, J.ny, J.nz, lim1)) return true;
@@ -617,7 +694,7 @@ __device__ __forceinline__ bool conflicts(const SmArgs& a, const RW& I, const RW
     if (an != kNP && mnear(a.m, lo, an) && near_rc(a.b, I.ox, I.oy, I.oz, J.nx, J.ny, J.nz, lim1)) return true;
   }
   if (i_acc) {  // two accepted moves: every changed point more than 2 r_c apart
-    const double lim2 = __dmul_rn(4.0, a.b.rc2) * (1.0 + 1e-9);
+    const double lim2 = (2.0 * a.b.rc + eps) * (2.0 * a.b.rc + eps);
     const int dm = a.m.dims;
     auto far = [&](uint32_t p, double px, double py, double pz, uint32_t q, double qx, double qy, double qz) {
       if (p == kNP || q == kNP) return true;
@@ -652,6 +729,41 @@ __device__ __forceinline__ void verify(const SmArgs& a, SmShared& sh, const Walk
 }
 
 // ------------------------------------------------------------- commits
+// One warp: the pruned 3x3x3 brick window of (x, y, z) appended at entry `at`
+// of ws (bricks and image codes; wmask / bpt: the proposal's precomputed
+// window, kNoMask: compute it). Returns the number of entries added.
+__device__ __forceinline__ int warp_window(const SmArgs& a, SWs& ws, int at, double x, double y, double z,
+                                          uint32_t wmask, uint32_t bpt, int lane) {
+  const Mirror& m = a.m;
+  if (m.dims < 3) {
+    if (lane < (int)m.nb) {
+      ws.brick[at + lane] = (uint32_t)lane;
+      ws.sc[at + lane] = 0;
+    }
+    return (int)m.nb;
+  }
+  if (wmask == kNoMask) {
+    bpt = (uint32_t)mpoint(m, x, y, z);
+    uint32_t id;
+    const bool keep = lane < 27 && window_keep(m, a.b, x, y, z, pt_x(bpt), pt_y(bpt), pt_z(bpt), lane, id);
+    wmask = __ballot_sync(0xffffffffu, keep);
+  }
+  if (lane < 27 && ((wmask >> lane) & 1u)) {
+    const int d = m.dims;
+    int cx = pt_x(bpt) + lane % 3 - 1, cy = pt_y(bpt) + (lane / 3) % 3 - 1, cz = pt_z(bpt) + lane / 9 - 1;
+    cx += cx < 0 ? d : 0;
+    cx -= cx >= d ? d : 0;
+    cy += cy < 0 ? d : 0;
+    cy -= cy >= d ? d : 0;
+    cz += cz < 0 ? d : 0;
+    cz -= cz >= d ? d : 0;
+    const int e = at + __popc(wmask & ((1u << lane) - 1u));
+    ws.brick[e] = (uint32_t)cx + (uint32_t)d * ((uint32_t)cy + (uint32_t)d * (uint32_t)cz);
+    ws.sc[e] = image_code(pt_x(bpt), pt_y(bpt), pt_z(bpt), lane, d);
+  }
+  return __popc(wmask);
+}
+
 // Neighbour energy updates of accepted move k (one warp): e_j -= pair(old,
 // x_j) for the neighbours of the old position, then e_j += pair(new, x_j) for
 // those of the new one, found on the state before the round's commits (the
@@ -664,15 +776,18 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
   const int i = W.acc_i[k];
   const int kind = sh.mkind[i];
   const Proposal& pr = sh.ring[(base + (uint64_t)i) % kSRing];
-  const double* xo = sh.off_x[i][W.acc_d[k] + kSHalf];
-  const double ox = xo[0], oy = xo[1], oz = xo[2];
+  double ox = 0.0, oy = 0.0, oz = 0.0;
+  if (kind != 1) {  // the mover's exact position (unchanged since the round began)
+    const double4 o = ld_cg(a.s.pos + sh.off_ia[i][W.acc_d[k] + kSHalf]);
+    ox = o.x;
+    oy = o.y;
+    oz = o.z;
+  }
   // window 0: old position (-), window 1: new position (+)
   int nent = 0;
-  if (kind != 1) nent = window_bricks_warp(a.m, a.b, ox, oy, oz, ws.brick, lane);
+  if (kind != 1) nent = warp_window(a, ws, 0, ox, oy, oz, kNoMask, 0u, lane);
   const int nent0 = nent;
-  if (kind != 2)
-    nent += pr.wmask != kNoMask ? window_bricks_mask(a.m, pr.wmask, pr.bpt, ws.brick + nent, lane)
-                                : window_bricks_warp(a.m, a.b, pr.x, pr.y, pr.z, ws.brick + nent, lane);
+  if (kind != 2) nent += warp_window(a, ws, nent, pr.x, pr.y, pr.z, pr.wmask, pr.bpt, lane);
   win_finish_s(a.m, ws, occ_s, nent, nent0, lane);
   __syncwarp();
   const int total = ws.total;
@@ -683,6 +798,7 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
     double rx[4], ry[4], rz[4];
     int32_t rid[4];
     bool ok[4], w1[4];
+    int ent[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int f = b0 + 32 * u + lane;
@@ -690,9 +806,11 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
       w1[u] = false;
       rx[u] = ry[u] = rz[u] = 0.0;
       rid[u] = -1;
+      ent[u] = 0;
       if (ok[u]) {
         int e;
         const int idx = cand_record(a.m, ws, f, &e);
+        ent[u] = e;
         w1[u] = e >= nent0;
         rx[u] = __ldcg(a.m.rx + idx);
         ry[u] = __ldcg(a.m.ry + idx);
@@ -705,8 +823,8 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
       bool hit = false;
       double pu = 0.0, pw = 0.0;
       if (ok[u] && !(kind != 1 && rx[u] == ox && ry[u] == oy && rz[u] == oz)) {  // not the mover
-        const double r2 = w1[u] ? min_image_dist2(pr.x, pr.y, pr.z, rx[u], ry[u], rz[u], a.b)
-                                : min_image_dist2(ox, oy, oz, rx[u], ry[u], rz[u], a.b);
+        const double r2 = w1[u] ? cand_dist2(a.m, a.b, ws, ent[u], pr.x, pr.y, pr.z, rx[u], ry[u], rz[u])
+                                : cand_dist2(a.m, a.b, ws, ent[u], ox, oy, oz, rx[u], ry[u], rz[u]);
         if (r2 <= a.b.rc2) {
           lj_pair_clamped(r2, a.b, pu, pw);
           hit = true;
@@ -743,7 +861,7 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
       if (e < nent0) continue;
       const double rx = __ldcg(a.m.rx + idx), ry = __ldcg(a.m.ry + idx), rz = __ldcg(a.m.rz + idx);
       if (kind != 1 && rx == ox && ry == oy && rz == oz) continue;
-      const double r2 = min_image_dist2(pr.x, pr.y, pr.z, rx, ry, rz, a.b);
+      const double r2 = cand_dist2(a.m, a.b, ws, e, pr.x, pr.y, pr.z, rx, ry, rz);
       if (r2 <= a.b.rc2) {
         double pu, pw;
         lj_pair_clamped(r2, a.b, pu, pw);
@@ -1001,7 +1119,12 @@ __device__ __noinline__ void statistics(const SmArgs& a, SmShared& sh, uint64_t 
       t.accepted = acc;
       t.delta_u = sh.off_du[i][dk];
       t.delta_w = sh.off_dw[i][dk];
-      t.acceptance_prob = sh.off_pe[i][dk];
+      {  // recomputed: the same operations as the evaluation's
+        const int kind = sh.mkind[i];
+        const int64_t nd = (int64_t)n + W.d[i];
+        const bool valid = kind == 1 ? nd >= 0 : nd >= 1;
+        t.acceptance_prob = valid ? accept_prob(a, kind, sh.off_du[i][dk], exchange_prefactor(a, kind, nd)) : 0.0;
+      }
       t.n_after = (uint64_t)((int64_t)n + dn);
       a.trace[base + (uint64_t)i] = t;
     }
@@ -1033,7 +1156,7 @@ __device__ __forceinline__ void ring_load(const SmArgs& a, Proposal* ring, uint6
 // One CTA per chain: the chain's arguments by value (one chain) or from a
 // device list indexed by blockIdx.x (K chains in one launch).
 template <bool kMulti>
-__global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs* __restrict__ list) {
+__global__ void __launch_bounds__(kST, kST <= 256 ? 2 : 1) k_engine_sm(SmArgs args, const SmArgs* __restrict__ list) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ SmArgs a;
   auto& sh = *reinterpret_cast<SmShared*>(smem);
@@ -1049,6 +1172,7 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
     sh.ks = *a.st;
     sh.pairs = 0;
     for (int k = 0; k < 6; ++k) sh.stops[k] = 0;
+    for (int k = 0; k < 16; ++k) sh.rmax[k] = sh.racc[k] = 0;
     sh.base = 0;
     sh.n = a.st->n;
     sh.cmin = kSM;
@@ -1067,31 +1191,55 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
     }
   };
   bool stop = false;
+  // role timers (diagnostics): lane 0 of each warp, max over warps per round
+  const bool dg = a.diag != nullptr;
+  unsigned long long rt0 = 0;
+  auto role_start = [&]() {
+    if (dg) rt0 = clock64();
+  };
+  auto role_end = [&](int k) {
+    if (dg && lane == 0) atomicMax(&sh.rmax[k], clock64() - rt0);
+    if (dg) rt0 = clock64();
+  };
   for (;;) {
     __syncthreads();
+    if (dg && tid == 0)
+      for (int k = 0; k < 16; ++k) {
+        sh.racc[k] += sh.rmax[k];
+        sh.rmax[k] = 0;
+      }
     const uint64_t base = sh.base, n = sh.n;
     const int fit = base >= a.nmoves ? 0 : (a.nmoves - base < (uint64_t)kSM ? (int)(a.nmoves - base) : kSM);
     if (fit == 0 || stop) break;
     mark(0);
     // ---- evaluate (two slots per call: half-warps)
+    role_start();
 #pragma unroll 1
     for (int s0 = warp; s0 < kSM; s0 += 2 * kSW) eval_pair(a, sh, occ_s, s0, fit, base, n, warp, lane);
+    role_end(0);
     __syncthreads();
     mark(1);
     // ---- walk (every warp) and verify (this warp's slots)
-    WalkRes& W = sh.wr[warp];
-    walk(a, sh, W, fit, lane);
+    WalkRes& W = sh.wr[0];
+    role_start();
+    if (warp == 0) walk(a, sh, W, fit, lane);
+    role_end(1);
+    __syncthreads();
     verify(a, sh, W, base, n, warp, lane);
+    role_end(2);
     __syncthreads();
     mark(2);
     const RoundOut ro = round_out(sh);
     const int len = ro.len, nacc = ro.nacc;
     // ---- commits, part 1: neighbour energy updates, structural loads; the
     // ring's next proposals and the statistics
+    role_start();
     if (warp < kEW) {
       for (int k = warp; k < nacc; k += kEW) energy_updates(a, sh, occ_s, base, k, warp, lane);
+      role_end(3);
     } else if (warp == kCW) {
       commit_loads(a, sh, base, n, nacc, lane);
+      role_end(4);
     } else {
       const uint64_t nbase = base + (uint64_t)len;
       const uint64_t want = nbase + kSAhead < a.nmoves ? nbase + kSAhead : a.nmoves;
@@ -1099,7 +1247,9 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
         ring_load(a, sh.ring, ring_hi, want, lane);
         ring_hi = want;
       }
+      role_end(5);
       statistics(a, sh, base, n, len, nacc, lane);
+      role_end(6);
       if (lane == 0) {
         ++sh.stops[sh.cmin < sh.wr[0].len ? (int)kSVerify : sh.wr[0].why];
       }
@@ -1107,8 +1257,10 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
     __syncthreads();  // the round's e updates and every mirror read happen-before the stores
     mark(3);
     // ---- commits, part 2: structural stores, the movers' e, the replica
+    role_start();
     if (warp == kCW) {
       commit_stores(a, sh, base, n, nacc, lane);
+      role_end(7);
     } else if (warp == kXW) {
       if (occ_s && lane < nacc) {  // replica = the mirror's occupancies after the round
         uint32_t* occ_w = reinterpret_cast<uint32_t*>(occ_s);
@@ -1128,6 +1280,7 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
         sh.nprev = n;
         sh.cmin = kSM;
       }
+      role_end(8);
     }
     stop = ro.err != 0;
     ++rounds;
@@ -1155,6 +1308,8 @@ __global__ void __launch_bounds__(kST, 1) k_engine_sm(SmArgs args, const SmArgs*
     a.st->pair_evals += sh.pairs;
     for (int k = 0; k < 5; ++k) a.st->pad[k] = ph[k];
     a.st->pad[8] = rounds;
+    if (a.diag)
+      for (int k = 0; k < 16; ++k) a.diag[k] = sh.racc[k];
     if (stop) {  // overflow at move `base` (slot len of the last round)
       const WalkRes& W = sh.wr[0];
       const int i = W.len;
@@ -1237,13 +1392,17 @@ SmArgs make_args(const Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d) {
 // the SM's shared memory stays L1 (the call frames live there).
 gcmc_status smem_plan(Chain* const* cs, int k, SmArgs* as, size_t& smem) {
   smem = (sizeof(SmShared) + 15) & ~size_t(15);
-  int max_optin = 0;
+  int max_optin = 0, per_sm = 0;
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cs[0]->device);
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cs[0]->device);
   max_optin -= 1024;  // the static shared arguments
+  // 256-thread build: two CTAs (chains) per SM, each within half the SM's
+  // shared memory; 512 threads: one, with a third of it left to L1
+  const size_t budget = kST <= 256 ? (size_t)per_sm / 2 - 2048 : (size_t)max_optin * 2 / 3;
   size_t occ = 0;
   for (int i = 0; i < k; ++i) {
     const size_t nb = ((size_t)cs[i]->mirror.nb + 15) & ~size_t(15);
-    as[i].smem_occ = smem + nb <= (size_t)max_optin * 2 / 3 ? 1 : 0;
+    as[i].smem_occ = smem + nb <= budget ? 1 : 0;
     if (as[i].smem_occ) occ = occ > nb ? occ : nb;
   }
   smem += occ;
@@ -1262,6 +1421,10 @@ gcmc_status engine_sm_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cu
     c.e_valid = true;
   }
   SmArgs a = make_args(c, nmoves, trace_d);
+  static thread_local unsigned long long* diag = nullptr;
+  const bool want_diag = std::getenv("GCMC_SM_PHASES") != nullptr;
+  if (want_diag && !diag && cudaMalloc(&diag, 16 * sizeof(unsigned long long)) != cudaSuccess) diag = nullptr;
+  if (want_diag) a.diag = diag;
   Chain* cp = &c;
   size_t smem = 0;
   gcmc_status st = smem_plan(&cp, 1, &a, smem);
@@ -1280,6 +1443,16 @@ gcmc_status engine_sm_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cu
                    "walk+verify %.0f commit1 %.0f commit2 %.0f\n",
                    smem, (unsigned long long)h.pad[8], h.moves_done / r, h.pad[0] / r, h.pad[1] / r,
                    h.pad[2] / r, h.pad[3] / r, h.pad[4] / r);
+      unsigned long long d[16];
+      if (diag && cudaMemcpy(d, diag, sizeof d, cudaMemcpyDeviceToHost) == cudaSuccess)
+        std::fprintf(stderr,
+                     "[engine_sm] role cycles/round (max over warps): eval %.0f walk %.0f verify %.0f "
+                     "e-updates %.0f commit_loads %.0f ring %.0f statistics %.0f commit_stores %.0f "
+                     "close %.0f\n",
+                     d[0] / r, d[1] / r, d[2] / r, d[3] / r, d[4] / r, d[5] / r, d[6] / r, d[7] / r, d[8] / r);
+      if (diag && cudaMemcpy(d, diag, sizeof d, cudaMemcpyDeviceToHost) == cudaSuccess)
+        std::fprintf(stderr, "[engine_sm] eval_pair steps (sum of max per call): setup %.0f window %.0f sum %.0f offsets %.0f store %.0f\n",
+                     d[9] / r, d[10] / r, d[11] / r, d[12] / r, d[13] / r);
     }
   }
   return GCMC_OK;
