@@ -1013,9 +1013,10 @@ gcmc_status gcmc_run_moves(gcmc_dev* h, uint64_t n, gcmc_trace_rec* trace, gcmc_
 
 // K chain-per-SM chains on one device in ONE launch per chunk (one CTA per
 // chain): separate launches from separate streams serialise once the streams
-// outnumber the device's hardware queues. Proposals are generated per chain
-// (the next chunk's during this one's engine launch); a chain whose mirror
-// overflows mid-chunk finishes that chunk on its own launches.
+// outnumber the device's hardware queues. The chunk's proposals of every
+// chain are generated in one launch too (one CTA per chain) before it; a
+// chain whose mirror overflows mid-chunk finishes that chunk on its own
+// launches.
 gcmc_status run_chains_sm(const std::vector<Chain*>& cs, const uint64_t* n, gcmc_run_result* out) {
   const int k = (int)cs.size();
   const uint64_t kChunk = 1ull << 21;
@@ -1038,22 +1039,40 @@ gcmc_status run_chains_sm(const std::vector<Chain*>& cs, const uint64_t* n, gcmc
     std::vector<int> idx;
     for (int i = 0; i < k; ++i) {
       if (done[i] >= n[i]) continue;
-      Chain& c = *cs[i];
       m[i] = std::min(cap[i], n[i] - done[i]);
-      const uint64_t left = n[i] - done[i] - m[i];
-      if ((s = props_next_chunk(c, m[i], left ? std::min(cap[i], left) : m[i]))) return s;
-      if ((s = ensure_store(c, m[i]))) return s;
+      run.push_back(cs[i]);
+      rm.push_back(m[i]);
+      idx.push_back(i);
+    }
+    if (run.empty()) break;
+    // this chunk's proposals: every chain's in one launch (a look-ahead batch
+    // left by gcmc_run_moves is used when it has the right size)
+    CK(cudaEventRecord(c0.ev[0], c0.stream), "event");
+    std::vector<Chain*> gen;
+    std::vector<uint64_t> gm;
+    for (size_t q = 0; q < run.size(); ++q) {
+      Chain& c = *run[q];
+      CK(cudaStreamWaitEvent(c0.stream, c.ev_ahead, 0), "ahead");
+      if (c.ahead_n == rm[q]) {
+        std::swap(c.props, c.props_next);
+        std::swap(c.mt, c.mt_next);
+      } else {
+        gen.push_back(&c);
+        gm.push_back(rm[q]);
+      }
+      c.ahead_n = 0;
+    }
+    if ((s = gen_proposals_many(gen.data(), (int)gen.size(), gm.data(), c0.stream))) return s;
+    for (size_t q = 0; q < run.size(); ++q) {
+      Chain& c = *run[q];
+      if ((s = ensure_store(c, rm[q]))) return s;
       if (!c.e_valid) {
         if ((s = epart_build(c, c.ep))) return s;
         c.e_valid = true;
       }
       CK(cudaEventRecord(c.ev[1], c.stream), "event");
       CK(cudaStreamWaitEvent(c0.stream, c.ev[1], 0), "event");
-      run.push_back(&c);
-      rm.push_back(m[i]);
-      idx.push_back(i);
     }
-    if (run.empty()) break;
     CK(cudaEventRecord(c0.ev[3], c0.stream), "event");
     if ((s = engine_sm_run_many(run.data(), (int)run.size(), rm.data(), c0.stream))) return s;
     CK(cudaEventRecord(c0.ev[2], c0.stream), "event");
@@ -1065,7 +1084,7 @@ gcmc_status run_chains_sm(const std::vector<Chain*>& cs, const uint64_t* n, gcmc
       Chain& c = *run[q];
       CK(cudaStreamWaitEvent(c.stream, c0.ev[2], 0), "event");
       float a = 0.f;
-      cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+      cudaEventElapsedTime(&a, c0.ev[0], c0.ev[3]);
       gen_ms[i] += a;
       eng_ms[i] += ems;
       if ((s = pull_state(c))) return s;

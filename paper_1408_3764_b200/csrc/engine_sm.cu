@@ -122,6 +122,8 @@ struct SmShared {
   // structural commits
   MoveData md[kSAcc];
   CommitIn cin[kSAcc];
+  int8_t cfwd[kSAcc];   // forwarded deletion: the insertion lane it takes q from (-1: none)
+  uint8_t cskip[kSAcc]; // insertion relabelled away by a forwarded deletion: index n not written
   uint32_t cdep;
   // window workspaces: [warp][half] (evaluation), [warp][0] (energy updates)
   SWs ws[kSW][2];
@@ -884,63 +886,120 @@ __device__ __forceinline__ void mover_of(const SmShared& sh, uint64_t base, uint
   pid = kind == 1 ? 0 : index_from(sh.ring[(base + (uint64_t)i) % kSRing].pick, nn);
 }
 
-// Structural commit loads (lane k = accepted move k) and their order: a
-// commit that touches an earlier one of the round (cell, brick or particle)
-// is re-loaded and applied after it; an insertion that reuses the index an
-// earlier deletion vacated is exempt unless that deletion is itself ordered
-// (its loads then follow the insertion's stores).
+// Structural commit loads (lane k = accepted move k) and their order
+// (engine2.cu:commit_round's rules): a commit that touches an earlier one of
+// the round (cell, brick or particle) is re-loaded and applied after it; an
+// insertion that reuses the index an earlier deletion vacated is exempt
+// unless that deletion is itself ordered (its loads then follow the
+// insertion's stores). A deletion whose relabel source q = n - 1 is the
+// particle an earlier insertion of the round created takes q's data
+// (position, reference slot, record) from the insertion's lane instead of
+// waiting for its stores, and is stored after it; that insertion then need
+// not write index n at all (the deletion moves it to pid).
 __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_t base, uint64_t n,
                                           int nacc, int lane) {
   const bool mine = lane < nacc;
   int kind = 0, i = 0;
   uint64_t pid = 0, nn = 0;
   Touch tc{};
+  MoveData md{};
+  CommitIn c{};
   if (mine) {
     mover_of(sh, base, n, lane, i, kind, pid, nn);
     const Proposal& pr = sh.ring[(base + (uint64_t)i) % kSRing];
-    MoveData md{};
     md.nx = pr.x;
     md.ny = pr.y;
     md.nz = pr.z;
     md.rslot_pid = md.bslot_pid = -1;
     load_move(a.s, kind, pid, md);
-    CommitIn c{};
     commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
-    sh.md[lane] = md;
-    sh.cin[lane] = c;
     tc = touch_of(a.m, kind, pid, nn, c);
   }
-  bool dep = false;
-  unsigned exm = 0u;
+  // forwarding
+  int fsrc = -1;
+  {
+    const int64_t myq = (mine && kind == 2 && pid != nn - 1) ? (int64_t)(nn - 1) : -2;
 #pragma unroll 1
-  for (int j = 0; j < nacc - 1; ++j) {
-    Touch tj;
-#pragma unroll
-    for (int x = 0; x < 3; ++x) {
-      tj.cell[x] = __shfl_sync(0xffffffffu, tc.cell[x], j);
-      tj.brick[x] = __shfl_sync(0xffffffffu, tc.brick[x], j);
+    for (int j = 0; j < nacc - 1; ++j) {
+      const int kj = __shfl_sync(0xffffffffu, kind, j);
+      const uint64_t nnj = __shfl_sync(0xffffffffu, nn, j);
+      if (j < lane && kj == 1 && (int64_t)nnj == myq) fsrc = j;
     }
+    const int f = fsrc >= 0 ? fsrc : lane;
+    const double fx = __shfl_sync(0xffffffffu, md.nx, f), fy = __shfl_sync(0xffffffffu, md.ny, f),
+                 fz = __shfl_sync(0xffffffffu, md.nz, f);
+    const int focb = __shfl_sync(0xffffffffu, c.occ_cb, f), fcb = __shfl_sync(0xffffffffu, c.cb, f);
+    const int fbb = __shfl_sync(0xffffffffu, c.bb, f), fobb = __shfl_sync(0xffffffffu, c.occ_bb, f);
+    if (fsrc >= 0) {
+      c.qx = fx;
+      c.qy = fy;
+      c.qz = fz;
+      c.rslot_q = focb;
+      c.bslot_q = fbb * a.m.cap + fobb;
+      c.cl = fcb;
+      tc = touch_of(a.m, kind, pid, nn, c);
+    }
+  }
+  const unsigned fwd_src = __reduce_or_sync(0xffffffffu, (mine && fsrc >= 0) ? (1u << fsrc) : 0u);
+  const bool away = mine && kind == 1 && ((fwd_src >> lane) & 1u);
+  const int chain = (fsrc >= 0 ? 1 : 0) | (away ? 2 : 0);
+  auto order = [&](bool chain_form, bool& dep) {
+    Touch tme = tc;
+    if (chain_form && (chain & 1)) tme.part[1] = -1;
+    if (chain_form && (chain & 2)) tme.part[0] = -1;
+    dep = false;
+    unsigned exm = 0u;
+#pragma unroll 1
+    for (int j = 0; j < nacc - 1; ++j) {
+      Touch tj;
 #pragma unroll
-    for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tc.part[x], j);
-    const int kj = __shfl_sync(0xffffffffu, kind, j);
-    if (mine && j < lane) {
-      Touch tm = tc;
-      if (kind == 1 && kj == 2 && tm.part[0] >= 0 && tm.part[0] == tj.part[1]) {
-        tm.part[0] = -1;
-        exm |= 1u << j;
+      for (int x = 0; x < 3; ++x) {
+        tj.cell[x] = __shfl_sync(0xffffffffu, tme.cell[x], j);
+        tj.brick[x] = __shfl_sync(0xffffffffu, tme.brick[x], j);
       }
-      if (touches(tm, tj)) dep = true;
+#pragma unroll
+      for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tme.part[x], j);
+      const int kj = __shfl_sync(0xffffffffu, kind, j);
+      if (mine && j < lane) {
+        Touch tm = tme;
+        if (kind == 1 && kj == 2 && tm.part[0] >= 0 && tm.part[0] == tj.part[1]) {
+          tm.part[0] = -1;
+          exm |= 1u << j;
+        }
+        if (j == fsrc) {  // the forwarded particle's index, cell and record are expected
+          tm.part[1] = -1;
+          tm.cell[2] = -1;
+          tm.brick[2] = -1;
+        }
+        if (touches(tm, tj)) dep = true;
+      }
     }
-  }
+    // an exempted / forwarded commit is ordered after its partner when the
+    // partner itself is (it then loads or stores late)
 #pragma unroll 1
-  for (int it = 0; it < 32; ++it) {
-    const unsigned b = __ballot_sync(0xffffffffu, dep);
-    const bool nd = dep || (b & exm);
-    if (__ballot_sync(0xffffffffu, nd) == b) break;
-    dep = nd;
-  }
+    for (int it = 0; it < 32; ++it) {
+      const unsigned b = __ballot_sync(0xffffffffu, dep);
+      const bool nd = dep || (b & exm) || (fsrc >= 0 && ((b >> fsrc) & 1u));
+      if (__ballot_sync(0xffffffffu, nd) == b) break;
+      dep = nd;
+    }
+  };
+  bool dep = false;
+  order(true, dep);
+  const bool chains_free = !__any_sync(0xffffffffu, chain != 0 && dep);
+  if (!chains_free) order(false, dep);  // full ordering (rare)
   const unsigned deps = __ballot_sync(0xffffffffu, dep);
+  if (mine) {
+    sh.md[lane] = md;
+    sh.cin[lane] = c;
+    sh.cfwd[lane] = (int8_t)fsrc;
+    sh.cskip[lane] = (uint8_t)(chains_free && away);
+  }
   if (lane == 0) sh.cdep = deps;
+  if (a.diag && lane == 0) {  // diagnostics: ordered commits and commits per round
+    sh.racc[14] += __popc(deps);
+    sh.racc[15] += nacc;
+  }
   __syncwarp();
 }
 
@@ -952,7 +1011,13 @@ __device__ __noinline__ void commit_stores(const SmArgs& a, SmShared& sh, uint64
   uint64_t pid = 0, nn = 0;
   if (mine) mover_of(sh, base, n, lane, i, kind, pid, nn);
   long long e1, e2, e3;
-  if (mine && !((deps >> lane) & 1u))
+  const bool free_ = mine && !((deps >> lane) & 1u);
+  const bool fwd = mine && sh.cfwd[lane] >= 0;
+  if (free_ && !fwd)
+    commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, sh.md[lane], sh.cin[lane], e1, e2, e3,
+                 sh.cskip[lane] != 0);
+  __syncwarp();  // forwarded deletions after their insertions
+  if (free_ && fwd)
     commit_store(a.g, a.m, a.s, &a.st->peak, kind, pid, nn, sh.md[lane], sh.cin[lane], e1, e2, e3);
   if (deps) {
     __syncwarp();
@@ -1451,8 +1516,8 @@ gcmc_status engine_sm_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cu
                      "close %.0f\n",
                      d[0] / r, d[1] / r, d[2] / r, d[3] / r, d[4] / r, d[5] / r, d[6] / r, d[7] / r, d[8] / r);
       if (diag && cudaMemcpy(d, diag, sizeof d, cudaMemcpyDeviceToHost) == cudaSuccess)
-        std::fprintf(stderr, "[engine_sm] eval_pair steps (sum of max per call): setup %.0f window %.0f sum %.0f offsets %.0f store %.0f\n",
-                     d[9] / r, d[10] / r, d[11] / r, d[12] / r, d[13] / r);
+        std::fprintf(stderr, "[engine_sm] eval_pair steps (sum of max per call): setup %.0f window %.0f sum %.0f offsets %.0f store %.0f; commits/round %.2f ordered %.2f\n",
+                     d[9] / r, d[10] / r, d[11] / r, d[12] / r, d[13] / r, d[15] / r, d[14] / r);
     }
   }
   return GCMC_OK;

@@ -19,6 +19,8 @@
 // re-walks and emits.
 #include <cstdlib>
 
+#include <vector>
+
 #include "internal.h"
 #include "mirror.cuh"
 
@@ -90,7 +92,11 @@ __device__ __forceinline__ uint32_t compose6(uint32_t g, uint32_t h) {  // (g o 
   return comp;
 }
 
-__global__ void __launch_bounds__(kThreads) k_gen2(GenArgs a) {
+// One chain per CTA: the arguments by value (one chain) or from a device
+// list indexed by blockIdx.x (K chains in one launch).
+template <bool kMulti>
+__global__ void __launch_bounds__(kThreads) k_gen2(GenArgs one, const GenArgs* __restrict__ list) {
+  const GenArgs a = kMulti ? list[blockIdx.x] : one;
   __shared__ uint64_t rawb[KB + 1][N];  // raw MT words of the iteration's blocks
   __shared__ double dr[KB + 1][N];      // their uniforms
   __shared__ uint32_t s_map[KB];
@@ -275,8 +281,23 @@ __global__ void __launch_bounds__(kThreads) k_gen2(GenArgs a) {
 // window_bricks_warp), its packed brick point and reference-grid cell.
 // Deletions and max_displacement displacements (new position relative to the
 // mover) get kNoMask and are computed in the engine.
-__global__ void __launch_bounds__(256) k_annotate(Proposal* p, uint64_t n, Mirror m, Box b,
-                                                  Grid g, int raw) {
+struct AnnArgs {
+  Proposal* p;
+  uint64_t n;
+  Mirror m;
+  Box b;
+  Grid g;
+  int raw;
+};
+template <bool kMulti>
+__global__ void __launch_bounds__(256) k_annotate(AnnArgs one, const AnnArgs* __restrict__ list) {
+  const AnnArgs& A = kMulti ? list[blockIdx.y] : one;
+  Proposal* const p = A.p;
+  const uint64_t n = A.n;
+  const Mirror m = A.m;
+  const Box b = A.b;
+  const Grid g = A.g;
+  const int raw = A.raw;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     Proposal& q = p[i];
@@ -309,10 +330,42 @@ gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n
   if (n == 0) return GCMC_OK;
   GenArgs a{mt, out, n, c.params.displace_percent, c.box.l,
             c.params.max_displacement > 0.0 ? 1 : 0};
-  k_gen2<<<1, kThreads, 0, s>>>(a);
+  k_gen2<false><<<1, kThreads, 0, s>>>(a, nullptr);
   const unsigned blocks = (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
-  k_annotate<<<blocks, 256, 0, s>>>(out, n, c.mirror, c.box, c.grid, a.raw_disp);
+  k_annotate<false><<<blocks, 256, 0, s>>>(AnnArgs{out, n, c.mirror, c.box, c.grid, a.raw_disp}, nullptr);
   cudaError_t e = cudaGetLastError();
+  if (e) return cuda_error(e, "gen_proposals");
+  return GCMC_OK;
+}
+
+gcmc_status gen_proposals_many(Chain* const* cs, int k, const uint64_t* n, cudaStream_t s) {
+  std::vector<GenArgs> ga;
+  std::vector<AnnArgs> aa;
+  uint64_t nmax = 0;
+  for (int i = 0; i < k; ++i) {
+    if (n[i] == 0) continue;
+    Chain& c = *cs[i];
+    ga.push_back(GenArgs{c.mt, c.props, n[i], c.params.displace_percent, c.box.l,
+                         c.params.max_displacement > 0.0 ? 1 : 0});
+    aa.push_back(AnnArgs{c.props, n[i], c.mirror, c.box, c.grid, ga.back().raw_disp});
+    nmax = n[i] > nmax ? n[i] : nmax;
+  }
+  if (ga.empty()) return GCMC_OK;
+  const int kk = (int)ga.size();
+  void* d = nullptr;
+  const size_t bytes = kk * (sizeof(GenArgs) + sizeof(AnnArgs));
+  cudaError_t e = cudaMallocAsync(&d, bytes, s);
+  if (e) return cuda_error(e, "gen_proposals args");
+  GenArgs* dg = static_cast<GenArgs*>(d);
+  AnnArgs* da = reinterpret_cast<AnnArgs*>(dg + kk);
+  if ((e = cudaMemcpyAsync(dg, ga.data(), kk * sizeof(GenArgs), cudaMemcpyHostToDevice, s)) ||
+      (e = cudaMemcpyAsync(da, aa.data(), kk * sizeof(AnnArgs), cudaMemcpyHostToDevice, s)))
+    return cuda_error(e, "gen_proposals args");
+  k_gen2<true><<<kk, kThreads, 0, s>>>(GenArgs{}, dg);
+  const unsigned blocks = (unsigned)((nmax + 255) / 256 < 64 ? (nmax + 255) / 256 : 64);
+  k_annotate<true><<<dim3(blocks, kk), 256, 0, s>>>(AnnArgs{}, da);
+  e = cudaGetLastError();
+  cudaFreeAsync(d, s);
   if (e) return cuda_error(e, "gen_proposals");
   return GCMC_OK;
 }

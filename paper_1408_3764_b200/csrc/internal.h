@@ -91,6 +91,8 @@ gcmc_status total_energy_bruteforce(Chain& c, double* u, double* w);
 // gen.cu: parse the next `n` moves of the MT stream into c.props[0..n).
 gcmc_status gen_proposals(Chain& c, uint64_t n, cudaStream_t s);
 gcmc_status gen_proposals_into(Chain& c, uint64_t* mt, Proposal* out, uint64_t n, cudaStream_t s);
+// K chains in one launch (one CTA each): c.props[0..n[i]) from c.mt
+gcmc_status gen_proposals_many(Chain* const* cs, int k, const uint64_t* n, cudaStream_t s);
 
 // engine.cu: run n moves from c.props; optional device trace.
 gcmc_status engine_run(Chain& c, uint64_t n, gcmc_trace_rec* trace_d, cudaStream_t s);
