@@ -123,6 +123,11 @@ struct SmShared {
   MoveData md[kSAcc];
   CommitIn cin[kSAcc];
   int8_t cfwd[kSAcc];   // forwarded deletion: the insertion lane it takes q from (-1: none)
+  Touch ctouch[kSAcc];  // commit ordering scratch
+  unsigned cexm[kSAcc], cdepm;
+  int8_t ckind[kSAcc];
+  double4 xacc[kSAcc];  // the accepted movers' store records (exact position, record), loaded in the verify
+  int32_t rsacc[kSAcc]; // ... and reference slots
   uint8_t cskip[kSAcc]; // insertion relabelled away by a forwarded deletion: index n not written
   uint32_t cdep;
   // window workspaces: [warp][half] (evaluation), [warp][0] (energy updates)
@@ -431,7 +436,7 @@ __device__ __forceinline__ void eval_pair(const SmArgs& a, SmShared& sh, const u
   // diagnostics build (-DGCMC_SM_STEPS): cycles of the steps, max over warps
   unsigned long long tq = clock64();
   auto step = [&](int k) {
-#ifdef GCMC_SM_STEPS
+#ifdef GCMC_SM_EVAL_STEPS
     const unsigned long long t = clock64();
     if (lane == 0) atomicMax(&sh.rmax[k], t - tq);
     tq = t;
@@ -770,6 +775,7 @@ __device__ __forceinline__ int warp_window(const SmArgs& a, SWs& ws, int at, dou
 // x_j) for the neighbours of the old position, then e_j += pair(new, x_j) for
 // those of the new one, found on the state before the round's commits (the
 // mover's own record excluded: the one at its old position).
+template <bool kImg>
 __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const uint8_t* occ_s,
                                             uint64_t base, int k, int warp, int lane) {
   SWs& ws = sh.ws[warp][0];
@@ -779,11 +785,10 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
   const int kind = sh.mkind[i];
   const Proposal& pr = sh.ring[(base + (uint64_t)i) % kSRing];
   double ox = 0.0, oy = 0.0, oz = 0.0;
-  if (kind != 1) {  // the mover's exact position (unchanged since the round began)
-    const double4 o = ld_cg(a.s.pos + sh.off_ia[i][W.acc_d[k] + kSHalf]);
-    ox = o.x;
-    oy = o.y;
-    oz = o.z;
+  if (kind != 1) {  // the mover's exact position (loaded during the verify)
+    ox = sh.xacc[k].x;
+    oy = sh.xacc[k].y;
+    oz = sh.xacc[k].z;
   }
   // window 0: old position (-), window 1: new position (+)
   int nent = 0;
@@ -820,18 +825,22 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
         rid[u] = __ldcg(a.m.rid + idx);
       }
     }
+    // branch-free pair chains (interleaved), then the updates
+    bool hits[4];
+    double pus[4], pws[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      bool hit = false;
-      double pu = 0.0, pw = 0.0;
-      if (ok[u] && !(kind != 1 && rx[u] == ox && ry[u] == oy && rz[u] == oz)) {  // not the mover
-        const double r2 = w1[u] ? cand_dist2(a.m, a.b, ws, ent[u], pr.x, pr.y, pr.z, rx[u], ry[u], rz[u])
-                                : cand_dist2(a.m, a.b, ws, ent[u], ox, oy, oz, rx[u], ry[u], rz[u]);
-        if (r2 <= a.b.rc2) {
-          lj_pair_clamped(r2, a.b, pu, pw);
-          hit = true;
-        }
-      }
+      const double cx = w1[u] ? pr.x : ox, cy = w1[u] ? pr.y : oy, cz = w1[u] ? pr.z : oz;
+      const double r2 = kImg ? image_dist2(cx, cy, cz, rx[u], ry[u], rz[u], ws.sc[ent[u]], a.b.l)
+                             : min_image_dist2(cx, cy, cz, rx[u], ry[u], rz[u], a.b);
+      const bool mover = kind != 1 && rx[u] == ox && ry[u] == oy && rz[u] == oz;  // its own record
+      hits[u] = ok[u] && !mover && r2 <= a.b.rc2;
+      lj_pair_clamped(hits[u] ? r2 : a.b.rc2, a.b, pus[u], pws[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool hit = hits[u];
+      const double pu = pus[u], pw = pws[u];
       if (hit && !w1[u]) {  // old window: now
         atomicAdd(&a.ep[rid[u]].x, -pu);
         atomicAdd(&a.ep[rid[u]].y, -pw);
@@ -898,6 +907,16 @@ __device__ __forceinline__ void mover_of(const SmShared& sh, uint64_t base, uint
 // not write index n at all (the deletion moves it to pid).
 __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_t base, uint64_t n,
                                           int nacc, int lane) {
+  unsigned long long tq = clock64();
+  auto step = [&](int k) {
+#ifdef GCMC_SM_STEPS
+    const unsigned long long t = clock64();
+    if (lane == 0) atomicMax(&sh.rmax[k], t - tq);
+    tq = t;
+#else
+    (void)k;
+#endif
+  };
   const bool mine = lane < nacc;
   int kind = 0, i = 0;
   uint64_t pid = 0, nn = 0;
@@ -911,10 +930,19 @@ __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_
     md.ny = pr.y;
     md.nz = pr.z;
     md.rslot_pid = md.bslot_pid = -1;
-    load_move(a.s, kind, pid, md);
+    if (kind != 1) {  // load_move's fields, loaded during the verify
+      const double4 o = sh.xacc[lane];
+      md.ox = o.x;
+      md.oy = o.y;
+      md.oz = o.z;
+      md.rslot_pid = sh.rsacc[lane];
+      md.bslot_pid = bslot_in(o);
+    }
     commit_load(a.g, a.m, a.s, kind, pid, nn, md, c);
     tc = touch_of(a.m, kind, pid, nn, c);
   }
+  __syncwarp();
+  step(9);
   // forwarding
   int fsrc = -1;
   {
@@ -940,40 +968,46 @@ __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_
       tc = touch_of(a.m, kind, pid, nn, c);
     }
   }
+  step(10);
+  if (mine) sh.cfwd[lane] = (int8_t)fsrc;
   const unsigned fwd_src = __reduce_or_sync(0xffffffffu, (mine && fsrc >= 0) ? (1u << fsrc) : 0u);
   const bool away = mine && kind == 1 && ((fwd_src >> lane) & 1u);
   const int chain = (fsrc >= 0 ? 1 : 0) | (away ? 2 : 0);
+  // every (later k, earlier j) pair of the round's commits in parallel over
+  // the lanes, Touches from shared memory
   auto order = [&](bool chain_form, bool& dep) {
     Touch tme = tc;
     if (chain_form && (chain & 1)) tme.part[1] = -1;
     if (chain_form && (chain & 2)) tme.part[0] = -1;
-    dep = false;
-    unsigned exm = 0u;
-#pragma unroll 1
-    for (int j = 0; j < nacc - 1; ++j) {
-      Touch tj;
-#pragma unroll
-      for (int x = 0; x < 3; ++x) {
-        tj.cell[x] = __shfl_sync(0xffffffffu, tme.cell[x], j);
-        tj.brick[x] = __shfl_sync(0xffffffffu, tme.brick[x], j);
-      }
-#pragma unroll
-      for (int x = 0; x < 5; ++x) tj.part[x] = __shfl_sync(0xffffffffu, tme.part[x], j);
-      const int kj = __shfl_sync(0xffffffffu, kind, j);
-      if (mine && j < lane) {
-        Touch tm = tme;
-        if (kind == 1 && kj == 2 && tm.part[0] >= 0 && tm.part[0] == tj.part[1]) {
-          tm.part[0] = -1;
-          exm |= 1u << j;
-        }
-        if (j == fsrc) {  // the forwarded particle's index, cell and record are expected
-          tm.part[1] = -1;
-          tm.cell[2] = -1;
-          tm.brick[2] = -1;
-        }
-        if (touches(tm, tj)) dep = true;
-      }
+    if (mine) {
+      sh.ctouch[lane] = tme;
+      sh.cexm[lane] = 0u;
+      sh.ckind[lane] = (int8_t)kind;
     }
+    if (lane == 0) sh.cdepm = 0u;
+    __syncwarp();
+    const int npairs = nacc * (nacc - 1) / 2;
+    for (int p = lane; p < npairs; p += 32) {
+      int kk = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)p)) * 0.5f);  // p = kk (kk - 1) / 2 + j
+      while (kk * (kk - 1) / 2 > p) --kk;
+      while ((kk + 1) * kk / 2 <= p) ++kk;
+      const int j = p - kk * (kk - 1) / 2;
+      Touch tm = sh.ctouch[kk];
+      const Touch tj = sh.ctouch[j];
+      if (sh.ckind[kk] == 1 && sh.ckind[j] == 2 && tm.part[0] >= 0 && tm.part[0] == tj.part[1]) {
+        tm.part[0] = -1;
+        atomicOr(&sh.cexm[kk], 1u << j);
+      }
+      if (j == sh.cfwd[kk]) {  // the forwarded particle's index, cell and record are expected
+        tm.part[1] = -1;
+        tm.cell[2] = -1;
+        tm.brick[2] = -1;
+      }
+      if (touches(tm, tj)) atomicOr(&sh.cdepm, 1u << kk);
+    }
+    __syncwarp();
+    dep = mine && ((sh.cdepm >> lane) & 1u);
+    const unsigned exm = mine ? sh.cexm[lane] : 0u;
     // an exempted / forwarded commit is ordered after its partner when the
     // partner itself is (it then loads or stores late)
 #pragma unroll 1
@@ -983,16 +1017,18 @@ __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_
       if (__ballot_sync(0xffffffffu, nd) == b) break;
       dep = nd;
     }
+    __syncwarp();
   };
   bool dep = false;
   order(true, dep);
+  step(11);
   const bool chains_free = !__any_sync(0xffffffffu, chain != 0 && dep);
   if (!chains_free) order(false, dep);  // full ordering (rare)
+  step(12);
   const unsigned deps = __ballot_sync(0xffffffffu, dep);
   if (mine) {
     sh.md[lane] = md;
     sh.cin[lane] = c;
-    sh.cfwd[lane] = (int8_t)fsrc;
     sh.cskip[lane] = (uint8_t)(chains_free && away);
   }
   if (lane == 0) sh.cdep = deps;
@@ -1001,6 +1037,7 @@ __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_
     sh.racc[15] += nacc;
   }
   __syncwarp();
+  step(13);
 }
 
 __device__ __noinline__ void commit_stores(const SmArgs& a, SmShared& sh, uint64_t base, uint64_t n,
@@ -1290,6 +1327,14 @@ __global__ void __launch_bounds__(kST, kST <= 256 ? 2 : 1) k_engine_sm(SmArgs ar
     if (warp == 0) walk(a, sh, W, fit, lane);
     role_end(1);
     __syncthreads();
+    if (warp == kXW && lane < W.nacc) {  // the accepted movers' records, ahead of the commits
+      const int i = W.acc_i[lane];
+      if (sh.mkind[i] != 1) {
+        const int32_t pid = sh.off_ia[i][W.acc_d[lane] + kSHalf];
+        sh.xacc[lane] = ld_cg(a.s.pos + pid);
+        sh.rsacc[lane] = __ldcg(a.s.rslot + pid);
+      }
+    }
     verify(a, sh, W, base, n, warp, lane);
     role_end(2);
     __syncthreads();
@@ -1300,7 +1345,12 @@ __global__ void __launch_bounds__(kST, kST <= 256 ? 2 : 1) k_engine_sm(SmArgs ar
     // ring's next proposals and the statistics
     role_start();
     if (warp < kEW) {
-      for (int k = warp; k < nacc; k += kEW) energy_updates(a, sh, occ_s, base, k, warp, lane);
+      for (int k = warp; k < nacc; k += kEW) {
+        if (a.m.dims >= 5)
+          energy_updates<true>(a, sh, occ_s, base, k, warp, lane);
+        else
+          energy_updates<false>(a, sh, occ_s, base, k, warp, lane);
+      }
       role_end(3);
     } else if (warp == kCW) {
       commit_loads(a, sh, base, n, nacc, lane);
@@ -1516,7 +1566,7 @@ gcmc_status engine_sm_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cu
                      "close %.0f\n",
                      d[0] / r, d[1] / r, d[2] / r, d[3] / r, d[4] / r, d[5] / r, d[6] / r, d[7] / r, d[8] / r);
       if (diag && cudaMemcpy(d, diag, sizeof d, cudaMemcpyDeviceToHost) == cudaSuccess)
-        std::fprintf(stderr, "[engine_sm] eval_pair steps (sum of max per call): setup %.0f window %.0f sum %.0f offsets %.0f store %.0f; commits/round %.2f ordered %.2f\n",
+        std::fprintf(stderr, "[engine_sm] steps (-DGCMC_SM_STEPS: commit_loads loads / forwarding / order / full order / store): %.0f %.0f %.0f %.0f %.0f; commits/round %.2f ordered %.2f\n",
                      d[9] / r, d[10] / r, d[11] / r, d[12] / r, d[13] / r, d[15] / r, d[14] / r);
     }
   }
