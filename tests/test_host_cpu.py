@@ -32,6 +32,36 @@ def test_library_exports_every_declared_symbol():
     assert lib.gcmc_version().decode().startswith("gcmc_b200")
 
 
+def test_abi_struct_layouts_match_the_header(tmp_path):
+    """ctypes mirrors of the C ABI structs (_lib.py) have the header's sizes
+    and field offsets (compiled here with gcc against include/gcmc_b200.h)."""
+    import shutil
+    import subprocess
+
+    from paper_1408_3764_b200 import _lib as L
+
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    structs = {"gcmc_params": L.GcmcParams, "gcmc_state": L.GcmcState,
+               "gcmc_run_result": L.GcmcRunResult}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "gcmc_b200.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for f in cls._fields_:
+            lines.append(f'  printf("{name} {f[0]} %zu\\n", offsetof({name}, {f[0].rstrip("_")}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for name, cls in structs.items():
+        assert got[(name, "size")] == C.sizeof(cls), name
+        for f in cls._fields_:
+            assert got[(name, f[0])] == getattr(cls, f[0]).offset, (name, f[0])
+
+
 def test_library_is_sm100a_cubin():
     so = os.path.join(ROOT, "paper_1408_3764_b200", "libgcmc_b200.so")
     import subprocess
