@@ -412,7 +412,7 @@ gcmc_status gcmc_create(const gcmc_params* params, int device, gcmc_dev** out) {
   // Engine shape (engine.cu): one persistent CTA per SM, 1 sequencer + evaluators.
   c->engine_group = P.engine_group == 128 || P.engine_group == 512 ? P.engine_group : 256;
   c->engine2_group = P.engine_group == 256 || P.engine_group == 512 ? P.engine_group : 128;
-  if (const char* eg = std::getenv("GCMC_ENGINE_GROUP")) {  // experiments
+  if (const char* eg = knob("GCMC_ENGINE_GROUP")) {  // experiments
     const int v = std::atoi(eg);
     if (v == 128 || v == 256 || v == 512) c->engine_group = c->engine2_group = v;
   }

@@ -436,7 +436,7 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   }
   cudaEventRecord(c.ev_e[1], s);
   // the image-shift prefilter needs cells >= r_cut (t >= 3 forced otherwise)
-  static const bool rint_form = std::getenv("GCMC_ENERGY_RINT") != nullptr;  // A/B
+  static const bool rint_form = knob("GCMC_ENERGY_RINT") != nullptr;  // A/B
   if (l / t >= rc && !rint_form)
     k_energy<true><<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
                                                                pu, pw, overlap);

@@ -1471,9 +1471,9 @@ gcmc_status engine_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cudaS
   a.bias0 = c.engine_bias;
   a.nvar = c.engine_variants;
   {
-    const char* e = std::getenv("GCMC_POLL_NS");
+    const char* e = knob("GCMC_POLL_NS");
     a.poll_ns = e ? (unsigned)std::atoi(e) : 64u;
-    const char* f = std::getenv("GCMC_EPOLL_NS");
+    const char* f = knob("GCMC_EPOLL_NS");
     a.epoll_ns = f ? (unsigned)std::atoi(f) : 64u;
   }
   size_t eval_bytes = T == 128 ? sizeof(EvalShared<128>) : (T == 256 ? sizeof(EvalShared<256>) : sizeof(EvalShared<512>));

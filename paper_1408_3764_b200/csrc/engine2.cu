@@ -2091,7 +2091,7 @@ __global__ void k_ediff(const double2* a, const double2* b, uint64_t n, unsigned
 
 bool engine2_supported(const Chain& c) {
   if (c.params.engine_mode == 1) return false;
-  if (std::getenv("GCMC_ENGINE_V1")) return false;
+  if (knob("GCMC_ENGINE_V1")) return false;
   if (c.params.max_displacement > 0.0) return false;
   const int mg = kThreads / c.engine2_group;
   return (c.engine2_ctas - 1) * mg > 8 + 1 + 8 && (c.engine2_ctas - 1) * mg <= kMaxSlots;
@@ -2200,7 +2200,7 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
                                                    : std::max(8, std::min(kMaxAcc, a.nslots / 4));
   a.fitmax = a.nslots - a.max_acc - 1 < kMaxMoves ? a.nslots - a.max_acc - 1 : kMaxMoves;  // + committer
   {
-    const char* f = std::getenv("GCMC_FITMAX");
+    const char* f = knob("GCMC_FITMAX");
     if (f && std::atoi(f) > 0 && std::atoi(f) < a.fitmax) a.fitmax = std::atoi(f);
   }
   if (!c.eng2_buf) {
@@ -2223,11 +2223,11 @@ gcmc_status engine2_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cuda
   p += kFlagWords * 8;
   a.ebig = reinterpret_cast<double4*>(p);
   {
-    const char* e1 = std::getenv("GCMC_POLL_NS");
+    const char* e1 = knob("GCMC_POLL_NS");
     a.poll_ns = e1 ? (unsigned)std::atoi(e1) : 64u;
-    const char* e2 = std::getenv("GCMC_EPOLL_NS");
+    const char* e2 = knob("GCMC_EPOLL_NS");
     a.epoll_ns = e2 ? (unsigned)std::atoi(e2) : 64u;
-    const char* e3 = std::getenv("GCMC_WALK_REPS");
+    const char* e3 = knob("GCMC_WALK_REPS");
     a.walk_reps = e3 && std::atoi(e3) > 1 ? std::atoi(e3) : 1;
 
   }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -69,6 +70,18 @@ struct Chain {
   unsigned long long* prof = nullptr;
   unsigned long long* stamp = nullptr;  // per-round global timestamps (GCMC_ENGINE_LATENCY=1)
 };
+
+// Experiment knobs (A/B timing of engine variants, tools/build_variant.py
+// NAME -DGCMC_EXPERIMENTS): read from the environment only in that build; the
+// product library ignores them.
+inline const char* knob(const char* name) {
+#ifdef GCMC_EXPERIMENTS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // Thread-local error plumbing (api.cu).
 gcmc_status set_error(gcmc_status s, const std::string& msg);

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Phase-timer profile of the default engine shape at the bench window
-# (needs: python tools/build_variant.py prof -DGCMC_PHASE_TIMERS).
+# (needs: python tools/build_variant.py prof -DGCMC_PHASE_TIMERS -DGCMC_EXPERIMENTS).
 # usage: bash tools/gpu_phase.sh TAG [extra env assignments...]
 O=gpurun_out/$1; mkdir -p $O; shift
 for rep in 1; do
