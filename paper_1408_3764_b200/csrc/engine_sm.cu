@@ -778,6 +778,16 @@ __device__ __forceinline__ int warp_window(const SmArgs& a, SWs& ws, int at, dou
 template <bool kImg>
 __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const uint8_t* occ_s,
                                             uint64_t base, int k, int warp, int lane) {
+  unsigned long long tq = clock64();
+  auto step = [&](int q) {
+#ifdef GCMC_SM_STEPS
+    const unsigned long long t = clock64();
+    if (lane == 0) atomicMax(&sh.rmax[q], t - tq);
+    tq = t;
+#else
+    (void)q;
+#endif
+  };
   SWs& ws = sh.ws[warp][0];
   auto& S = sh.stash[warp];
   const WalkRes& W = sh.wr[0];
@@ -795,8 +805,10 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
   if (kind != 1) nent = warp_window(a, ws, 0, ox, oy, oz, kNoMask, 0u, lane);
   const int nent0 = nent;
   if (kind != 2) nent += warp_window(a, ws, nent, pr.x, pr.y, pr.z, pr.wmask, pr.bpt, lane);
+  step(9);
   win_finish_s(a.m, ws, occ_s, nent, nent0, lane);
   __syncwarp();
+  step(10);
   const int total = ws.total;
   if (lane == 0) atomicAdd(&sh.pairs, (unsigned long long)total);
   int nst = 0;  // stash entries (warp-uniform)
@@ -858,12 +870,14 @@ __device__ __noinline__ void energy_updates(const SmArgs& a, SmShared& sh, const
       nst += __popc(lm);
     }
   }
+  step(11);
   __syncwarp();  // the old-window updates happen-before the new-window ones
   if (nst <= kStash) {
     for (int q = lane; q < nst; q += 32) {
       atomicAdd(&a.ep[S.id[q]].x, S.u[q]);
       atomicAdd(&a.ep[S.id[q]].y, S.w[q]);
     }
+    step(12);
   } else {  // rare (a very dense window): the new window again, applied directly
 #pragma unroll 1
     for (int f = lane; f < total; f += 32) {
@@ -909,7 +923,7 @@ __device__ __noinline__ void commit_loads(const SmArgs& a, SmShared& sh, uint64_
                                           int nacc, int lane) {
   unsigned long long tq = clock64();
   auto step = [&](int k) {
-#ifdef GCMC_SM_STEPS
+#ifdef GCMC_SM_CL_STEPS
     const unsigned long long t = clock64();
     if (lane == 0) atomicMax(&sh.rmax[k], t - tq);
     tq = t;
@@ -1566,7 +1580,7 @@ gcmc_status engine_sm_run(Chain& c, uint64_t nmoves, gcmc_trace_rec* trace_d, cu
                      "close %.0f\n",
                      d[0] / r, d[1] / r, d[2] / r, d[3] / r, d[4] / r, d[5] / r, d[6] / r, d[7] / r, d[8] / r);
       if (diag && cudaMemcpy(d, diag, sizeof d, cudaMemcpyDeviceToHost) == cudaSuccess)
-        std::fprintf(stderr, "[engine_sm] steps (-DGCMC_SM_STEPS: commit_loads loads / forwarding / order / full order / store): %.0f %.0f %.0f %.0f %.0f; commits/round %.2f ordered %.2f\n",
+        std::fprintf(stderr, "[engine_sm] steps (diagnostics build: -DGCMC_SM_STEPS energy updates: windows / occupancies+expansion / gather / stash; -DGCMC_SM_CL_STEPS commit loads): %.0f %.0f %.0f %.0f %.0f; commits/round %.2f ordered %.2f\n",
                      d[9] / r, d[10] / r, d[11] / r, d[12] / r, d[13] / r, d[15] / r, d[14] / r);
     }
   }
