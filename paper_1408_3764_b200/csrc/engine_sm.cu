@@ -66,7 +66,10 @@ constexpr int kCW = kSW - 2;        // warp loading / storing the structural com
 constexpr int kXW = kSW - 1;        // warp: proposal ring, statistics, trace
 constexpr int kStash = 48;          // new-window updates buffered per e-update warp
 constexpr int kSCand = 384;         // window candidates expanded per workspace (beyond: searched)
-constexpr double kSHuge = 1e4;      // |pair(n, x_pid)| above this: re-sum without pid
+constexpr double kSHuge = 1e4;
+#ifndef GCMC_SM_UNROLL
+#define GCMC_SM_UNROLL 4  // window candidates per lane in flight (evaluation)
+#endif      // |pair(n, x_pid)| above this: re-sum without pid
 
 struct SmArgs {
   Grid g;
@@ -364,7 +367,7 @@ __device__ __forceinline__ void half_window(const SmArgs& a, SWs& ws, const uint
   __syncwarp();
 }
 
-template <bool kImg>
+template <bool kImg, int U>
 __device__ __forceinline__ void half_sum_t(const Mirror& m, const Box& b, const SWs& ws, double px, double py,
                                            double pz, int excl, bool on, int hl, double& su, double& sw) {
   su = 0.0;
@@ -372,12 +375,12 @@ __device__ __forceinline__ void half_sum_t(const Mirror& m, const Box& b, const 
   const int total = on ? ws.total : 0;
   const int tmax = max(total, __shfl_xor_sync(0xffffffffu, total, 16));
 #pragma unroll 1
-  for (int base = 0; base < tmax; base += 64) {
-    double rx[4], ry[4], rz[4];
-    bool ok[4];
-    int ent[4];
+  for (int base = 0; base < tmax; base += 16 * U) {
+    double rx[U], ry[U], rz[U];
+    bool ok[U];
+    int ent[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int f = base + 16 * u + hl;
       ok[u] = f < total;
       rx[u] = ry[u] = rz[u] = 0.0;
@@ -395,9 +398,9 @@ __device__ __forceinline__ void half_sum_t(const Mirror& m, const Box& b, const 
     }
     // branch-free: the four pair chains interleave (a term outside r_c adds
     // +0.0, which leaves the sum's bits unchanged)
-    double pu[4], pw[4];
+    double pu[U], pw[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const double r2 = kImg ? image_dist2(px, py, pz, rx[u], ry[u], rz[u], ws.sc[ent[u]], b.l)
                              : min_image_dist2(px, py, pz, rx[u], ry[u], rz[u], b);
       const bool in = ok[u] && r2 <= b.rc2;
@@ -407,7 +410,7 @@ __device__ __forceinline__ void half_sum_t(const Mirror& m, const Box& b, const 
       pw[u] = in ? tw : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       su = __dadd_rn(su, pu[u]);
       sw = __dadd_rn(sw, pw[u]);
     }
@@ -425,9 +428,9 @@ __device__ __forceinline__ void half_sum_t(const Mirror& m, const Box& b, const 
 __device__ __forceinline__ void half_sum(const Mirror& m, const Box& b, const SWs& ws, double px, double py,
                                          double pz, int excl, bool on, int hl, double& su, double& sw) {
   if (m.dims >= 5)
-    half_sum_t<true>(m, b, ws, px, py, pz, excl, on, hl, su, sw);
+    half_sum_t<true, GCMC_SM_UNROLL>(m, b, ws, px, py, pz, excl, on, hl, su, sw);
   else
-    half_sum_t<false>(m, b, ws, px, py, pz, excl, on, hl, su, sw);
+    half_sum_t<false, GCMC_SM_UNROLL>(m, b, ws, px, py, pz, excl, on, hl, su, sw);
 }
 
 // Two slots per warp call: half hw evaluates slot s0 + kSW * hw.
