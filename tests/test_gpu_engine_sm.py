@@ -135,3 +135,36 @@ def test_sm_engine_sampling_tail_and_equilibration():
     assert st.samples == rs.samples and st.sum_n == rs.sum_n and st.sum_n2 == rs.sum_n2
     assert abs(st.sum_u - rs.sum_u) <= 1e-9 * max(1.0, abs(rs.sum_u))
     assert abs(st.sum_p - rs.sum_p) <= 1e-9 * max(1.0, abs(rs.sum_p))
+
+
+@pytest.mark.parametrize("engine_mode", [0, 2])
+def test_engine_cell_overflow_like_the_reference(engine_mode):
+    """An accepted insertion into a full reference cell (microcell capacity 2,
+    mu = +4 at 400 particles) ends the run with the reference's error at the
+    same move (cell_grid / microcell_grid insert_id: runtime_error), on both
+    engines; everything before it is committed and identical."""
+    from paper_1408_3764_b200 import _lib
+
+    import oracle as O
+
+    n0 = 400
+    box = (n0 / 0.5) ** (1.0 / 3.0)
+    xyz, rng = E().random_initial_configuration(n0, box, 0.85, 1)
+    cfg = RC()(temperature=2.0, chemical_potential=4.0, box_length=box, strategy="microcell",
+               microcell_capacity=2)
+    sim = E().Simulation(cfg, xyz, rng, engine_mode=engine_mode)
+    with pytest.raises(_lib.GcmcError) as ei:
+        sim.run(20000)
+    assert ei.value.status == "CELL_OVERFLOW"
+    msg = str(ei.value)
+    assert "microcell: cell" in msg and "exceeds capacity 2" in msg
+    st = sim.dev.get_state()
+    if use_ref():
+        ref = O.RefSim(O.ref_config(box_length=box, strategy="microcell", temperature=2.0,
+                                    chemical_potential=4.0, microcell_capacity=2),
+                       mode=2, xyz=xyz, rng_hex=rng.serialize_hex(), step=0, energy=0.0, virial=0.0)
+        with pytest.raises(O.RefError) as er:
+            ref.run(20000)
+        assert str(er.value).split("microcell: ")[-1] in msg
+        assert st.step == ref.state().step
+    sim.close()
