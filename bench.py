@@ -334,7 +334,10 @@ def cpu_baseline(s0s, s1s, a, box, mus):
 
     timed = a.cpu_steps * a.moves_per_step
     model, ncpu = host_cpu()
-    k = len(s0s)
+    # one reference chain per host core: with more GPU chains than cores, the
+    # first ncpu chains (the host's full throughput, bounded CPU time)
+    k = min(len(s0s), ncpu or 1)
+    s0s, s1s, mus = s0s[:k], (s1s[:k] if s1s is not None else None), mus[:k]
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=min(k, ncpu or 1)) as ex:  # ctypes calls drop the GIL
         res = list(ex.map(lambda c: cpu_chain(s0s[c], s1s[c], a, box, mus[c]), range(k)))
@@ -347,7 +350,7 @@ def cpu_baseline(s0s, s1s, a, box, mus):
     s0 = s0s[0]
     return ({"value": k * timed / wall, "unit": "moves/s", "cores": min(k, ncpu or 1),
              "kind": kind,
-             "sample": f"moves {s0['step']}..{s0['step'] + timed} of each of the {k} chain(s) (the "
+             "sample": f"moves {s0['step']}..{s0['step'] + timed} of each of the first {k} chain(s) (the "
                        f"first {a.cpu_steps} of the {a.steps} timed GPU steps), reference "
                        f"Simulation::step loop resumed from each GPU chain's state there, "
                        f"{wall:.2f} s wall, {min(k, ncpu or 1)} thread(s) on host '{model}' "
