@@ -58,7 +58,10 @@ constexpr int kSW = kST / 32;       // warps
 constexpr int kSM = 64;             // move slots per round
 constexpr int kSAhead = 2 * kSM;    // proposals loaded ahead of the round
 constexpr int kSRing = 4 * kSM;     // proposal ring (a refill never reaches the current round)
-constexpr int kSAcc = 24;           // accepted moves per round (at most)
+#ifndef GCMC_SM_ACC
+#define GCMC_SM_ACC 24
+#endif
+constexpr int kSAcc = GCMC_SM_ACC;  // accepted moves per round (at most)
 constexpr int kSOff = 16;           // N offsets per slot: d = -8..7 <-> half-warp lane d + 8
 constexpr int kSHalf = kSOff / 2;
 constexpr int kEW = kSW - 2;        // warps applying neighbour energy updates
