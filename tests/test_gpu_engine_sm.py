@@ -34,10 +34,12 @@ def sm_pair(strategy, n0, mu, seed=1, **kw):
 
 @pytest.mark.parametrize("strategy", ["microcell", "cell_list"])
 @pytest.mark.parametrize("n0,mu,chunks", [(2048, 1.0, 5), (2048, -2.0, 5), (32768, 1.0, 4),
-                                          (65536, -3.0, 4)])
+                                          (65536, -3.0, 4), (1 << 20, 1.0, 2)])
 def test_sm_engine_trace_state_and_grid(strategy, n0, mu, chunks):
     """Trace parity, full state and the byte-identical reference grid after
-    every chunk (2k dense / dilute, 32k, and the 64k sweep's mu = -3)."""
+    every chunk (2k dense / dilute, 32k, the 64k sweep's mu = -3, and 1M,
+    where the mirror occupancies are read from global memory: no shared
+    replica fits)."""
     sim, o, st0 = sm_pair(strategy, n0, mu)
     acc = 0
     for k in range(chunks):
