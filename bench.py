@@ -564,7 +564,9 @@ def main():
             "clocks": clk.summary(),
             # per step, chain and 2^21-move chunk (gcmc_run_moves): the engine
             # plus the look-ahead proposal generation (k_gen2, k_annotate)
-            "gpu_launches": (a.steps * launches * (1 + 2 * K) if sm_engine and K > 1
+            # per step and 2^21-move chunk: K > 1 chain-per-SM chains go out as one
+            # generator, one annotate and one engine launch for all chains
+            "gpu_launches": (3 * a.steps * launches if sm_engine and K > 1
                              else 3 * a.steps * K * launches),
             "engine": {1: "per-window (engine.cu)", 2: "multi-SM maintained-energy (engine2.cu)",
                        3: "chain-per-SM (engine_sm.cu)"}.get(engine_used[0], "?"),
