@@ -232,6 +232,151 @@ __global__ void __launch_bounds__(kEWarps * 32)
   }
 }
 
+// The image-shift pass with the FP32 prefilter on paired lanes of Blackwell's
+// packed FP32 pipe (FADD2 / FMUL2 / FFMA2): each lane tests two candidates
+// against an own particle per instruction stream, 64 candidates per chunk and
+// one vote pair per own particle. Same pair set and the same rounding of the
+// prefilter r^2 as k_energy<true>; survivors are queued and evaluated exactly
+// 32 at a time in (own, chunk half, lane) order.
+__global__ void __launch_bounds__(kEWarps * 32)
+    k_energy_pk(EGrid eg, Box b, Prefilter pf, const int* __restrict__ start,
+                const int* __restrict__ count, const double4* __restrict__ rec,
+                const float4* __restrict__ recf, double* part_u, double* part_w,
+                unsigned long long* overlap) {
+  __shared__ double4 own_s[kEWarps][kOwnMax];
+  __shared__ float4 ownf_s[kEWarps][kOwnMax];
+  __shared__ int cand_s[kEWarps][kECand];
+  __shared__ int queue_s[kEWarps][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t c = blockIdx.x * (uint64_t)kEWarps + warp;
+  if (c >= eg.ncells) return;
+  const int d = eg.dims;
+  const int cx = (int)(c % d), cy = (int)((c / d) % d), cz = (int)(c / ((uint64_t)d * d));
+  int ncnt = 0, nstart = 0, scode = 21;
+  if (lane < 14) {
+    const int t = 13 + lane;
+    const int ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
+    const int rx = cx + ox, ry = cy + oy, rz = cz + oz;
+    const int nx = (rx + d) % d, ny = (ry + d) % d, nz = (rz + d) % d;
+    const int nc = nx + d * (ny + d * nz);
+    scode = (rx < 0 ? 0 : (rx >= d ? 2 : 1)) | (ry < 0 ? 0 : (ry >= d ? 2 : 1)) << 2 |
+            (rz < 0 ? 0 : (rz >= d ? 2 : 1)) << 4;
+    ncnt = count[nc];
+    nstart = start[nc];
+  }
+  int incl = ncnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 13);
+  const int own_start = __shfl_sync(0xffffffffu, nstart, 0);
+  const int own_n = __shfl_sync(0xffffffffu, ncnt, 0);
+  Kahan ku = {0, 0}, kw = {0, 0};
+  auto exact = [&](int pk) {
+    const double4 p = own_s[warp][pk & 63];
+    const double4 q = rec[(unsigned)pk >> 6];
+    const double r2 = min_image_dist2(p.x, p.y, p.z, q.x, q.y, q.z, b);
+    if (r2 <= b.rc2) {
+      if (r2 < __dmul_rn(1e-12, b.sigma2)) {
+        long long iid = bits_pid(p.w), jid = bits_pid(q.w);
+        if (iid > jid) {
+          const long long t2 = iid;
+          iid = jid;
+          jid = t2;
+        }
+        atomicMin(overlap, ((unsigned long long)iid << 32) | (unsigned long long)jid);
+      } else {
+        double u, w;
+        lj_pair_clamped(r2, b, u, w);
+        ku.add(u);
+        kw.add(w);
+      }
+    }
+  };
+  const float cut2 = pf.on ? pf.cut2 : __int_as_float(0x7f800000);
+  for (int ob = 0; ob < own_n; ob += kOwnMax) {
+    const int on = min(kOwnMax, own_n - ob);
+    for (int i = lane; i < on; i += 32) {
+      own_s[warp][i] = rec[own_start + ob + i];
+      ownf_s[warp][i] = recf[own_start + ob + i];
+    }
+    for (int cb = 0; cb < total; cb += kECand) {
+      __syncwarp();
+      {
+        const int e0 = incl - ncnt;
+        for (int k = 0; k < ncnt; ++k) {
+          const int f = e0 + k - cb;
+          if (f >= 0 && f < kECand) cand_s[warp][f] = ((nstart + k) << 6) | scode;
+        }
+      }
+      __syncwarp();
+      const int ctot = min(kECand, total - cb);
+      int qn = 0;
+      for (int t0 = 0; t0 < ctot; t0 += 64) {
+        int qi[2], lim[2];
+        float2 nqx, nqy, nqz;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int t = t0 + 32 * hh + lane;
+          const bool have = t < ctot;
+          const int ce = have ? cand_s[warp][t] : 0;
+          qi[hh] = ce >> 6;
+          float4 qf = have ? recf[qi[hh]] : make_float4(0, 0, 0, 0);
+          qf.x += (float)((ce & 3) - 1) * pf.l;
+          qf.y += (float)(((ce >> 2) & 3) - 1) * pf.l;
+          qf.z += (float)(((ce >> 4) & 3) - 1) * pf.l;
+          if (hh == 0) {
+            nqx.x = -qf.x;
+            nqy.x = -qf.y;
+            nqz.x = -qf.z;
+          } else {
+            nqx.y = -qf.x;
+            nqy.y = -qf.y;
+            nqz.y = -qf.z;
+          }
+          lim[hh] = !have ? 0 : (cb + t < own_n ? cb + t - ob : on);
+        }
+        for (int i = 0; i < on; ++i) {
+          const float4 pff = ownf_s[warp][i];
+          const float2 dx = __fadd2_rn(make_float2(pff.x, pff.x), nqx);
+          const float2 dy = __fadd2_rn(make_float2(pff.y, pff.y), nqy);
+          const float2 dz = __fadd2_rn(make_float2(pff.z, pff.z), nqz);
+          const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+          const bool pa = i < lim[0] && r2.x <= cut2, pb = i < lim[1] && r2.y <= cut2;
+          const unsigned ma = __ballot_sync(0xffffffffu, pa), mb = __ballot_sync(0xffffffffu, pb);
+          if (ma | mb) {
+            const unsigned below = (1u << lane) - 1u;
+            if (pa) queue_s[warp][qn + __popc(ma & below)] = (qi[0] << 6) | i;
+            if (pb) queue_s[warp][qn + __popc(ma) + __popc(mb & below)] = (qi[1] << 6) | i;
+            qn += __popc(ma) + __popc(mb);
+            __syncwarp();
+            while (qn >= 32) {
+              exact(queue_s[warp][lane]);
+              qn -= 32;
+              const int c0 = queue_s[warp][32 + lane], c1 = queue_s[warp][64 + lane];
+              __syncwarp();
+              if (lane < qn) queue_s[warp][lane] = c0;
+              if (32 + lane < qn) queue_s[warp][32 + lane] = c1;
+              __syncwarp();
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < qn) exact(queue_s[warp][lane]);
+      __syncwarp();
+    }
+    __syncwarp();
+  }
+  const double su = warp_sum_comp(ku), sw = warp_sum_comp(kw);
+  if (lane == 0) {
+    part_u[c] = su;
+    part_w[c] = sw;
+  }
+}
+
 // Deterministic final reduction over the per-cell partials.
 // Deterministic reduction of n partials (u, w): block b sums its contiguous
 // chunk (Kahan per thread + compensated trees) into ou[b], ow[b]. Used twice:
@@ -437,7 +582,11 @@ gcmc_status total_energy(Chain& c, double* u, double* w) {
   cudaEventRecord(c.ev_e[1], s);
   // the image-shift prefilter needs cells >= r_cut (t >= 3 forced otherwise)
   static const bool rint_form = knob("GCMC_ENERGY_RINT") != nullptr;  // A/B
-  if (l / t >= rc && !rint_form)
+  static const bool scalar_form = knob("GCMC_ENERGY_SCALAR") != nullptr;  // A/B
+  if (l / t >= rc && !rint_form && !scalar_form)
+    k_energy_pk<<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
+                                                            pu, pw, overlap);
+  else if (l / t >= rc && !rint_form)
     k_energy<true><<<blocks(nc, kEWarps), kEWarps * 32, 0, s>>>(eg, c.box, pf, start, count, rec, recf,
                                                                pu, pw, overlap);
   else
