@@ -28,11 +28,16 @@
 //             (old window first, then new; the round's accepted moves are
 //             > 2 r_c apart so the sets are disjoint) with fire-and-forget
 //             atomics, while one warp loads the structural commits
-//             (commit.cuh) and one refills the proposal ring and accumulates
-//             the statistics / trace; after a barrier the structural stores
-//             (commits that touch an earlier commit of the round are
-//             re-loaded and applied after it, in move order) and the movers'
-//             e (in move order).
+//             (commit.cuh; the movers' records were fetched during the
+//             verify) and orders them, and one refills the proposal ring and
+//             accumulates the statistics / trace; after a barrier the
+//             structural stores (a deletion relabelling a particle inserted
+//             earlier in the round takes its data from that insertion;
+//             commits that touch an earlier one are re-loaded and applied
+//             after it, in move order) and the movers' e (in move order).
+//
+// Windows use the brick's known periodic image (dims >= 5) instead of
+// box.hpp's rint, with the same operations and roundings.
 //
 // The chain is the reference's: the same proposals (gen.cu), the same
 // acceptance arithmetic and order, the same grid and mirror commits
