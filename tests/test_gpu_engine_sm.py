@@ -196,3 +196,67 @@ def test_sm_engine_filling_a_dilute_box(strategy):
     du, dw = sim.dev.energy_drift()
     assert du <= 1e-9 and dw <= 1e-8, (du, dw)
     sim.close()
+
+
+def _ideal_gas_pair(engine_mode, **kw):
+    box, xyz, rng = config(2048)
+    cfg = RC()(temperature=2.0, chemical_potential=3.0, box_length=box, strategy="cell_list",
+               epsilon=0.0)
+    sim = E().Simulation(cfg, xyz, rng, engine_mode=engine_mode, **kw)
+    st = sim.dev.get_state()
+    o = oracle_sim("cell_list", box, xyz, rng.serialize_hex(), st.energy, st.virial,
+                   temperature=2.0, chemical_potential=3.0, epsilon=0.0)
+    return sim, o, st
+
+
+@pytest.mark.parametrize("engine_mode", [0, 2])
+def test_mirror_growth_then_reference_overflow(engine_mode):
+    """epsilon = 0 at mu = +3: an ideal gas that fills the box. The brick
+    mirror (32 records per brick) overflows first — the engine doubles it and
+    continues at that move, invisibly — then the reference's cell list (48)
+    overflows: the same error at the same move (T/test_engine.cpp:143-158's
+    epsilon = 0 case; cell_grid.hpp insert_id)."""
+    from paper_1408_3764_b200 import _lib
+
+    sim, o, st0 = _ideal_gas_pair(engine_mode)
+    failed = False
+    for k in range(20):
+        try:
+            tr = sim.run(1000, trace=True)
+        except _lib.GcmcError as e:
+            assert e.status == "CELL_OVERFLOW" and "exceeds capacity 48" in str(e)
+            with pytest.raises(Exception) as er:
+                o.run(1000, trace=True)
+            assert "exceeds capacity 48" in str(er.value)
+            assert sim.dev.get_state().step == o.state().step
+            failed = True
+            break
+        _, tp = o.run(1000, trace=True)
+        assert_trace_parity(tr, tp)
+        assert_full_state(sim, o, st0)
+        peak = sim.peak_cell_occupancy()
+    assert failed
+    # cells and bricks partition this box alike (5^3 of side L/5 >= r_c): a
+    # cell past 32 means the mirror grew
+    assert peak > 32, peak
+    sim.close()
+
+
+def test_mirror_growth_in_a_batched_launch():
+    """The same ideal gas as two chain-per-SM chains in one launch: a chain
+    whose mirror overflows mid-chunk finishes the chunk on its own launches
+    (grown mirror); both stay the reference's chain up to the overflow."""
+    from paper_1408_3764_b200 import _lib
+
+    pairs = [_ideal_gas_pair(2, engine_share=2) for _ in range(2)]
+    sims = [p[0] for p in pairs]
+    for k in range(6):
+        E().run_chains(sims, 1000)
+        for sim, o, st0 in pairs:
+            o.run(1000)
+            assert_full_state(sim, o, st0)
+    assert all(s.peak_cell_occupancy() > 32 for s in sims)  # past the mirror's 32 per brick
+    with pytest.raises(_lib.GcmcError):
+        E().run_chains(sims, 4000)
+    for s in sims:
+        s.close()
