@@ -173,20 +173,23 @@ def test_engine_cell_overflow_like_the_reference(engine_mode):
 
 
 @pytest.mark.parametrize("strategy", ["microcell", "cell_list"])
-def test_sm_engine_filling_a_dilute_box(strategy):
+@pytest.mark.parametrize("engine_mode", [0, 2])
+def test_sm_engine_filling_a_dilute_box(strategy, engine_mode):
     """mu = +6 from density 0.1: nearly every insertion is accepted, so rounds
     end at the N-offset range (d = +8) or at max_acc and almost every commit
     is an insertion (index chains, forwarded relabels when a deletion follows);
-    trace, state and grid bytes stay the reference's."""
+    the store starts at 4096 + 64 particles and grows with N (store
+    reallocation between launches). Trace, state and grid bytes stay the
+    reference's, on both maintained-energy engines."""
     box, xyz, rng = config(4096, seed=7, density=0.1)
     cfg = RC()(temperature=2.0, chemical_potential=6.0, box_length=box, strategy=strategy, seed=7)
-    sim = E().Simulation(cfg, xyz, rng, engine_mode=2)
+    sim = E().Simulation(cfg, xyz, rng, engine_mode=engine_mode, max_particles=4096 + 64)
     st0 = sim.dev.get_state()
     o = oracle_sim(strategy, box, xyz, rng.serialize_hex(), st0.energy, st0.virial,
                    temperature=2.0, chemical_potential=6.0)
     for k in range(3):
         tr = sim.run(10000, trace=True)
-        assert sim.last_run.engine == 3
+        assert sim.last_run.engine == (3 if engine_mode == 2 else 2)
         _, tp = o.run(10000, trace=True)
         assert_trace_parity(tr, tp)
         assert_full_state(sim, o, st0)
