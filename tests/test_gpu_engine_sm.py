@@ -263,3 +263,30 @@ def test_mirror_growth_in_a_batched_launch():
         E().run_chains(sims, 4000)
     for s in sims:
         s.close()
+
+
+def test_batched_chains_of_different_shapes():
+    """One launch over chains with different strategies, box sizes and state
+    points (the shared-memory plan takes the largest replica): each chain is
+    its own reference chain."""
+    specs = [("microcell", 2048, -2.0, 11), ("cell_list", 32768, 1.0, 12), ("microcell", 65536, -3.0, 13)]
+    sims, refs, st0 = [], [], []
+    for strategy, n0, mu, seed in specs:
+        box, xyz, rng = config(n0, seed=seed)
+        cfg = RC()(temperature=2.0, chemical_potential=mu, box_length=box, strategy=strategy, seed=seed)
+        sim = E().Simulation(cfg, xyz, rng, engine_mode=2)
+        st = sim.dev.get_state()
+        sims.append(sim)
+        st0.append(st)
+        refs.append(oracle_sim(strategy, box, xyz, rng.serialize_hex(), st.energy, st.virial,
+                               temperature=2.0, chemical_potential=mu))
+    for rep in range(2):
+        res = E().run_chains(sims, [15000, 20000, 25000])
+        assert all(r.engine == 3 for r in res)
+        for c, (sim, o) in enumerate(zip(sims, refs)):
+            o.run([15000, 20000, 25000][c])
+            assert_full_state(sim, o, st0[c])
+            if use_ref():
+                assert_same_grid(sim, o, f"chain {c} rep {rep}")
+    for s in sims:
+        s.close()
